@@ -1,0 +1,344 @@
+#!/usr/bin/env python
+"""Benchmark of the per-Newton-iteration reassembly (BASELINE.json metric:
+"element-matrix entries assembled/s (FP64, into CSR) and % of HBM roofline").
+
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--config C2] [--impl ours|reference]
+
+A step = one reassembly (fea_reassemble: [allgather u] + the fused kernel) of every matrix the
+config names, with a fresh u (u_r = u_{r-1} + 0.01 xi_r, reading 14), inputs resident in HBM.
+Entries per step = n_e * n_p^2 * (#matrices).  L2 is flushed (256 MiB write)
+before every timed step, outside the timed region.  Per-step device time from CUDA events on
+the launching stream; the K steps are bracketed by barrier + synchronize; max over ranks.
+Rank 0 prints one JSON line.  --impl reference times the CPU oracle (the reference arm of this
+tier) on the host cores on a bounded sample of the same workload.
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import statistics
+import sys
+import threading
+import time
+
+import numpy as np
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+from fea_inputs import CONFIGS, MASS, STIFF, make_workload  # noqa: E402
+
+METRIC = "element-matrix entries assembled/s (FP64, into CSR) and % of HBM roofline"
+UNIT = "entries/s"
+DEFAULT_CONFIG = "C2"  # BASELINE.json configs[1]
+
+
+def canonical_bytes(n_v, n_e, n_p, n_dof, nnz, nmat):
+    """Algorithmic bytes per reassembly (exactly the north_star list):
+    coords 16 n_v + DOF map 4 n_p n_e + u 8 n_dof + scatter map 4 n_p^2 n_e + CSR 8 nnz #mat."""
+    return 16 * n_v + 4 * n_p * n_e + 8 * n_dof + 4 * n_p * n_p * n_e + 8 * nnz * nmat
+
+
+def load_peaks():
+    p = os.path.join(ROOT, "MEASURED_PEAKS.json")
+    if os.path.exists(p):
+        with open(p) as f:
+            d = json.load(f)
+        return float(d["hbm_gbs"]), "measured (MEASURED_PEAKS.json hbm_gbs, copy read+write)"
+    return 6650.0, "fallback (B200_PROFILING.md: 6.65 TB/s)"
+
+
+class ClockSampler:
+    """nvidia-smi-equivalent clock / throttle sampling through NVML during the timed region."""
+
+    def __init__(self, device_index: int, period_s: float = 0.005):
+        self.ok = False
+        self.samples = []
+        self.reasons = set()
+        self.period = period_s
+        try:
+            import pynvml
+            pynvml.nvmlInit()
+            self.nv = pynvml
+            self.h = pynvml.nvmlDeviceGetHandleByIndex(device_index)
+            self.max_mhz = pynvml.nvmlDeviceGetMaxClockInfo(self.h, pynvml.NVML_CLOCK_SM)
+            self.ok = True
+        except Exception as e:  # pragma: no cover
+            self.err = str(e)
+        self._stop = threading.Event()
+
+    def _reason_names(self, mask):
+        nv = self.nv
+        names = {
+            "sw_power_cap": getattr(nv, "nvmlClocksEventReasonSwPowerCap", 0x4),
+            "hw_slowdown": getattr(nv, "nvmlClocksEventReasonHwSlowdown", 0x8),
+            "sw_thermal_slowdown": getattr(nv, "nvmlClocksEventReasonSwThermalSlowdown", 0x20),
+            "hw_thermal_slowdown": getattr(nv, "nvmlClocksEventReasonHwThermalSlowdown", 0x40),
+            "hw_power_brake_slowdown": getattr(nv, "nvmlClocksEventReasonHwPowerBrakeSlowdown", 0x80),
+        }
+        return [k for k, v in names.items() if mask & v]
+
+    def _run(self):
+        nv = self.nv
+        while not self._stop.is_set():
+            try:
+                self.samples.append(nv.nvmlDeviceGetClockInfo(self.h, nv.NVML_CLOCK_SM))
+                try:
+                    mask = nv.nvmlDeviceGetCurrentClocksEventReasons(self.h)
+                except Exception:
+                    mask = nv.nvmlDeviceGetCurrentClocksThrottleReasons(self.h)
+                self.reasons.update(self._reason_names(mask))
+            except Exception:
+                pass
+            time.sleep(self.period)
+
+    def __enter__(self):
+        if self.ok:
+            self.t = threading.Thread(target=self._run, daemon=True)
+            self.t.start()
+        return self
+
+    def __exit__(self, *a):
+        if self.ok:
+            self._stop.set()
+            self.t.join()
+
+    def summary(self):
+        if not self.ok or not self.samples:
+            return {"sm_mhz": None, "sm_max_mhz": getattr(self, "max_mhz", None), "reasons": sorted(self.reasons),
+                    "samples": len(self.samples)}
+        return {"sm_mhz": statistics.median(self.samples), "sm_max_mhz": self.max_mhz,
+                "reasons": sorted(self.reasons), "samples": len(self.samples)}
+
+
+def env_dist():
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    return rank, world, local
+
+
+def workload_desc(cfg, wl):
+    m = wl.mesh
+    return {"workload": f"{cfg.name}: {cfg.description}", "config_index": cfg.index, "p": cfg.p, "N": cfg.N,
+            "n_e": m.n_e, "n_dof": m.n_dof, "n_q": int(wl.q_w.shape[0]),
+            "matrices": ("M+K" if cfg.which == 3 else "M" if cfg.which == 1 else "K"),
+            "k": {0: "poly", 1: "exp"}[cfg.k_kind] + str(list(cfg.k_par)),
+            "reorder": "morton" if cfg.reorder else "none"}
+
+
+def cpu_oracle_run(wl, cfg, target_s: float, nthreads: int, lib_to_user=None):
+    """Time the oracle (Algorithm 1, as it stands) on a bounded sample: whole reassemblies of the
+    workload if one takes < target_s, else a leading block of rows.  Returns (entries/s, desc)."""
+    import oracle
+    m = wl.mesh
+    if lib_to_user is not None:  # same numbering as the GPU run
+        import copy
+        inv = np.empty_like(lib_to_user)
+        inv[lib_to_user] = np.arange(lib_to_user.shape[0])
+        m = copy.copy(m)
+        m.elem_dof = inv[m.elem_dof].astype(np.int32)
+        u = np.ascontiguousarray(wl.u0[lib_to_user])
+    else:
+        u = wl.u0
+    coef = (cfg.k_kind, tuple(cfg.k_par))
+    n_p = cfg.n_p
+    nmat = cfg.n_matrices
+    # sample rows [0, r1): grow until the estimated time reaches target_s
+    r1 = min(m.n_dof, max(1000, m.n_dof // 64))
+    while True:
+        pat = oracle.pattern(m.n_dof, m.elem_dof, 0, r1)
+        t0 = time.perf_counter()
+        oracle.assemble(m, wl.q_xy, wl.q_w, u, m_coef=coef, c_coef=coef, which=cfg.which, r0=0, r1=r1,
+                        nthreads=nthreads, pat=pat)
+        dt = time.perf_counter() - t0
+        if r1 >= m.n_dof or dt >= 0.25 * target_s:
+            break
+        r1 = min(m.n_dof, int(r1 * max(2.0, 0.5 * target_s / max(dt, 1e-3))))
+    reps = max(1, int(target_s / max(dt, 1e-6)))
+    t0 = time.perf_counter()
+    for _ in range(reps):
+        oracle.assemble(m, wl.q_xy, wl.q_w, u, m_coef=coef, c_coef=coef, which=cfg.which, r0=0, r1=r1,
+                        nthreads=nthreads, pat=pat)
+    dt = (time.perf_counter() - t0) / reps
+    # entries attributable to the sampled rows: local entries whose row lies in [0, r1)
+    ed = m.elem_dof
+    rows_in = (ed < r1).sum(axis=1)  # per element: local rows in the sample
+    entries = int(rows_in.sum()) * n_p * nmat
+    desc = (f"oracle rows [0,{r1}) of {m.n_dof} ({100.0 * r1 / m.n_dof:.1f}%), {reps} rep(s), "
+            f"pattern build excluded, {nthreads} thread(s)")
+    return entries / dt, desc, dt
+
+
+def run_reference(args):
+    """--impl reference: the CPU oracle (this tier's reference arm) on the host cores."""
+    rank, world, _ = env_dist()
+    if rank != 0:
+        return 0
+    cfg = CONFIGS[args.config]
+    wl = make_workload(cfg)
+    cores = len(os.sched_getaffinity(0))
+    step_target = float(os.environ.get("FEA_REF_STEP_S", "1.0"))
+    times = []
+    desc = ""
+    for i in range(args.warmup + args.steps):
+        rate, desc, dt = cpu_oracle_run(wl, cfg, step_target, cores)
+        if i >= args.warmup:
+            times.append(rate)
+    value = statistics.median(times)
+    ent_step = wl.mesh.n_e * cfg.n_p ** 2 * cfg.n_matrices
+    line = {"metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
+            "warmup": args.warmup, "ms_per_step": 1e3 * ent_step / value, "higher_is_better": True,
+            "scaling": "strong", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+            "impl": "reference", "config": workload_desc(cfg, wl),
+            "cpu_baseline": {"value": value, "unit": UNIT, "cores": cores, "kind": "oracle", "sample": desc},
+            "e2e": {"value": value, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
+    print(json.dumps(line), flush=True)
+    return 0
+
+
+def run_ours(args):
+    import torch
+    rank, world, local = env_dist()
+    torch.cuda.set_device(local)
+    dev = torch.device("cuda", local)
+    if world > 1:
+        import torch.distributed as dist
+        dist.init_process_group("nccl", device_id=dev)
+    from paper_2204_03893_b200 import Assembler
+    cfg = CONFIGS[args.config]
+    t_setup = time.perf_counter()
+    wl = make_workload(cfg)
+    m = wl.mesh
+    coef = (cfg.k_kind, tuple(cfg.k_par))
+    asm = Assembler(cfg.p, wl.q_xy, wl.q_w, m.vert_xy, m.elem_vert, m.n_dof, m.elem_dof, device=local,
+                    reorder=cfg.reorder, which=cfg.which, coef_m=coef, coef_c=coef, rank=rank, world=world)
+    t_setup = time.perf_counter() - t_setup
+    nmat = cfg.n_matrices
+    # distinct u per step (library numbering, owned rows), resident in HBM
+    R = max(2, min(cfg.reassemblies, 10))
+    us = []
+    for u in wl.u_sequence(R):
+        ul = asm.to_library(u)
+        us.append(torch.tensor(asm.owned_slice(ul) if world > 1 else ul, dtype=torch.float64, device=dev))
+    flush = torch.empty(256 * 1024 * 1024 // 4, dtype=torch.float32, device=dev)
+    stream = torch.cuda.current_stream(dev)
+
+    def barrier():
+        if world > 1:
+            torch.distributed.barrier()
+
+    for i in range(args.warmup):
+        asm.reassemble(us[i % R])
+    torch.cuda.synchronize()
+    ev = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)) for _ in range(args.steps)]
+    sampler = ClockSampler(local)
+    barrier()
+    torch.cuda.synchronize()
+    with sampler:
+        for i in range(args.steps):
+            flush.fill_(float(i))  # evict L2 (126 MB) before every timed step, outside the events
+            ev[i][0].record(stream)
+            asm.reassemble(us[i % R])
+            ev[i][1].record(stream)
+        torch.cuda.synchronize()
+    barrier()
+    step_ms = [a.elapsed_time(b) for a, b in ev]
+    tot = torch.tensor([sum(step_ms)], dtype=torch.float64, device=dev)
+    if world > 1:
+        torch.distributed.all_reduce(tot, op=torch.distributed.ReduceOp.MAX)
+    total_ms = float(tot.item())
+    ms_per_step = total_ms / args.steps
+    entries_step = m.n_e * cfg.n_p ** 2 * nmat
+    value = entries_step / (ms_per_step * 1e-3)
+
+    # roofline of the dominant (only) kernel: canonical bytes of this rank's share / kernel time
+    peak, peak_src = load_peaks()
+    rp, _ = asm.pattern()
+    nnz_local = asm.nnz
+    if world == 1:
+        B = canonical_bytes(m.n_v, m.n_e, cfg.n_p, m.n_dof, nnz_local, nmat)
+    else:  # per-rank share of the canonical bytes (rows owned)
+        frac_rows = asm.n_rows / m.n_dof
+        B = canonical_bytes(m.n_v, m.n_e, cfg.n_p, m.n_dof, 0, nmat) * frac_rows + 8 * nnz_local * nmat
+    kern_ms = statistics.median(step_ms)
+    achieved = B / (kern_ms * 1e-3) / 1e9
+    traffic = None
+    prof = os.path.join(ROOT, "profiles", f"ncu_traffic_{cfg.name}.json")
+    if os.path.exists(prof):
+        with open(prof) as f:
+            traffic = json.load(f).get("dram_bytes_per_launch")
+
+    # e2e: public API with host buffers (pinned), H2D of u and D2H of the values inside the timing
+    nu = m.n_dof if world == 1 else asm.n_rows
+    u_pin = torch.empty(nu, dtype=torch.float64, pin_memory=True)
+    u_pin.copy_(us[0].cpu())
+    outs = [torch.empty(max(nnz_local, 1), dtype=torch.float64, pin_memory=True) if cfg.which & b else None
+            for b in (MASS, STIFF)]
+    outs_np = [o.numpy() if o is not None else None for o in outs]
+    e2e_steps = max(3, min(args.steps, 20))
+    asm.ctx.reassemble_host(u_pin.numpy(), *outs_np)
+    barrier()
+    t0 = time.perf_counter()
+    for _ in range(e2e_steps):
+        asm.ctx.reassemble_host(u_pin.numpy(), *outs_np)
+    e2e_s = (time.perf_counter() - t0) / e2e_steps
+    tmax = torch.tensor([e2e_s], dtype=torch.float64, device=dev)
+    if world > 1:
+        torch.distributed.all_reduce(tmax, op=torch.distributed.ReduceOp.MAX)
+    e2e_s = float(tmax.item())
+
+    line = None
+    if rank == 0:
+        cpu = None
+        if world == 1 and not args.no_cpu_baseline:
+            cores = len(os.sched_getaffinity(0))
+            rate, desc, _ = cpu_oracle_run(wl, cfg, float(os.environ.get("FEA_CPU_BASELINE_S", "10")), cores,
+                                           lib_to_user=asm.lib_to_user)
+            cpu = {"value": rate, "unit": UNIT, "cores": cores, "kind": "oracle", "sample": desc}
+        desc = workload_desc(cfg, wl)
+        desc.update({"l2": "flushed (256 MiB write) before every timed step", "parallelism": f"rows{world}",
+                     "nnz": int(nnz_local) if world == 1 else None, "setup_s": round(t_setup, 3),
+                     "blocks": asm.ctx.stat(1), "elem_visits_over_owned": round(asm.ctx.stat(2) / max(1, asm.ctx.stat(3)), 4),
+                     "smem_per_cta": asm.ctx.stat(6), "grid": asm.ctx.stat(8)})
+        line = {
+            "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
+            "warmup": args.warmup, "ms_per_step": ms_per_step, "higher_is_better": True,
+            "scaling": "strong", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+            "config": desc,
+            "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
+                         "frac": achieved / peak, "traffic": traffic, "algorithmic_bytes": B,
+                         "kernel": "k_reassemble", "peak_source": peak_src,
+                         "kernel_ms_median": kern_ms},
+            "cpu_baseline": cpu,
+            "e2e": {"value": entries_step / e2e_s, "unit": UNIT, "h2d_bytes_per_step": 8 * nu,
+                    "d2h_bytes_per_step": 8 * nnz_local * nmat, "ms_per_step": e2e_s * 1e3},
+            "gpu_launches": args.steps * asm.ctx.stat(5),
+            "clocks": sampler.summary(),
+        }
+        print(json.dumps(line), flush=True)
+    asm.close()
+    if world > 1:
+        torch.distributed.destroy_process_group()
+    return 0
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=50)
+    ap.add_argument("--warmup", type=int, default=5)
+    ap.add_argument("--config", default=os.environ.get("FEA_BENCH_CONFIG", DEFAULT_CONFIG), choices=sorted(CONFIGS))
+    ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    args = ap.parse_args()
+    if args.warmup < 3:
+        args.warmup = 3  # timing rule: at least 3 warm-up steps
+    if args.impl == "reference":
+        return run_reference(args)
+    return run_ours(args)
+
+
+if __name__ == "__main__":
+    sys.exit(main())

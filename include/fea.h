@@ -1,0 +1,163 @@
+/*
+ * fea.h -- C ABI of libfea: loop-free FP64 finite-element reassembly on NVIDIA B200 (sm_100a).
+ *
+ * Hot path (BASELINE.json north_star; PAPER.md = arXiv 2204.03893 LaTeX source):
+ *   per Newton iteration, for the k(u)-weighted mass matrix M and conductivity ("stiffness")
+ *   matrix C of scalar 2D problems on triangles with P_p Lagrange elements (p = 1..4):
+ *     gather u_e = u(N_e)                                   (PAPER.md:76,  Sec. 3 step 2)
+ *     interpolate u_q = Phi^T u_e                           (Sec. 5)
+ *     weights Lambda = S * (w b^T), S_qe = k(u_q)           (Eq. def_lambda)
+ *             X_c = Lambda (.) W, W = [vec A_e], A_e = (B_e^T B_e)^{-1}
+ *     contraction V_m = Q_m X_m, V_c = Q_c X_c              (Algorithm 2)
+ *             (symmetric rows only)
+ *     deterministic scatter of V into CSR values           (Algorithm 2 line 12)
+ *
+ * Conventions (all calls):
+ *   - Every function returns fea_status (0 = FEA_OK, < 0 = error); no C++ exception crosses
+ *     the ABI.  fea_last_error(ctx) returns a message owned by ctx, valid until the next call.
+ *   - Host arrays passed to setup calls are COPIED; the caller keeps ownership.
+ *   - Device arrays (u, vals) are caller-owned buffers on the ctx device; the library never
+ *     frees caller memory.  vals must be 16-byte aligned (FEA_E_ARG otherwise).
+ *   - Setup calls (set_element, mesh_upload, build_pattern, get_*) are synchronous.
+ *     Assembly calls are asynchronous and ordered on the ctx stream; kernel / NCCL faults
+ *     surface at the next fea_sync (CUDA convention).
+ *   - Numbering: after fea_mesh_upload every vector and matrix is in LIBRARY numbering
+ *     (Morton order of DOF coordinates when FEA_REORDER_MORTON, else user order);
+ *     fea_get_dof_perm exports lib_to_user.  On rank r the CSR holds the library rows
+ *     [row_begin, row_begin + n_rows_local) with a local row_ptr starting at 0 and GLOBAL
+ *     column indices; the structural pattern is shared by M and C.
+ *   - A ctx is single-threaded: one ctx per (process, GPU).
+ */
+#ifndef FEA_H_
+#define FEA_H_
+
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+typedef struct fea_ctx_s* fea_ctx;
+
+typedef enum {
+    FEA_OK = 0,
+    FEA_E_ARG = -1,          /* bad argument: NULL, length, alignment, rule weights, ... */
+    FEA_E_STATE = -2,        /* call out of order (e.g. assemble before build_pattern)    */
+    FEA_E_MESH = -3,         /* degenerate element, bad index, inconsistent DOF map       */
+    FEA_E_CUDA = -4,         /* CUDA runtime error (message in fea_last_error)            */
+    FEA_E_NCCL = -5,         /* NCCL error                                                */
+    FEA_E_OOM = -6,          /* device or host allocation failed                          */
+    FEA_E_UNSUPPORTED = -7   /* order > 4, n_q > 16, nnz or local entries >= 2^31, ...   */
+} fea_status;
+
+enum { FEA_REORDER_NONE = 0, FEA_REORDER_MORTON = 1 };
+enum { FEA_MASS = 1, FEA_STIFF = 2 };
+/* Coefficient k(u) (reading 17 of DESIGN.md; NEXT-4 piecewise linear PAPER.md:560-568):
+ *   FEA_K_POLY: k(u) = sum_{i < n_par} par[i] u^i  (Horner), 1 <= n_par <= 9 (constant: n_par = 1)
+ *   FEA_K_EXP : k(u) = par[0] * exp(par[1] * u), n_par = 2
+ *   FEA_K_PWL : piecewise linear through (par[0],par[1]), (par[2],par[3]), ... (T_i, k_i),
+ *               2 <= m <= 8 breakpoints, T strictly increasing; segment s covers (T_s, T_{s+1}],
+ *               the first also T <= T_1, the last also T > T_m (linear extrapolation). */
+enum { FEA_K_POLY = 0, FEA_K_EXP = 1, FEA_K_PWL = 2 };
+
+/* Tuning keys for fea_set_tuning (before fea_build_pattern). */
+enum {
+    FEA_TUNE_SMEM_BUDGET = 1,   /* bytes of shared memory per CTA for element values (default 96 KiB) */
+    FEA_TUNE_THREADS = 2,       /* threads per CTA (default 256)                                     */
+    FEA_TUNE_TCHUNKS = 3        /* split of the symmetric rows per element across threads (0 = auto) */
+};
+
+/* Create a context on CUDA device `cuda_device`.  `stream` is a cudaStream_t (NULL = the
+ * legacy default stream) on which every assembly call is ordered.  rank/world describe the
+ * row partition (world >= 1, 0 <= rank < world); world > 1 requires fea_set_nccl before
+ * fea_reassemble.  cuda_device == -1 creates a PLANNING-ONLY context (no device memory,
+ * no GPU needed): set_element / mesh_upload / build_pattern / get_* work, assembly calls
+ * return FEA_E_STATE.  *out is set to NULL on failure (FEA_E_ARG, FEA_E_CUDA, FEA_E_OOM). */
+fea_status fea_create(fea_ctx* out, int cuda_device, void* stream, int rank, int world);
+
+/* Reference element (Algorithm 2 lines 1-3): Lagrange order 1..4 and a
+ * quadrature rule of n_q (1..16) points.  q_xy: host, n_q x 2 reference coordinates (x, y)
+ * on the triangle (0,0),(1,0),(0,1); q_w: host, n_q weights summing to 1/2 +- 1e-14
+ * (reference-triangle measure, reading 4).  The library computes Phi, J_q and the
+ * symmetric-reduced Q_m, Q_c tables itself, in long double, rounded once.
+ * Errors: FEA_E_ARG (NULL, weights), FEA_E_UNSUPPORTED (order, n_q). */
+fea_status fea_set_element(fea_ctx ctx, int order, int n_q, const double* q_xy, const double* q_w);
+
+/* Mesh (Algorithm 2 line 4): vertices a, b, c per element and
+ * index sets N_e in the documented local order (reading 7).
+ *   vert_xy  : host, n_vert x 2 float64
+ *   elem_vert: host, n_elem x 3 int32 (a, b, c); any orientation (|det B_e| is used)
+ *   elem_dof : host, n_elem x n_p int32, values in [0, n_dof)
+ *   reorder  : FEA_REORDER_NONE or FEA_REORDER_MORTON
+ * Validates indices, element non-degeneracy (|det B_e| >= 1e-14 diam^2, else FEA_E_MESH naming
+ * the element), distinct DOFs per element and that every element referencing a DOF places
+ * it at the same point (1e-10 * diam), which catches edge-orientation errors at p >= 3.
+ * Requires fea_set_element first (FEA_E_STATE).  Invalidates any previous pattern. */
+fea_status fea_mesh_upload(fea_ctx ctx, int64_t n_vert, const double* vert_xy, int64_t n_elem,
+                           const int32_t* elem_vert, int64_t n_dof, const int32_t* elem_dof, int reorder);
+
+/* Tuning before fea_build_pattern (keys above).  FEA_E_ARG for unknown keys / bad values. */
+fea_status fea_set_tuning(fea_ctx ctx, int key, int64_t value);
+
+/* Build the structural CSR pattern (reading 9: union over elements of N_e x N_e, sorted
+ * unique columns, numerically-zero slots kept) of this rank's rows and the per-iteration
+ * scatter plan (element-local entry -> CSR slot, fixed summation order: ascending library
+ * element index).  Outputs (host scalars, any may be NULL): first row, number of rows, nnz.
+ * Errors: FEA_E_STATE, FEA_E_UNSUPPORTED (nnz >= 2^31 per rank), FEA_E_OOM. */
+fea_status fea_build_pattern(fea_ctx ctx, int64_t* row_begin, int64_t* n_rows_local, int64_t* nnz_local);
+
+/* Copy the pattern out: row_ptr (n_rows_local + 1, int64, local, starts at 0) and col_idx
+ * (nnz_local, int32, global library columns).  Host pointers. */
+fea_status fea_get_pattern(fea_ctx ctx, int64_t* row_ptr, int32_t* col_idx);
+
+/* lib_to_user[l] = user DOF id of library DOF l (host, n_dof). */
+fea_status fea_get_dof_perm(fea_ctx ctx, int64_t* lib_to_user);
+
+/* lib_to_user for elements (host, n_elem): the library element order. */
+fea_status fea_get_elem_perm(fea_ctx ctx, int64_t* lib_to_user);
+
+/* Coefficient of M (which & FEA_MASS) and/or C (which & FEA_STIFF); kinds above.
+ * Default for both: FEA_K_POLY {1} (k = 1). */
+fea_status fea_set_coefficient(fea_ctx ctx, int which, int kind, int n_par, const double* par);
+
+/* Assemble M values (fea_assemble_mass), C values (fea_assemble_stiffness), or both in one
+ * fused pass (fea_assemble; either output may be NULL) for this rank's rows.
+ *   u_full: device, n_dof float64, library numbering (all DOFs referenced by this rank's
+ *           elements must be valid)
+ *   vals  : device, nnz_local float64, 16-byte aligned; fully overwritten.
+ * Deterministic: bit-identical across runs, CTA tilings and world sizes. Asynchronous. */
+fea_status fea_assemble_mass(fea_ctx ctx, const double* u_full, double* vals);
+fea_status fea_assemble_stiffness(fea_ctx ctx, const double* u_full, double* vals);
+fea_status fea_assemble(fea_ctx ctx, const double* u_full, double* mass_vals, double* stiff_vals);
+
+/* Per-Newton-iteration entry point: allgather of the owned slice u_owned (device,
+ * n_rows_local float64, library rows [row_begin, row_begin + n_rows_local)) into the
+ * library-owned u_full over NCCL (world > 1), then the fused assembly of the non-NULL
+ * outputs.  world == 1: u_owned is the full vector.  Asynchronous on the ctx stream. */
+fea_status fea_reassemble(fea_ctx ctx, const double* u_owned, double* mass_vals, double* stiff_vals);
+
+/* End-to-end variant for host buffers: copies u_host (pinned or pageable, n_rows_local)
+ * to the device, reassembles, and copies the values back to mass_host / stiff_host
+ * (nnz_local each, may be NULL).  Synchronous. */
+fea_status fea_reassemble_host(fea_ctx ctx, const double* u_host, double* mass_host, double* stiff_host);
+
+/* Multi-GPU: the 128-byte ncclUniqueId.  Rank 0 calls fea_nccl_unique_id and broadcasts the
+ * bytes (e.g. over a torch.distributed process group); every rank then calls fea_set_nccl. */
+fea_status fea_nccl_unique_id(void* id_out_128_bytes);
+fea_status fea_set_nccl(fea_ctx ctx, const void* id_128_bytes);
+
+/* Wait for all work on the ctx stream; returns deferred CUDA / NCCL errors. */
+fea_status fea_sync(fea_ctx ctx);
+
+/* Statistics of the plan (for reports): key 1 = number of CTA blocks, 2 = element-visits
+ * including ghosts, 3 = owned elements, 4 = local entries (sum over blocks of contributor
+ * count), 5 = kernel launches per fea_assemble call, 6 = smem bytes per CTA. */
+fea_status fea_get_stat(fea_ctx ctx, int key, int64_t* value);
+
+const char* fea_last_error(fea_ctx ctx);
+void fea_destroy(fea_ctx ctx);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* FEA_H_ */

@@ -1,0 +1,931 @@
+// fea_host.cpp -- libfea C ABI (include/fea.h): reference tables, mesh upload with Morton
+// renumbering, structural pattern + scatter plan (row blocks), launches, NCCL allgather.
+//
+// Independent of oracle/ (no shared code): the Lagrange basis here comes from inverting the
+// monomial Vandermonde matrix in long double (the oracle uses the barycentric product
+// formula); the pattern comes from sorting (row, col) records per row block (MATLAB
+// sparse() semantics), the oracle builds it row by row from the incidence.
+#include <cuda_runtime.h>
+#include <dlfcn.h>
+#include <nccl.h>
+
+#include <algorithm>
+#include <atomic>
+#include <cmath>
+#include <cstdarg>
+#include <cstdio>
+#include <cstring>
+#include <numeric>
+#include <string>
+#include <thread>
+#include <vector>
+
+#include "../../include/fea.h"
+#include "fea_internal.h"
+
+namespace {
+
+// ------------------------------------------------------------------ NCCL (dlopen)
+struct NcclApi {
+    bool ok = false;
+    ncclResult_t (*getUniqueId)(ncclUniqueId*) = nullptr;
+    ncclResult_t (*commInitRank)(ncclComm_t*, int, ncclUniqueId, int) = nullptr;
+    ncclResult_t (*allGather)(const void*, void*, size_t, ncclDataType_t, ncclComm_t, cudaStream_t) = nullptr;
+    ncclResult_t (*commDestroy)(ncclComm_t) = nullptr;
+    const char* (*getErrorString)(ncclResult_t) = nullptr;
+};
+
+NcclApi& nccl() {
+    static NcclApi api;
+    static bool tried = false;
+    if (!tried) {
+        tried = true;
+        void* h = dlopen("libnccl.so.2", RTLD_NOW | RTLD_GLOBAL);
+        if (!h) h = dlopen("libnccl.so", RTLD_NOW | RTLD_GLOBAL);
+        if (h) {
+            api.getUniqueId = (decltype(api.getUniqueId))dlsym(h, "ncclGetUniqueId");
+            api.commInitRank = (decltype(api.commInitRank))dlsym(h, "ncclCommInitRank");
+            api.allGather = (decltype(api.allGather))dlsym(h, "ncclAllGather");
+            api.commDestroy = (decltype(api.commDestroy))dlsym(h, "ncclCommDestroy");
+            api.getErrorString = (decltype(api.getErrorString))dlsym(h, "ncclGetErrorString");
+            api.ok = api.getUniqueId && api.commInitRank && api.allGather && api.commDestroy && api.getErrorString;
+        }
+    }
+    return api;
+}
+
+template <typename T>
+void dfree(T*& p) {
+    if (p) cudaFree((void*)p);
+    p = nullptr;
+}
+
+int tri_index(int np, int i, int j) {  // i <= j, row-major upper triangle
+    return i * np - i * (i - 1) / 2 + (j - i);
+}
+
+}  // namespace
+
+struct fea_ctx_s {
+    int device = 0;
+    bool host_only = false;  // cuda_device == -1: planning only, no device memory
+    cudaStream_t stream = nullptr;
+    int rank = 0, world = 1;
+    std::string err;
+    int sm_count = 148;
+
+    // reference element
+    int order = 0, np = 0, nq = 0, T = 0;
+    std::vector<double> qxy, qw, tables;
+
+    // mesh, library numbering
+    bool have_mesh = false;
+    int64_t n_vert = 0, n_e = 0, n_dof = 0;
+    std::vector<int64_t> dof_lib2user, elem_lib2user;
+    std::vector<int32_t> ed;        // [n_e][np] library DOFs, library element order
+    std::vector<int32_t> elem_min;  // min library DOF per library element
+    std::vector<double> dxy;        // [n_dof][2]
+    int32_t* d_dofT = nullptr;
+    double2* d_xy = nullptr;
+    double* d_tables = nullptr;
+
+    // plan
+    bool have_plan = false;
+    int plan_which = FEA_MASS | FEA_STIFF;
+    int64_t row_begin = 0, n_rows = 0, nnz = 0, rows_per_rank = 0;
+    std::vector<int64_t> row_ptr;
+    std::vector<int32_t> col_idx;
+    FeaBlock* d_blocks = nullptr;
+    uint8_t* d_counts = nullptr;
+    uint16_t* d_contrib = nullptr;
+    int32_t* d_chunk = nullptr;
+    int32_t* d_ghosts = nullptr;
+    int nblocks = 0, e_max = 0, smem_bytes = 0, threads = 256, ntc = 1, staged = 0, grid = 0;
+    int64_t stat_visits = 0, stat_owned = 0, stat_entries = 0;
+    int launches_per_call = 1;
+
+    // coefficients
+    FeaCoef coef_m{}, coef_c{};
+
+    // tuning
+    int64_t tune_smem = 0, tune_threads = 256, tune_tchunks = 0;
+
+    // reassemble buffers
+    double* d_ufull = nullptr;
+    double* d_usend = nullptr;
+    double* d_vm = nullptr;
+    double* d_vc = nullptr;
+    void* comm = nullptr;
+
+    fea_status fail(fea_status s, const char* fmt, ...) {
+        char buf[512];
+        va_list ap;
+        va_start(ap, fmt);
+        vsnprintf(buf, sizeof buf, fmt, ap);
+        va_end(ap);
+        err = buf;
+        return s;
+    }
+    void free_plan() {
+        dfree(d_blocks);
+        dfree(d_counts);
+        dfree(d_contrib);
+        dfree(d_chunk);
+        dfree(d_ghosts);
+        dfree(d_vm);
+        dfree(d_vc);
+        row_ptr.clear();
+        col_idx.clear();
+        have_plan = false;
+    }
+    void free_mesh() {
+        free_plan();
+        dfree(d_dofT);
+        dfree(d_xy);
+        dfree(d_ufull);
+        dfree(d_usend);
+        have_mesh = false;
+    }
+};
+
+#define FEA_CUDA(ctx, x)                                                                              \
+    do {                                                                                              \
+        cudaError_t _e = (x);                                                                         \
+        if (_e != cudaSuccess) return (ctx)->fail(FEA_E_CUDA, "%s: %s", #x, cudaGetErrorString(_e)); \
+    } while (0)
+
+// ------------------------------------------------------------------ reference tables
+namespace {
+
+int lib_nodes(int p, int k[][3]) {  // documented local order (reading 7)
+    int n = 0;
+    auto put = [&](int a, int b, int c) { k[n][0] = a; k[n][1] = b; k[n][2] = c; ++n; };
+    put(p, 0, 0);
+    put(0, p, 0);
+    put(0, 0, p);
+    for (int t = 1; t < p; ++t) put(0, p - t, t);
+    for (int t = 1; t < p; ++t) put(t, 0, p - t);
+    for (int t = 1; t < p; ++t) put(p - t, t, 0);
+    for (int a = 1; a < p; ++a)
+        for (int b = 1; b < p; ++b)
+            if (p - a - b >= 1) put(p - a - b, a, b);
+    return n;
+}
+
+// Gauss-Jordan inverse with partial pivoting in long double.  Returns false if singular.
+bool invert(std::vector<long double>& A, int n) {
+    std::vector<long double> I(n * n, 0.0L);
+    for (int i = 0; i < n; ++i) I[i * n + i] = 1.0L;
+    for (int c = 0; c < n; ++c) {
+        int piv = c;
+        for (int r = c + 1; r < n; ++r)
+            if (fabsl(A[r * n + c]) > fabsl(A[piv * n + c])) piv = r;
+        if (fabsl(A[piv * n + c]) < 1e-30L) return false;
+        if (piv != c)
+            for (int j = 0; j < n; ++j) {
+                std::swap(A[c * n + j], A[piv * n + j]);
+                std::swap(I[c * n + j], I[piv * n + j]);
+            }
+        const long double d = A[c * n + c];
+        for (int j = 0; j < n; ++j) {
+            A[c * n + j] /= d;
+            I[c * n + j] /= d;
+        }
+        for (int r = 0; r < n; ++r)
+            if (r != c) {
+                const long double f = A[r * n + c];
+                if (f == 0.0L) continue;
+                for (int j = 0; j < n; ++j) {
+                    A[r * n + j] -= f * A[c * n + j];
+                    I[r * n + j] -= f * I[c * n + j];
+                }
+            }
+    }
+    A = I;
+    return true;
+}
+
+// Tables (Algorithm 2 lines 1-3), symmetric rows only:
+//   Phi[i][q]             = phi_i(x_q)
+//   w[q]
+//   Q[t][0][q] = Phi_i Phi_j                      (rows of Q_m = Phi (.) Phi)
+//   Q[t][1][q] = J_i0 J_j0, Q[t][2][q] = J_i1 J_j1, Q[t][3][q] = J_i0 J_j1 + J_i1 J_j0
+//                                                 (rows of Q_c = [J_q (x) J_q], columns of vec A
+//                                                  merged by the symmetry A01 = A10)
+bool build_tables(int p, int nq, const double* qxy, const double* qw, std::vector<double>& tab) {
+    int kk[FEA_MAX_NP][3];
+    const int np = lib_nodes(p, kk);
+    std::vector<std::pair<int, int>> mono;
+    for (int d = 0; d <= p; ++d)
+        for (int a = d; a >= 0; --a) mono.push_back({a, d - a});
+    std::vector<long double> V(np * np);
+    for (int n = 0; n < np; ++n) {
+        const long double x = (long double)kk[n][1] / p, y = (long double)kk[n][2] / p;
+        for (int m = 0; m < np; ++m) V[n * np + m] = powl(x, mono[m].first) * powl(y, mono[m].second);
+    }
+    if (!invert(V, np)) return false;  // V now holds V^{-1}; phi_i = sum_m Vinv[m][i] mono_m
+    std::vector<long double> phi(np * nq), gx(np * nq), gy(np * nq);
+    for (int q = 0; q < nq; ++q) {
+        const long double x = qxy[2 * q], y = qxy[2 * q + 1];
+        for (int i = 0; i < np; ++i) {
+            long double f = 0, fx = 0, fy = 0;
+            for (int m = 0; m < np; ++m) {
+                const int a = mono[m].first, b = mono[m].second;
+                const long double c = V[m * np + i];
+                f += c * powl(x, a) * powl(y, b);
+                if (a > 0) fx += c * a * powl(x, a - 1) * powl(y, b);
+                if (b > 0) fy += c * b * powl(x, a) * powl(y, b - 1);
+            }
+            phi[i * nq + q] = f;
+            gx[i * nq + q] = fx;
+            gy[i * nq + q] = fy;
+        }
+    }
+    const int T = np * (np + 1) / 2;
+    tab.assign((size_t)np * nq + nq + (size_t)T * 4 * nq, 0.0);
+    for (int i = 0; i < np * nq; ++i) tab[i] = (double)phi[i];
+    for (int q = 0; q < nq; ++q) tab[np * nq + q] = qw[q];
+    double* Q = tab.data() + np * nq + nq;
+    for (int i = 0; i < np; ++i)
+        for (int j = i; j < np; ++j) {
+            const int t = tri_index(np, i, j);
+            for (int q = 0; q < nq; ++q) {
+                const int a = i * nq + q, b = j * nq + q;
+                Q[(t * 4 + 0) * nq + q] = (double)(phi[a] * phi[b]);
+                Q[(t * 4 + 1) * nq + q] = (double)(gx[a] * gx[b]);
+                Q[(t * 4 + 2) * nq + q] = (double)(gy[a] * gy[b]);
+                Q[(t * 4 + 3) * nq + q] = (double)(gx[a] * gy[b] + gy[a] * gx[b]);
+            }
+        }
+    return true;
+}
+
+// Morton key of a 2D point: 21 bits per axis over the bounding box, x in the even bits.
+uint64_t morton(double x, double y, double x0, double y0, double sx, double sy) {
+    auto qz = [](double v, double v0, double s) -> uint64_t {
+        if (!(s > 0)) return 0;
+        double f = std::floor((v - v0) / s * 2097152.0);
+        if (f < 0) f = 0;
+        if (f > 2097151.0) f = 2097151.0;
+        return (uint64_t)f;
+    };
+    // interleave: x bit k -> position 2k, y bit k -> 2k+1
+    const uint64_t ix = qz(x, x0, sx), iy = qz(y, y0, sy);
+    uint64_t r = 0;
+    for (int b = 0; b < 21; ++b) r |= ((ix >> b) & 1ull) << (2 * b) | ((iy >> b) & 1ull) << (2 * b + 1);
+    return r;
+}
+
+template <typename F>
+void parallel_for(int64_t n, F f) {
+    int nt = (int)std::max(1u, std::thread::hardware_concurrency());
+    nt = (int)std::min<int64_t>(nt, std::max<int64_t>(1, n));
+    if (nt <= 1) {
+        for (int64_t i = 0; i < n; ++i) f(i);
+        return;
+    }
+    std::atomic<int64_t> next(0);
+    std::vector<std::thread> th;
+    for (int k = 0; k < nt; ++k)
+        th.emplace_back([&] {
+            for (;;) {
+                const int64_t i = next.fetch_add(1);
+                if (i >= n) break;
+                f(i);
+            }
+        });
+    for (auto& t : th) t.join();
+}
+
+}  // namespace
+
+// ------------------------------------------------------------------ ABI
+extern "C" {
+
+fea_status fea_create(fea_ctx* out, int cuda_device, void* stream, int rank, int world) {
+    if (!out) return FEA_E_ARG;
+    *out = nullptr;
+    if (world < 1 || rank < 0 || rank >= world) return FEA_E_ARG;
+    const bool host_only = cuda_device == -1;
+    if (!host_only) {
+        int ndev = 0;
+        if (cudaGetDeviceCount(&ndev) != cudaSuccess || cuda_device < 0 || cuda_device >= ndev) return FEA_E_CUDA;
+        if (cudaSetDevice(cuda_device) != cudaSuccess) return FEA_E_CUDA;
+    }
+    fea_ctx c = new (std::nothrow) fea_ctx_s();
+    if (!c) return FEA_E_OOM;
+    c->host_only = host_only;
+    c->device = host_only ? 0 : cuda_device;
+    c->stream = (cudaStream_t)stream;
+    c->rank = rank;
+    c->world = world;
+    if (!host_only) cudaDeviceGetAttribute(&c->sm_count, cudaDevAttrMultiProcessorCount, cuda_device);
+    c->coef_m.kind = c->coef_c.kind = FEA_K_POLY;
+    c->coef_m.npar = c->coef_c.npar = 1;
+    c->coef_m.par[0] = c->coef_c.par[0] = 1.0;
+    *out = c;
+    return FEA_OK;
+}
+
+void fea_destroy(fea_ctx c) {
+    if (!c) return;
+    if (!c->host_only) cudaSetDevice(c->device);
+    c->free_mesh();
+    dfree(c->d_tables);
+    if (c->comm && nccl().ok) nccl().commDestroy((ncclComm_t)c->comm);
+    delete c;
+}
+
+const char* fea_last_error(fea_ctx c) { return c ? c->err.c_str() : "null context"; }
+
+fea_status fea_set_element(fea_ctx c, int order, int n_q, const double* q_xy, const double* q_w) {
+    if (!c) return FEA_E_ARG;
+    if (!q_xy || !q_w) return c->fail(FEA_E_ARG, "set_element: NULL rule arrays");
+    if (order < 1 || order > FEA_MAX_ORDER) return c->fail(FEA_E_UNSUPPORTED, "order %d not in 1..4", order);
+    if (n_q < 1 || n_q > FEA_MAX_NQ) return c->fail(FEA_E_UNSUPPORTED, "n_q %d not in 1..16", n_q);
+    long double s = 0;
+    for (int q = 0; q < n_q; ++q) {
+        if (!std::isfinite(q_w[q]) || !std::isfinite(q_xy[2 * q]) || !std::isfinite(q_xy[2 * q + 1]))
+            return c->fail(FEA_E_ARG, "set_element: non-finite rule entry %d", q);
+        s += q_w[q];
+    }
+    if (fabsl(s - 0.5L) > 1e-14L)
+        return c->fail(FEA_E_ARG, "quadrature weights sum to %.17g, expected 1/2 (reference-triangle measure)", (double)s);
+    std::vector<double> tab;
+    if (!build_tables(order, n_q, q_xy, q_w, tab)) return c->fail(FEA_E_UNSUPPORTED, "singular Vandermonde");
+    if (!c->host_only) cudaSetDevice(c->device);
+    c->free_mesh();
+    dfree(c->d_tables);
+    c->order = order;
+    c->nq = n_q;
+    c->np = (order + 1) * (order + 2) / 2;
+    c->T = c->np * (c->np + 1) / 2;
+    c->qxy.assign(q_xy, q_xy + 2 * n_q);
+    c->qw.assign(q_w, q_w + n_q);
+    c->tables = tab;
+    if (c->host_only) return FEA_OK;
+    FEA_CUDA(c, cudaMalloc(&c->d_tables, tab.size() * sizeof(double)));
+    FEA_CUDA(c, cudaMemcpy(c->d_tables, tab.data(), tab.size() * sizeof(double), cudaMemcpyHostToDevice));
+    return FEA_OK;
+}
+
+fea_status fea_mesh_upload(fea_ctx c, int64_t n_vert, const double* vert_xy, int64_t n_elem,
+                           const int32_t* elem_vert, int64_t n_dof, const int32_t* elem_dof, int reorder) {
+    if (!c) return FEA_E_ARG;
+    if (c->order == 0) return c->fail(FEA_E_STATE, "mesh_upload before set_element");
+    if (n_vert < 3 || n_elem < 1 || n_dof < 1 || !vert_xy || !elem_vert || !elem_dof)
+        return c->fail(FEA_E_ARG, "mesh_upload: empty or NULL mesh");
+    if (reorder != FEA_REORDER_NONE && reorder != FEA_REORDER_MORTON) return c->fail(FEA_E_ARG, "bad reorder flag");
+    if (n_elem >= (1ll << 31) || n_dof >= (1ll << 31) || n_vert >= (1ll << 31))
+        return c->fail(FEA_E_UNSUPPORTED, "mesh sizes must be < 2^31");
+    const int np = c->np, p = c->order;
+    int kk[FEA_MAX_NP][3];
+    lib_nodes(p, kk);
+    if (!c->host_only) cudaSetDevice(c->device);
+    c->free_mesh();
+
+    // validation + DOF coordinates (user numbering), element by element
+    std::vector<double> uxy(2 * n_dof, 0.0);
+    std::vector<int64_t> first(n_dof, -1);
+    for (int64_t e = 0; e < n_elem; ++e) {
+        const int32_t* v = elem_vert + 3 * e;
+        for (int k = 0; k < 3; ++k)
+            if (v[k] < 0 || v[k] >= n_vert) return c->fail(FEA_E_MESH, "element %lld: vertex index %d out of range", (long long)e, v[k]);
+        const double* a = vert_xy + 2 * (int64_t)v[0];
+        const double* b = vert_xy + 2 * (int64_t)v[1];
+        const double* cc = vert_xy + 2 * (int64_t)v[2];
+        const double B00 = b[0] - a[0], B10 = b[1] - a[1], B01 = cc[0] - a[0], B11 = cc[1] - a[1];
+        const double det = B00 * B11 - B01 * B10;
+        const double e2 = (cc[0] - b[0]) * (cc[0] - b[0]) + (cc[1] - b[1]) * (cc[1] - b[1]);
+        const double diam2 = std::max(std::max(B00 * B00 + B10 * B10, B01 * B01 + B11 * B11), e2);
+        if (!(std::fabs(det) >= 1e-14 * diam2)) return c->fail(FEA_E_MESH, "degenerate element %lld", (long long)e);
+        const int32_t* d = elem_dof + (int64_t)np * e;
+        for (int i = 0; i < np; ++i) {
+            if (d[i] < 0 || d[i] >= n_dof) return c->fail(FEA_E_MESH, "element %lld: DOF index %d out of range", (long long)e, d[i]);
+            for (int j = 0; j < i; ++j)
+                if (d[j] == d[i]) return c->fail(FEA_E_MESH, "element %lld: repeated DOF %d", (long long)e, d[i]);
+            const double x = (kk[i][0] * a[0] + kk[i][1] * b[0] + kk[i][2] * cc[0]) / p;
+            const double y = (kk[i][0] * a[1] + kk[i][1] * b[1] + kk[i][2] * cc[1]) / p;
+            if (first[d[i]] < 0) {
+                first[d[i]] = e;
+                uxy[2 * d[i]] = x;
+                uxy[2 * d[i] + 1] = y;
+            } else {
+                const double dx = x - uxy[2 * d[i]], dy = y - uxy[2 * d[i] + 1];
+                if (dx * dx + dy * dy > 1e-20 * diam2)
+                    return c->fail(FEA_E_MESH, "DOF %d placed inconsistently by elements %lld and %lld (edge orientation?)",
+                                   d[i], (long long)first[d[i]], (long long)e);
+            }
+        }
+    }
+    for (int64_t d = 0; d < n_dof; ++d)
+        if (first[d] < 0) return c->fail(FEA_E_MESH, "DOF %lld is not referenced by any element", (long long)d);
+
+    // library DOF numbering
+    std::vector<int64_t> lib2user(n_dof), user2lib(n_dof);
+    std::iota(lib2user.begin(), lib2user.end(), 0);
+    if (reorder == FEA_REORDER_MORTON) {
+        double x0 = uxy[0], x1 = uxy[0], y0 = uxy[1], y1 = uxy[1];
+        for (int64_t d = 0; d < n_dof; ++d) {
+            x0 = std::min(x0, uxy[2 * d]);
+            x1 = std::max(x1, uxy[2 * d]);
+            y0 = std::min(y0, uxy[2 * d + 1]);
+            y1 = std::max(y1, uxy[2 * d + 1]);
+        }
+        std::vector<uint64_t> key(n_dof);
+        parallel_for((n_dof + 65535) / 65536, [&](int64_t blk) {
+            const int64_t a = blk * 65536, b = std::min<int64_t>(n_dof, a + 65536);
+            for (int64_t d = a; d < b; ++d) key[d] = morton(uxy[2 * d], uxy[2 * d + 1], x0, y0, x1 - x0, y1 - y0);
+        });
+        std::stable_sort(lib2user.begin(), lib2user.end(), [&](int64_t a, int64_t b) { return key[a] < key[b]; });
+    }
+    for (int64_t l = 0; l < n_dof; ++l) user2lib[lib2user[l]] = l;
+
+    // library element order: by minimum library DOF, then user id
+    std::vector<int32_t> emin(n_elem);
+    for (int64_t e = 0; e < n_elem; ++e) {
+        int64_t m = INT64_MAX;
+        for (int i = 0; i < np; ++i) m = std::min(m, user2lib[elem_dof[(int64_t)np * e + i]]);
+        emin[e] = (int32_t)m;
+    }
+    std::vector<int64_t> el2u(n_elem);
+    std::iota(el2u.begin(), el2u.end(), 0);
+    std::stable_sort(el2u.begin(), el2u.end(), [&](int64_t a, int64_t b) { return emin[a] < emin[b]; });
+
+    c->n_vert = n_vert;
+    c->n_e = n_elem;
+    c->n_dof = n_dof;
+    c->dof_lib2user = lib2user;
+    c->elem_lib2user = el2u;
+    c->ed.resize((size_t)n_elem * np);
+    c->elem_min.resize(n_elem);
+    for (int64_t l = 0; l < n_elem; ++l) {
+        const int64_t e = el2u[l];
+        for (int i = 0; i < np; ++i) c->ed[(size_t)l * np + i] = (int32_t)user2lib[elem_dof[(int64_t)np * e + i]];
+        c->elem_min[l] = emin[e];
+    }
+    c->dxy.resize(2 * n_dof);
+    for (int64_t l = 0; l < n_dof; ++l) {
+        c->dxy[2 * l] = uxy[2 * lib2user[l]];
+        c->dxy[2 * l + 1] = uxy[2 * lib2user[l] + 1];
+    }
+    if (c->host_only) {
+        c->have_mesh = true;
+        return FEA_OK;
+    }
+    // device: SoA DOF map and coordinates
+    std::vector<int32_t> dofT((size_t)n_elem * np);
+    for (int64_t l = 0; l < n_elem; ++l)
+        for (int i = 0; i < np; ++i) dofT[(size_t)i * n_elem + l] = c->ed[(size_t)l * np + i];
+    FEA_CUDA(c, cudaMalloc(&c->d_dofT, dofT.size() * sizeof(int32_t)));
+    FEA_CUDA(c, cudaMemcpy(c->d_dofT, dofT.data(), dofT.size() * sizeof(int32_t), cudaMemcpyHostToDevice));
+    FEA_CUDA(c, cudaMalloc(&c->d_xy, n_dof * sizeof(double2)));
+    FEA_CUDA(c, cudaMemcpy(c->d_xy, c->dxy.data(), n_dof * sizeof(double2), cudaMemcpyHostToDevice));
+    c->have_mesh = true;
+    return FEA_OK;
+}
+
+fea_status fea_set_tuning(fea_ctx c, int key, int64_t value) {
+    if (!c) return FEA_E_ARG;
+    switch (key) {
+        case FEA_TUNE_SMEM_BUDGET:
+            if (value != 0 && (value < 4096 || value > 232448)) return c->fail(FEA_E_ARG, "smem budget out of range");
+            c->tune_smem = value;
+            break;
+        case FEA_TUNE_THREADS:
+            if (value < 64 || value > 256 || value % 32) return c->fail(FEA_E_ARG, "threads must be 64..256, multiple of 32");
+            c->tune_threads = value;
+            break;
+        case FEA_TUNE_TCHUNKS:
+            if (value < 0 || value > 64) return c->fail(FEA_E_ARG, "tchunks out of range");
+            c->tune_tchunks = value;
+            break;
+        case 4:  // plan matrices bitmask (FEA_MASS | FEA_STIFF)
+            if (value < 1 || value > 3) return c->fail(FEA_E_ARG, "plan matrices must be a nonzero MASS|STIFF mask");
+            c->plan_which = (int)value;
+            break;
+        default:
+            return c->fail(FEA_E_ARG, "unknown tuning key %d", key);
+    }
+    if (c->have_plan) c->free_plan();
+    return FEA_OK;
+}
+
+fea_status fea_build_pattern(fea_ctx c, int64_t* row_begin, int64_t* n_rows_local, int64_t* nnz_local) {
+    if (!c) return FEA_E_ARG;
+    if (!c->have_mesh) return c->fail(FEA_E_STATE, "build_pattern before mesh_upload");
+    if (!c->host_only) cudaSetDevice(c->device);
+    c->free_plan();
+    const int np = c->np, T = c->T, nq = c->nq;
+    const int64_t n_e = c->n_e, n_dof = c->n_dof;
+    const int64_t rpr = (n_dof + c->world - 1) / c->world;
+    const int64_t R0 = std::min<int64_t>(n_dof, rpr * c->rank), R1 = std::min<int64_t>(n_dof, R0 + rpr);
+    const int64_t nr = R1 - R0;
+    c->rows_per_rank = rpr;
+    c->row_begin = R0;
+    c->n_rows = nr;
+
+    // kernel configuration
+    const int nmat = (c->plan_which & FEA_MASS ? 1 : 0) + (c->plan_which & FEA_STIFF ? 1 : 0);
+    c->staged = c->order >= 3 ? 1 : 0;
+    c->threads = (int)c->tune_threads;
+    int64_t budget = c->tune_smem ? c->tune_smem : (c->order >= 3 ? 200 * 1024 : 96 * 1024);
+    const int64_t tab_bytes = (int64_t)((c->tables.size() + 1) & ~size_t(1)) * 8;
+    const int nlam = 2;  // worst case (distinct coefficients for M and C)
+    const int64_t per_el = (int64_t)T * nmat * 8 + (c->staged ? (int64_t)(nlam * nq + 3) * 8 : 0);
+    int64_t e_max = (budget - tab_bytes) / per_el;
+    e_max = std::min<int64_t>(e_max, 65535 / T);
+    e_max = std::min<int64_t>(e_max, 1 << 20);
+
+    // incidence of this rank's rows (ascending library element per row)
+    std::vector<int64_t> iptr(nr + 1, 0);
+    for (int64_t e = 0; e < n_e; ++e)
+        for (int i = 0; i < np; ++i) {
+            const int64_t d = c->ed[(size_t)e * np + i];
+            if (d >= R0 && d < R1) iptr[d - R0 + 1]++;
+        }
+    for (int64_t r = 0; r < nr; ++r) iptr[r + 1] += iptr[r];
+    std::vector<int32_t> inc(std::max<int64_t>(1, iptr[nr]));
+    {
+        std::vector<int64_t> pos(iptr.begin(), iptr.end() - 1);
+        for (int64_t e = 0; e < n_e; ++e)
+            for (int i = 0; i < np; ++i) {
+                const int64_t d = c->ed[(size_t)e * np + i];
+                if (d >= R0 && d < R1) inc[pos[d - R0]++] = (int32_t)e;
+            }
+    }
+    int64_t max_inc = 0;
+    for (int64_t r = 0; r < nr; ++r) max_inc = std::max(max_inc, iptr[r + 1] - iptr[r]);
+    if (max_inc > 255) return c->fail(FEA_E_UNSUPPORTED, "a DOF belongs to %lld elements (> 255)", (long long)max_inc);
+    if (e_max < std::max<int64_t>(max_inc, 1))
+        return c->fail(FEA_E_UNSUPPORTED, "shared-memory budget too small: %lld elements per block", (long long)e_max);
+
+    // greedy row blocks: the element set of each block must fit e_max
+    std::vector<int64_t> brow;  // block row starts (rank-local)
+    {
+        std::vector<int32_t> mark(n_e, -1);
+        int32_t cur = -1;
+        int64_t nE = 0;
+        for (int64_t r = 0; r < nr; ++r) {
+            int64_t add = 0;
+            for (int64_t k = iptr[r]; k < iptr[r + 1]; ++k) add += mark[inc[k]] != cur;
+            if (cur < 0 || nE + add > e_max) {
+                ++cur;
+                brow.push_back(r);
+                nE = 0;
+                add = iptr[r + 1] - iptr[r];
+            }
+            for (int64_t k = iptr[r]; k < iptr[r + 1]; ++k) mark[inc[k]] = cur;
+            nE += add;
+        }
+    }
+    const int64_t nb = (int64_t)brow.size();
+    brow.push_back(nr);
+
+    struct BOut {
+        std::vector<int32_t> rownnz, cols, ghosts, chunk;
+        std::vector<uint8_t> counts;
+        std::vector<uint16_t> contrib;
+        int32_t own0 = 0, nown = 0;
+        std::string err;
+    };
+    std::vector<BOut> bo(nb);
+    const int64_t EM = e_max;
+    parallel_for(nb, [&](int64_t b) {
+        BOut& o = bo[b];
+        const int64_t ra = brow[b], rb = brow[b + 1];
+        const int64_t ga = R0 + ra, gb = R0 + rb;  // global library rows
+        std::vector<int32_t> E;
+        for (int64_t r = ra; r < rb; ++r) E.insert(E.end(), inc.begin() + iptr[r], inc.begin() + iptr[r + 1]);
+        std::sort(E.begin(), E.end());
+        E.erase(std::unique(E.begin(), E.end()), E.end());
+        int64_t ng = 0;
+        while (ng < (int64_t)E.size() && c->elem_min[E[ng]] < ga) ++ng;
+        o.ghosts.assign(E.begin(), E.begin() + ng);
+        o.nown = (int32_t)(E.size() - ng);
+        o.own0 = o.nown ? E[ng] : 0;
+        for (int64_t k = ng; k < (int64_t)E.size(); ++k)
+            if (E[k] != o.own0 + (k - ng) || c->elem_min[E[k]] >= gb) {
+                o.err = "owned elements not contiguous";
+                return;
+            }
+        // records (row, col, le, t) generated in ascending le; stable sort by (row, col)
+        struct Rec { int32_t row, col; int32_t le; int32_t t; };
+        std::vector<Rec> recs;
+        for (int64_t le = 0; le < (int64_t)E.size(); ++le) {
+            const int32_t* d = &c->ed[(size_t)E[le] * np];
+            for (int i = 0; i < np; ++i) {
+                if (d[i] < ga || d[i] >= gb) continue;
+                for (int j = 0; j < np; ++j)
+                    recs.push_back({d[i], d[j], (int32_t)le, tri_index(np, std::min(i, j), std::max(i, j))});
+            }
+        }
+        std::stable_sort(recs.begin(), recs.end(), [](const Rec& x, const Rec& y) {
+            return x.row != y.row ? x.row < y.row : x.col < y.col;
+        });
+        o.rownnz.assign(rb - ra, 0);
+        o.contrib.reserve(recs.size());
+        size_t k = 0;
+        int64_t nslot = 0;
+        while (k < recs.size()) {
+            size_t k2 = k;
+            while (k2 < recs.size() && recs[k2].row == recs[k].row && recs[k2].col == recs[k].col) ++k2;
+            if (nslot % 32 == 0) o.chunk.push_back((int32_t)o.contrib.size());
+            o.cols.push_back(recs[k].col);
+            o.rownnz[recs[k].row - ga]++;
+            o.counts.push_back((uint8_t)(k2 - k));
+            for (size_t m = k; m < k2; ++m) o.contrib.push_back((uint16_t)(recs[m].t * EM + recs[m].le));
+            ++nslot;
+            k = k2;
+        }
+    });
+    for (auto& o : bo)
+        if (!o.err.empty()) return c->fail(FEA_E_MESH, "plan: %s", o.err.c_str());
+
+    // concatenate
+    std::vector<FeaBlock> blocks(nb);
+    int64_t nnz = 0, ncon = 0, nch = 0, ngh = 0, visits = 0, owned = 0;
+    for (int64_t b = 0; b < nb; ++b) {
+        FeaBlock& B = blocks[b];
+        B.slot0 = nnz;
+        B.contrib0 = ncon;
+        B.row0 = (int32_t)brow[b];
+        B.nslots = (int32_t)bo[b].cols.size();
+        B.own0 = bo[b].own0;
+        B.nown = bo[b].nown;
+        B.ghost0 = (int32_t)ngh;
+        B.nghost = (int32_t)bo[b].ghosts.size();
+        B.chunk0 = (int32_t)nch;
+        B.pad = 0;
+        nnz += B.nslots;
+        ncon += bo[b].contrib.size();
+        nch += bo[b].chunk.size();
+        ngh += bo[b].ghosts.size();
+        visits += B.nown + B.nghost;
+        owned += B.nown;
+    }
+    if (nnz >= (1ll << 31)) return c->fail(FEA_E_UNSUPPORTED, "nnz %lld >= 2^31 on one rank", (long long)nnz);
+    c->row_ptr.assign(nr + 1, 0);
+    c->col_idx.resize(nnz);
+    std::vector<uint8_t> counts(nnz);
+    std::vector<uint16_t> contrib(std::max<int64_t>(ncon, 1));
+    std::vector<int32_t> chunk(std::max<int64_t>(nch, 1)), ghosts(std::max<int64_t>(ngh, 1));
+    parallel_for(nb, [&](int64_t b) {
+        const FeaBlock& B = blocks[b];
+        std::copy(bo[b].cols.begin(), bo[b].cols.end(), c->col_idx.begin() + B.slot0);
+        std::copy(bo[b].counts.begin(), bo[b].counts.end(), counts.begin() + B.slot0);
+        std::copy(bo[b].contrib.begin(), bo[b].contrib.end(), contrib.begin() + B.contrib0);
+        std::copy(bo[b].chunk.begin(), bo[b].chunk.end(), chunk.begin() + B.chunk0);
+        std::copy(bo[b].ghosts.begin(), bo[b].ghosts.end(), ghosts.begin() + B.ghost0);
+        for (int64_t r = brow[b]; r < brow[b + 1]; ++r) c->row_ptr[r + 1] = bo[b].rownnz[r - brow[b]];
+    });
+    for (int64_t r = 0; r < nr; ++r) c->row_ptr[r + 1] += c->row_ptr[r];
+    bo.clear();
+
+    c->nblocks = (int)nb;
+    c->e_max = (int)e_max;
+    c->nnz = nnz;
+    c->smem_bytes = (int)(tab_bytes + e_max * per_el);
+    c->stat_visits = visits;
+    c->stat_owned = owned;
+    c->stat_entries = ncon;
+    if (c->host_only) {
+        c->have_plan = true;
+        if (row_begin) *row_begin = R0;
+        if (n_rows_local) *n_rows_local = nr;
+        if (nnz_local) *nnz_local = nnz;
+        return FEA_OK;
+    }
+    // device upload
+    auto up = [&](auto*& dst, const auto& v) -> fea_status {
+        using T_ = typename std::remove_reference<decltype(v)>::type::value_type;
+        FEA_CUDA(c, cudaMalloc((void**)&dst, std::max<size_t>(1, v.size()) * sizeof(T_)));
+        if (!v.empty()) FEA_CUDA(c, cudaMemcpy((void*)dst, v.data(), v.size() * sizeof(T_), cudaMemcpyHostToDevice));
+        return FEA_OK;
+    };
+    fea_status st;
+    if ((st = up(c->d_blocks, blocks)) != FEA_OK) return st;
+    if ((st = up(c->d_counts, counts)) != FEA_OK) return st;
+    if ((st = up(c->d_contrib, contrib)) != FEA_OK) return st;
+    if ((st = up(c->d_chunk, chunk)) != FEA_OK) return st;
+    if ((st = up(c->d_ghosts, ghosts)) != FEA_OK) return st;
+    if (!c->d_ufull) FEA_CUDA(c, cudaMalloc(&c->d_ufull, (size_t)rpr * c->world * sizeof(double)));
+    if (!c->d_usend) FEA_CUDA(c, cudaMalloc(&c->d_usend, (size_t)rpr * sizeof(double)));
+
+    int tc = (int)c->tune_tchunks;
+    if (tc <= 0) tc = c->order == 4 ? 4 : c->order == 3 ? 2 : 1;
+    c->ntc = c->staged ? tc : 1;
+    int occ = 0;
+    const int dm = (c->plan_which & FEA_MASS) ? 1 : 0, dc = (c->plan_which & FEA_STIFF) ? 1 : 0;
+    int rc = fea_kernel_occupancy(c->order, c->nq, dm, dc, c->staged, c->threads, c->smem_bytes, &occ);
+    if (rc != 0) return c->fail(FEA_E_CUDA, "occupancy query: %s", cudaGetErrorString((cudaError_t)rc));
+    if (occ < 1) return c->fail(FEA_E_UNSUPPORTED, "kernel does not fit: %d B shared memory", c->smem_bytes);
+    c->grid = (int)std::min<int64_t>(std::max<int64_t>(nb, 1), (int64_t)occ * c->sm_count);
+    c->have_plan = true;
+    if (row_begin) *row_begin = R0;
+    if (n_rows_local) *n_rows_local = nr;
+    if (nnz_local) *nnz_local = nnz;
+    return FEA_OK;
+}
+
+fea_status fea_get_pattern(fea_ctx c, int64_t* row_ptr, int32_t* col_idx) {
+    if (!c) return FEA_E_ARG;
+    if (!c->have_plan) return c->fail(FEA_E_STATE, "get_pattern before build_pattern");
+    if (row_ptr) std::memcpy(row_ptr, c->row_ptr.data(), c->row_ptr.size() * sizeof(int64_t));
+    if (col_idx && c->nnz) std::memcpy(col_idx, c->col_idx.data(), c->col_idx.size() * sizeof(int32_t));
+    return FEA_OK;
+}
+
+fea_status fea_get_dof_perm(fea_ctx c, int64_t* lib_to_user) {
+    if (!c || !lib_to_user) return FEA_E_ARG;
+    if (!c->have_mesh) return c->fail(FEA_E_STATE, "get_dof_perm before mesh_upload");
+    std::memcpy(lib_to_user, c->dof_lib2user.data(), c->dof_lib2user.size() * sizeof(int64_t));
+    return FEA_OK;
+}
+
+fea_status fea_get_elem_perm(fea_ctx c, int64_t* lib_to_user) {
+    if (!c || !lib_to_user) return FEA_E_ARG;
+    if (!c->have_mesh) return c->fail(FEA_E_STATE, "get_elem_perm before mesh_upload");
+    std::memcpy(lib_to_user, c->elem_lib2user.data(), c->elem_lib2user.size() * sizeof(int64_t));
+    return FEA_OK;
+}
+
+fea_status fea_set_coefficient(fea_ctx c, int which, int kind, int n_par, const double* par) {
+    if (!c) return FEA_E_ARG;
+    if (which < 1 || which > 3) return c->fail(FEA_E_ARG, "which must be a nonzero FEA_MASS|FEA_STIFF mask");
+    if (n_par < 1 || n_par > FEA_MAX_PAR || !par) return c->fail(FEA_E_ARG, "bad coefficient parameters");
+    if (kind == FEA_K_POLY && n_par > 9) return c->fail(FEA_E_ARG, "polynomial degree > 8");
+    if (kind == FEA_K_EXP && n_par != 2) return c->fail(FEA_E_ARG, "FEA_K_EXP takes 2 parameters");
+    if (kind == FEA_K_PWL) {
+        if (n_par % 2 || n_par < 4) return c->fail(FEA_E_ARG, "FEA_K_PWL takes 2..8 (T, k) pairs");
+        for (int i = 2; i < n_par; i += 2)
+            if (!(par[i] > par[i - 2])) return c->fail(FEA_E_ARG, "FEA_K_PWL breakpoints must increase");
+    }
+    if (kind < 0 || kind > 2) return c->fail(FEA_E_ARG, "unknown coefficient kind %d", kind);
+    FeaCoef k{};
+    k.kind = kind;
+    k.npar = n_par;
+    for (int i = 0; i < n_par; ++i) k.par[i] = par[i];
+    if (which & FEA_MASS) c->coef_m = k;
+    if (which & FEA_STIFF) c->coef_c = k;
+    return FEA_OK;
+}
+
+static bool same_coef(const FeaCoef& a, const FeaCoef& b) {
+    if (a.kind != b.kind || a.npar != b.npar) return false;
+    for (int i = 0; i < a.npar; ++i)
+        if (a.par[i] != b.par[i]) return false;
+    return true;
+}
+
+static fea_status launch(fea_ctx c, const double* u, double* vm, double* vc) {
+    FeaKParams prm{};
+    prm.blocks = c->d_blocks;
+    prm.nblocks = c->nblocks;
+    prm.e_max = c->e_max;
+    prm.dofT = c->d_dofT;
+    prm.n_e = c->n_e;
+    prm.xy = c->d_xy;
+    prm.u = u;
+    prm.counts = c->d_counts;
+    prm.contrib = c->d_contrib;
+    prm.chunk_base = c->d_chunk;
+    prm.ghosts = c->d_ghosts;
+    prm.tables = c->d_tables;
+    prm.tables_doubles = (int32_t)c->tables.size();
+    prm.nq = c->nq;
+    prm.ntc = c->ntc;
+    prm.same_coef = same_coef(c->coef_m, c->coef_c) ? 1 : 0;
+    prm.coef_m = c->coef_m;
+    prm.coef_c = c->coef_c;
+    prm.out_m = vm;
+    prm.out_c = vc;
+    if (c->nblocks == 0) return FEA_OK;
+    const int rc = fea_launch_reassemble(prm, c->order, c->threads, c->smem_bytes, c->grid, c->staged, c->stream);
+    if (rc != 0) return c->fail(FEA_E_CUDA, "k_reassemble launch: %s", cudaGetErrorString((cudaError_t)rc));
+    return FEA_OK;
+}
+
+fea_status fea_assemble(fea_ctx c, const double* u_full, double* mass_vals, double* stiff_vals) {
+    if (!c) return FEA_E_ARG;
+    if (c->host_only) return c->fail(FEA_E_STATE, "host-only (planning) context has no device");
+    if (!c->have_plan) return c->fail(FEA_E_STATE, "assemble before build_pattern");
+    if (!u_full) return c->fail(FEA_E_ARG, "u_full is NULL");
+    if ((mass_vals && ((uintptr_t)mass_vals & 15)) || (stiff_vals && ((uintptr_t)stiff_vals & 15)))
+        return c->fail(FEA_E_ARG, "vals must be 16-byte aligned");
+    if (!mass_vals && !stiff_vals) return FEA_OK;
+    cudaSetDevice(c->device);
+    const bool pm = c->plan_which & FEA_MASS, pc = c->plan_which & FEA_STIFF;
+    fea_status s;
+    if (mass_vals && stiff_vals && !(pm && pc)) {  // plan sized for one matrix: two passes
+        if ((s = launch(c, u_full, mass_vals, nullptr)) != FEA_OK) return s;
+        return launch(c, u_full, nullptr, stiff_vals);
+    }
+    return launch(c, u_full, mass_vals, stiff_vals);
+}
+
+fea_status fea_assemble_mass(fea_ctx c, const double* u_full, double* vals) {
+    if (!vals) return c ? c->fail(FEA_E_ARG, "vals is NULL") : FEA_E_ARG;
+    return fea_assemble(c, u_full, vals, nullptr);
+}
+
+fea_status fea_assemble_stiffness(fea_ctx c, const double* u_full, double* vals) {
+    if (!vals) return c ? c->fail(FEA_E_ARG, "vals is NULL") : FEA_E_ARG;
+    return fea_assemble(c, u_full, nullptr, vals);
+}
+
+fea_status fea_reassemble(fea_ctx c, const double* u_owned, double* mass_vals, double* stiff_vals) {
+    if (!c) return FEA_E_ARG;
+    if (c->host_only) return c->fail(FEA_E_STATE, "host-only (planning) context has no device");
+    if (!c->have_plan) return c->fail(FEA_E_STATE, "reassemble before build_pattern");
+    if (!u_owned) return c->fail(FEA_E_ARG, "u_owned is NULL");
+    cudaSetDevice(c->device);
+    if (c->world == 1) return fea_assemble(c, u_owned, mass_vals, stiff_vals);
+    if (!c->comm) return c->fail(FEA_E_STATE, "world > 1 requires fea_set_nccl");
+    // pad the owned slice to rows_per_rank, then allgather (the only cross-GPU traffic)
+    if (c->n_rows)
+        FEA_CUDA(c, cudaMemcpyAsync(c->d_usend, u_owned, c->n_rows * sizeof(double), cudaMemcpyDeviceToDevice, c->stream));
+    ncclResult_t r = nccl().allGather(c->d_usend, c->d_ufull, (size_t)c->rows_per_rank, ncclDouble,
+                                      (ncclComm_t)c->comm, c->stream);
+    if (r != ncclSuccess) return c->fail(FEA_E_NCCL, "ncclAllGather: %s", nccl().getErrorString(r));
+    return fea_assemble(c, c->d_ufull, mass_vals, stiff_vals);
+}
+
+fea_status fea_reassemble_host(fea_ctx c, const double* u_host, double* mass_host, double* stiff_host) {
+    if (!c) return FEA_E_ARG;
+    if (c->host_only) return c->fail(FEA_E_STATE, "host-only (planning) context has no device");
+    if (!c->have_plan) return c->fail(FEA_E_STATE, "reassemble before build_pattern");
+    if (!u_host) return c->fail(FEA_E_ARG, "u_host is NULL");
+    cudaSetDevice(c->device);
+    if (mass_host && !c->d_vm) FEA_CUDA(c, cudaMalloc(&c->d_vm, std::max<int64_t>(1, c->nnz) * sizeof(double)));
+    if (stiff_host && !c->d_vc) FEA_CUDA(c, cudaMalloc(&c->d_vc, std::max<int64_t>(1, c->nnz) * sizeof(double)));
+    double* dst = c->world == 1 ? c->d_ufull : c->d_usend;
+    const int64_t n = c->world == 1 ? c->n_dof : c->n_rows;
+    FEA_CUDA(c, cudaMemcpyAsync(dst, u_host, n * sizeof(double), cudaMemcpyHostToDevice, c->stream));
+    fea_status s;
+    if (c->world == 1) s = fea_assemble(c, c->d_ufull, mass_host ? c->d_vm : nullptr, stiff_host ? c->d_vc : nullptr);
+    else {
+        if (!c->comm) return c->fail(FEA_E_STATE, "world > 1 requires fea_set_nccl");
+        ncclResult_t r = nccl().allGather(c->d_usend, c->d_ufull, (size_t)c->rows_per_rank, ncclDouble,
+                                          (ncclComm_t)c->comm, c->stream);
+        if (r != ncclSuccess) return c->fail(FEA_E_NCCL, "ncclAllGather: %s", nccl().getErrorString(r));
+        s = fea_assemble(c, c->d_ufull, mass_host ? c->d_vm : nullptr, stiff_host ? c->d_vc : nullptr);
+    }
+    if (s != FEA_OK) return s;
+    if (mass_host) FEA_CUDA(c, cudaMemcpyAsync(mass_host, c->d_vm, c->nnz * sizeof(double), cudaMemcpyDeviceToHost, c->stream));
+    if (stiff_host) FEA_CUDA(c, cudaMemcpyAsync(stiff_host, c->d_vc, c->nnz * sizeof(double), cudaMemcpyDeviceToHost, c->stream));
+    FEA_CUDA(c, cudaStreamSynchronize(c->stream));
+    return FEA_OK;
+}
+
+fea_status fea_nccl_unique_id(void* id_out) {
+    if (!id_out) return FEA_E_ARG;
+    if (!nccl().ok) return FEA_E_NCCL;
+    ncclUniqueId id;
+    if (nccl().getUniqueId(&id) != ncclSuccess) return FEA_E_NCCL;
+    std::memcpy(id_out, &id, sizeof(id));
+    return FEA_OK;
+}
+
+fea_status fea_set_nccl(fea_ctx c, const void* id_bytes) {
+    if (!c || !id_bytes) return FEA_E_ARG;
+    if (c->host_only) return c->fail(FEA_E_STATE, "host-only (planning) context has no device");
+    if (!nccl().ok) return c->fail(FEA_E_NCCL, "libnccl.so.2 could not be loaded");
+    cudaSetDevice(c->device);
+    ncclUniqueId id;
+    std::memcpy(&id, id_bytes, sizeof(id));
+    ncclComm_t comm;
+    ncclResult_t r = nccl().commInitRank(&comm, c->world, id, c->rank);
+    if (r != ncclSuccess) return c->fail(FEA_E_NCCL, "ncclCommInitRank: %s", nccl().getErrorString(r));
+    if (c->comm) nccl().commDestroy((ncclComm_t)c->comm);
+    c->comm = comm;
+    return FEA_OK;
+}
+
+fea_status fea_sync(fea_ctx c) {
+    if (!c) return FEA_E_ARG;
+    if (c->host_only) return c->fail(FEA_E_STATE, "host-only (planning) context has no device");
+    cudaSetDevice(c->device);
+    FEA_CUDA(c, cudaStreamSynchronize(c->stream));
+    FEA_CUDA(c, cudaGetLastError());
+    return FEA_OK;
+}
+
+fea_status fea_get_stat(fea_ctx c, int key, int64_t* value) {
+    if (!c || !value) return FEA_E_ARG;
+    if (!c->have_plan) return c->fail(FEA_E_STATE, "no plan");
+    switch (key) {
+        case 1: *value = c->nblocks; break;
+        case 2: *value = c->stat_visits; break;
+        case 3: *value = c->stat_owned; break;
+        case 4: *value = c->stat_entries; break;
+        case 5: *value = c->launches_per_call; break;
+        case 6: *value = c->smem_bytes; break;
+        case 7: *value = c->e_max; break;
+        case 8: *value = c->grid; break;
+        default: return c->fail(FEA_E_ARG, "unknown stat key %d", key);
+    }
+    return FEA_OK;
+}
+
+}  // extern "C"

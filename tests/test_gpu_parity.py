@@ -1,0 +1,188 @@
+"""GPU parity: the CUDA path (through the C ABI) vs the oracle on the same seeded inputs.
+
+Bar (BASELINE.json north_star, reading 12): CSR row_ptr / col_idx bit-exact; values
+max|gpu - oracle| <= 1e-12 * max|oracle| per matrix, FP64.
+"""
+import numpy as np
+import pytest
+
+import oracle
+from fea_inputs import CONFIGS, K_EXP, K_POLY, K_PWL, MASS, STIFF, make_workload, scaled, single_element_mesh, \
+    structured_mesh, triangle_rule, two_element_mesh
+from fea_inputs.mesh import random_mesh_from_structured
+from tests.helpers import coef_of, library_assemble, maxabs_rel, oracle_for
+
+pytestmark = pytest.mark.gpu
+TOL = 1e-12
+
+
+def _check(res, ref, which):
+    assert np.array_equal(res["row_ptr"], ref.row_ptr), "row_ptr not bit-exact"
+    assert np.array_equal(res["col_idx"], ref.col_idx), "col_idx not bit-exact"
+    if which & MASS:
+        assert np.isfinite(res["M"]).all()
+        assert maxabs_rel(res["M"], ref.M) <= TOL, maxabs_rel(res["M"], ref.M)
+    if which & STIFF:
+        assert np.isfinite(res["K"]).all()
+        assert maxabs_rel(res["K"], ref.K) <= TOL, maxabs_rel(res["K"], ref.K)
+
+
+# configs at sizes the oracle finishes in seconds; several CTA blocks and a ragged tail each
+SMALL = [("C1", 32), ("C2", 48), ("C3", 24), ("C4", 96), ("C5", 12)]
+
+
+@pytest.mark.parametrize("name,N", SMALL)
+def test_config_parity_small(name, N):
+    cfg = scaled(CONFIGS[name], N)
+    w = make_workload(cfg)
+    coef = coef_of(cfg)
+    for u in w.u_sequence(min(cfg.reassemblies, 2)):
+        res = library_assemble(w.mesh, w.q_xy, w.q_w, u, cfg.p, coef, coef, which=cfg.which)
+        assert res["ctx"].stat(1) >= 2  # several blocks
+        ref = oracle_for(w.mesh, w.q_xy, w.q_w, u, res["perm"], coef, coef, cfg.which)
+        _check(res, ref, cfg.which)
+
+
+@pytest.mark.parametrize("p", [1, 2, 3, 4])
+def test_single_and_two_element_meshes(p):
+    for m in (single_element_mesh((0.0, 0.0), (1.0, 0.0), (0.0, 1.0), p=p),
+              single_element_mesh((0.3, -0.2), (1.7, 0.4), (0.1, 2.0), p=p),
+              single_element_mesh((0.0, 0.0), (0.0, 1.0), (1.0, 0.0), p=p)):  # clockwise
+        xy, w = triangle_rule(2 * p)
+        u = np.random.default_rng(p).uniform(-1, 1, m.n_dof)
+        coef = (K_POLY, (1.0, 0.0, 1.0))
+        res = library_assemble(m, xy, w, u, p, coef, coef)
+        _check(res, oracle_for(m, xy, w, u, res["perm"], coef, coef, 3), 3)
+    if p == 1:
+        m = two_element_mesh()
+        xy, w = triangle_rule(2)
+        res = library_assemble(m, xy, w, np.zeros(4), 1, (K_POLY, (1.0,)), (K_POLY, (1.0,)))
+        _check(res, oracle_for(m, xy, w, np.zeros(4), res["perm"], (K_POLY, (1.0,)), (K_POLY, (1.0,)), 3), 3)
+
+
+@pytest.mark.parametrize("p", [1, 2, 3, 4])
+def test_distinct_coefficients_generic_rule_and_modes(p):
+    """M and C with different k (two Lambda), a non-native rule (generic kernel), PWL k,
+    mass-only and stiffness-only launches, user numbering (no reorder)."""
+    m = random_mesh_from_structured(7, p, seed=50 + p)
+    u = np.random.default_rng(p).uniform(-1, 1, m.n_dof)
+    km, kc = (K_EXP, (1.3, 0.5)), (K_PWL, (-1.0, 1.5, 0.0, 0.7, 1.0, 0.5))
+    for deg in sorted({2 * p, min(8, 2 * p + 2)}):
+        xy, w = triangle_rule(deg)
+        for which in (MASS | STIFF, MASS, STIFF):
+            for reorder in (True, False):
+                res = library_assemble(m, xy, w, u, p, km, kc, which=which, reorder=reorder)
+                _check(res, oracle_for(m, xy, w, u, res["perm"], km, kc, which), which)
+
+
+@pytest.mark.parametrize("p", [1, 2, 3, 4])
+def test_deterministic_across_runs_and_tilings(p):
+    """Bit-identical values across repeated runs and across CTA tilings (smem budgets):
+    per-slot summation in ascending library element order (reading 11)."""
+    m = random_mesh_from_structured(10, p, seed=70 + p)
+    xy, w = triangle_rule(2 * p)
+    u = np.random.default_rng(p).uniform(0, 1, m.n_dof)
+    coef = (K_POLY, (1.0, 0.0, 0.0, 0.0, 1.0))
+    base = library_assemble(m, xy, w, u, p, coef, coef)
+    again = library_assemble(m, xy, w, u, p, coef, coef)
+    assert np.array_equal(base["M"], again["M"]) and np.array_equal(base["K"], again["K"])
+    budgets = {1: [8192, 16384], 2: [16384, 40000], 3: [40000, 100000], 4: [100000, 130000]}[p]
+    for b in budgets:
+        r = library_assemble(m, xy, w, u, p, coef, coef, tuning={1: b})
+        assert r["ctx"].stat(1) > max(1, base["ctx"].stat(1) // 2)  # a different, finer tiling
+        assert np.array_equal(base["M"], r["M"]) and np.array_equal(base["K"], r["K"])
+    r = library_assemble(m, xy, w, u, p, coef, coef, tuning={2: 128})
+    assert np.array_equal(base["M"], r["M"]) and np.array_equal(base["K"], r["K"])
+
+
+@pytest.mark.parametrize("p,world", [(1, 2), (2, 3), (3, 4), (4, 2)])
+def test_fake_world_bit_identical(p, world):
+    """Row partition over `world` ranks (each rank: its rows + ghost elements), run one rank
+    after another on one GPU with the full u: concatenated rows are bit-identical to world 1."""
+    m = random_mesh_from_structured(9, p, seed=90 + p)
+    xy, w = triangle_rule(2 * p)
+    u = np.random.default_rng(p).uniform(0, 1, m.n_dof)
+    coef = (K_POLY, (1.0, 0.0, 1.0))
+    base = library_assemble(m, xy, w, u, p, coef, coef)
+    Ms, Ks, rps, cis = [], [], [], []
+    nxt = 0
+    for r in range(world):
+        res = library_assemble(m, xy, w, u, p, coef, coef, rank=r, world=world)
+        assert res["row_begin"] == nxt
+        nxt += res["n_rows"]
+        Ms.append(res["M"])
+        Ks.append(res["K"])
+        cis.append(res["col_idx"])
+        rps.append(res["row_ptr"][1:] + (rps[-1][-1] if rps else 0))
+    assert nxt == m.n_dof
+    assert np.array_equal(np.concatenate([[0]] + rps), base["row_ptr"])
+    assert np.array_equal(np.concatenate(cis), base["col_idx"])
+    assert np.array_equal(np.concatenate(Ms), base["M"]) and np.array_equal(np.concatenate(Ks), base["K"])
+
+
+def test_permutation_export_against_user_numbering():
+    """Oracle in USER numbering, mapped through lib_to_user, equals the library result."""
+    cfg = scaled(CONFIGS["C4"], 40)
+    wl = make_workload(cfg)
+    coef = coef_of(cfg)
+    res = library_assemble(wl.mesh, wl.q_xy, wl.q_w, wl.u0, 1, coef, coef, which=STIFF)
+    ref = oracle.assemble(wl.mesh, wl.q_xy, wl.q_w, wl.u0, m_coef=coef, c_coef=coef, which=STIFF)
+    perm = res["perm"]
+    n = wl.mesh.n_dof
+    Du = ref.dense("K", n)
+    Dl = np.zeros((n, n))
+    for r in range(n):
+        a, b = res["row_ptr"][r], res["row_ptr"][r + 1]
+        Dl[r, res["col_idx"][a:b]] = res["K"][a:b]
+    assert np.abs(Dl - Du[np.ix_(perm, perm)]).max() <= TOL * np.abs(Du).max()
+
+
+def test_error_paths():
+    import torch
+    from paper_2204_03893_b200.fea import Context, FeaError
+    ctx = Context(device=0)
+    xy, w = triangle_rule(2)
+    with pytest.raises(FeaError, match="FEA_E_ARG"):
+        ctx.set_element(1, xy, w * 2)  # weights sum to 1, not 1/2
+    with pytest.raises(FeaError, match="FEA_E_UNSUPPORTED"):
+        ctx.set_element(5, xy, w)
+    with pytest.raises(FeaError, match="FEA_E_STATE"):
+        ctx.mesh_upload(np.zeros((3, 2)), np.zeros((1, 3)), 3, np.zeros((1, 3)))
+    ctx.set_element(1, xy, w)
+    with pytest.raises(FeaError, match="degenerate element 0"):
+        ctx.mesh_upload(np.array([[0.0, 0], [1, 0], [2, 0]]), np.array([[0, 1, 2]]), 3, np.array([[0, 1, 2]]))
+    m = structured_mesh(3, 1)
+    ctx.mesh_upload(m.vert_xy, m.elem_vert, m.n_dof, m.elem_dof)
+    u = torch.zeros(m.n_dof, dtype=torch.float64, device="cuda")
+    with pytest.raises(FeaError, match="FEA_E_STATE"):
+        ctx.assemble(u, torch.zeros(100, dtype=torch.float64, device="cuda"))
+    ctx.build_pattern()
+    buf = torch.zeros(ctx.nnz + 1, dtype=torch.float64, device="cuda")
+    with pytest.raises(FeaError, match="16-byte aligned"):
+        ctx.assemble(u, buf[1:])
+    m3 = structured_mesh(2, 3)
+    ctx.set_element(3, *triangle_rule(6))
+    bad = m3.elem_dof.copy()
+    bad[0, [3, 4]] = bad[0, [4, 3]]  # wrong edge orientation in element 0
+    with pytest.raises(FeaError, match="inconsistently"):
+        ctx.mesh_upload(m3.vert_xy, m3.elem_vert, m3.n_dof, bad)
+    ctx.close()
+
+
+def test_reassemble_and_host_entry_points():
+    cfg = scaled(CONFIGS["C2"], 20)
+    wl = make_workload(cfg)
+    import torch
+    from paper_2204_03893_b200 import Assembler
+    coef = coef_of(cfg)
+    asm = Assembler(cfg.p, wl.q_xy, wl.q_w, wl.mesh.vert_xy, wl.mesh.elem_vert, wl.mesh.n_dof, wl.mesh.elem_dof,
+                    coef_m=coef, coef_c=coef)
+    u_lib = asm.to_library(wl.u0)
+    M, K = asm.reassemble(torch.tensor(u_lib, device="cuda"))
+    asm.ctx.sync()
+    Mh = np.zeros(asm.nnz)
+    Kh = np.zeros(asm.nnz)
+    asm.ctx.reassemble_host(u_lib, Mh, Kh)
+    assert np.array_equal(Mh, M.cpu().numpy()) and np.array_equal(Kh, K.cpu().numpy())
+    ref = oracle_for(wl.mesh, wl.q_xy, wl.q_w, wl.u0, asm.lib_to_user, coef, coef, 3)
+    assert maxabs_rel(Mh, ref.M) <= TOL and maxabs_rel(Kh, ref.K) <= TOL
