@@ -85,7 +85,6 @@ struct fea_ctx_s {
     std::vector<int32_t> ed;        // [n_e][np] library DOFs, library element order
     std::vector<int32_t> elem_min;  // min library DOF per library element
     std::vector<double> dxy;        // [n_dof][2]
-    int32_t* d_dofT = nullptr;
     double2* d_xy = nullptr;
     double* d_tables = nullptr;
 
@@ -96,11 +95,10 @@ struct fea_ctx_s {
     std::vector<int64_t> row_ptr;
     std::vector<int32_t> col_idx;
     FeaBlock* d_blocks = nullptr;
-    uint8_t* d_counts = nullptr;
-    uint16_t* d_contrib = nullptr;
-    int32_t* d_chunk = nullptr;
-    int32_t* d_ghosts = nullptr;
-    int nblocks = 0, e_max = 0, smem_bytes = 0, threads = 256, ntc = 1, staged = 0, grid = 0;
+    uint8_t* d_records = nullptr;
+    int nblocks = 0, e_max = 0, rec_max = 0, smem_bytes = 0, threads = 256, ntc = 1, staged = 0, grid = 0;
+    int32_t lay[10] = {0};
+    int64_t record_bytes = 0;
     int64_t stat_visits = 0, stat_owned = 0, stat_entries = 0;
     int launches_per_call = 1;
 
@@ -128,10 +126,7 @@ struct fea_ctx_s {
     }
     void free_plan() {
         dfree(d_blocks);
-        dfree(d_counts);
-        dfree(d_contrib);
-        dfree(d_chunk);
-        dfree(d_ghosts);
+        dfree(d_records);
         dfree(d_vm);
         dfree(d_vc);
         row_ptr.clear();
@@ -140,7 +135,6 @@ struct fea_ctx_s {
     }
     void free_mesh() {
         free_plan();
-        dfree(d_dofT);
         dfree(d_xy);
         dfree(d_ufull);
         dfree(d_usend);
@@ -208,8 +202,8 @@ bool invert(std::vector<long double>& A, int n) {
 // Tables (Algorithm 2 lines 1-3), symmetric rows only:
 //   Phi[i][q]             = phi_i(x_q)
 //   w[q]
-//   Q[t][0][q] = Phi_i Phi_j                      (rows of Q_m = Phi (.) Phi)
-//   Q[t][1][q] = J_i0 J_j0, Q[t][2][q] = J_i1 J_j1, Q[t][3][q] = J_i0 J_j1 + J_i1 J_j0
+//   Q[t][q][0] = Phi_i Phi_j                      (rows of Q_m = Phi (.) Phi)
+//   Q[t][q][1] = J_i0 J_j0, Q[t][q][2] = J_i1 J_j1, Q[t][q][3] = J_i0 J_j1 + J_i1 J_j0
 //                                                 (rows of Q_c = [J_q (x) J_q], columns of vec A
 //                                                  merged by the symmetry A01 = A10)
 bool build_tables(int p, int nq, const double* qxy, const double* qw, std::vector<double>& tab) {
@@ -242,19 +236,22 @@ bool build_tables(int p, int nq, const double* qxy, const double* qw, std::vecto
         }
     }
     const int T = np * (np + 1) / 2;
-    tab.assign((size_t)np * nq + nq + (size_t)T * 4 * nq, 0.0);
+    // layout (kernel view): Phi at 0, w at pad2(np nq), Q[T][nq][4] at pad2(np nq) + pad2(nq)
+    const size_t oW = ((size_t)np * nq + 1) & ~size_t(1), oQ = oW + (((size_t)nq + 1) & ~size_t(1));
+    tab.assign(oQ + (size_t)T * nq * 4, 0.0);
     for (int i = 0; i < np * nq; ++i) tab[i] = (double)phi[i];
-    for (int q = 0; q < nq; ++q) tab[np * nq + q] = qw[q];
-    double* Q = tab.data() + np * nq + nq;
+    for (int q = 0; q < nq; ++q) tab[oW + q] = qw[q];
+    double* Q = tab.data() + oQ;
     for (int i = 0; i < np; ++i)
         for (int j = i; j < np; ++j) {
             const int t = tri_index(np, i, j);
             for (int q = 0; q < nq; ++q) {
                 const int a = i * nq + q, b = j * nq + q;
-                Q[(t * 4 + 0) * nq + q] = (double)(phi[a] * phi[b]);
-                Q[(t * 4 + 1) * nq + q] = (double)(gx[a] * gx[b]);
-                Q[(t * 4 + 2) * nq + q] = (double)(gy[a] * gy[b]);
-                Q[(t * 4 + 3) * nq + q] = (double)(gx[a] * gy[b] + gy[a] * gx[b]);
+                double* o = Q + ((size_t)t * nq + q) * 4;
+                o[0] = (double)(phi[a] * phi[b]);
+                o[1] = (double)(gx[a] * gx[b]);
+                o[2] = (double)(gy[a] * gy[b]);
+                o[3] = (double)(gx[a] * gy[b] + gy[a] * gx[b]);
             }
         }
     return true;
@@ -473,12 +470,7 @@ fea_status fea_mesh_upload(fea_ctx c, int64_t n_vert, const double* vert_xy, int
         c->have_mesh = true;
         return FEA_OK;
     }
-    // device: SoA DOF map and coordinates
-    std::vector<int32_t> dofT((size_t)n_elem * np);
-    for (int64_t l = 0; l < n_elem; ++l)
-        for (int i = 0; i < np; ++i) dofT[(size_t)i * n_elem + l] = c->ed[(size_t)l * np + i];
-    FEA_CUDA(c, cudaMalloc(&c->d_dofT, dofT.size() * sizeof(int32_t)));
-    FEA_CUDA(c, cudaMemcpy(c->d_dofT, dofT.data(), dofT.size() * sizeof(int32_t), cudaMemcpyHostToDevice));
+    // device: DOF coordinates (vertex DOFs give B_e); the DOF map travels in the block records
     FEA_CUDA(c, cudaMalloc(&c->d_xy, n_dof * sizeof(double2)));
     FEA_CUDA(c, cudaMemcpy(c->d_xy, c->dxy.data(), n_dof * sizeof(double2), cudaMemcpyHostToDevice));
     c->have_mesh = true;
@@ -525,19 +517,20 @@ fea_status fea_build_pattern(fea_ctx c, int64_t* row_begin, int64_t* n_rows_loca
     c->row_begin = R0;
     c->n_rows = nr;
 
-    // kernel configuration
-    const int nmat = (c->plan_which & FEA_MASS ? 1 : 0) + (c->plan_which & FEA_STIFF ? 1 : 0);
+    // ---- shared-memory budget -> elements per block (e_max) and record budget
+    const int dm = (c->plan_which & FEA_MASS) ? 1 : 0, dcm = (c->plan_which & FEA_STIFF) ? 1 : 0;
+    const int nmat = dm + dcm;
     c->staged = c->order >= 3 ? 1 : 0;
     c->threads = (int)c->tune_threads;
-    int64_t budget = c->tune_smem ? c->tune_smem : (c->order >= 3 ? 200 * 1024 : 96 * 1024);
-    const int64_t tab_bytes = (int64_t)((c->tables.size() + 1) & ~size_t(1)) * 8;
-    const int nlam = 2;  // worst case (distinct coefficients for M and C)
-    const int64_t per_el = (int64_t)T * nmat * 8 + (c->staged ? (int64_t)(nlam * nq + 3) * 8 : 0);
-    int64_t e_max = (budget - tab_bytes) / per_el;
+    const int64_t budget = c->tune_smem ? c->tune_smem : (c->order >= 3 ? 225 * 1024 : 110 * 1024);
+    const int64_t tab_bytes = (int64_t)((c->tables.size() * 8 + 15) & ~size_t(15));
+    const int64_t per_el_smem = 8LL * T * nmat + 8LL * np + 48 + (c->staged ? 8LL * (2 * nq + 3) : 0);
+    const double rec_el = 1.3 * (3.125 * np * np + 4.0 * np);  // record bytes per element (estimate)
+    int64_t e_max = (int64_t)((budget - tab_bytes - 64) / (per_el_smem + 2.0 * rec_el));
     e_max = std::min<int64_t>(e_max, 65535 / T);
-    e_max = std::min<int64_t>(e_max, 1 << 20);
+    const int64_t rec_budget = ((int64_t)(rec_el * e_max) + 15) & ~int64_t(15);
 
-    // incidence of this rank's rows (ascending library element per row)
+    // ---- incidence of this rank's rows (ascending library element per row)
     std::vector<int64_t> iptr(nr + 1, 0);
     for (int64_t e = 0; e < n_e; ++e)
         for (int i = 0; i < np; ++i) {
@@ -557,36 +550,44 @@ fea_status fea_build_pattern(fea_ctx c, int64_t* row_begin, int64_t* n_rows_loca
     int64_t max_inc = 0;
     for (int64_t r = 0; r < nr; ++r) max_inc = std::max(max_inc, iptr[r + 1] - iptr[r]);
     if (max_inc > 255) return c->fail(FEA_E_UNSUPPORTED, "a DOF belongs to %lld elements (> 255)", (long long)max_inc);
-    if (e_max < std::max<int64_t>(max_inc, 1))
+    // one row must fit a block: its elements and its record upper bound
+    const int64_t row_ub_max = max_inc * np * 7 + 4 * np * max_inc + 64;
+    if (e_max < std::max<int64_t>(max_inc, 1) || rec_budget < row_ub_max)
         return c->fail(FEA_E_UNSUPPORTED, "shared-memory budget too small: %lld elements per block", (long long)e_max);
 
-    // greedy row blocks: the element set of each block must fit e_max
-    std::vector<int64_t> brow;  // block row starts (rank-local)
+    // ---- greedy row blocks: elements <= e_max and record upper bound <= rec_budget
+    // record upper bound: slots <= entries, so counts + contrib + chunks <= 3 entries + entries/8
+    std::vector<int64_t> brow;
     {
         std::vector<int32_t> mark(n_e, -1);
         int32_t cur = -1;
-        int64_t nE = 0;
+        int64_t nE = 0, ent = 0;
         for (int64_t r = 0; r < nr; ++r) {
             int64_t add = 0;
             for (int64_t k = iptr[r]; k < iptr[r + 1]; ++k) add += mark[inc[k]] != cur;
-            if (cur < 0 || nE + add > e_max) {
+            const int64_t rent = (iptr[r + 1] - iptr[r]) * np;
+            const int64_t ub = 3 * (ent + rent) + (ent + rent) / 8 + 4 * np * (nE + add + 3) + 64;
+            if (cur < 0 || nE + add > e_max || ub > rec_budget) {
                 ++cur;
                 brow.push_back(r);
                 nE = 0;
+                ent = 0;
                 add = iptr[r + 1] - iptr[r];
             }
             for (int64_t k = iptr[r]; k < iptr[r + 1]; ++k) mark[inc[k]] = cur;
             nE += add;
+            ent += rent;
         }
     }
     const int64_t nb = (int64_t)brow.size();
     brow.push_back(nr);
 
+    // ---- per block: element set, (row, col) records sorted -> slots, contributors, record
     struct BOut {
-        std::vector<int32_t> rownnz, cols, ghosts, chunk;
-        std::vector<uint8_t> counts;
-        std::vector<uint16_t> contrib;
-        int32_t own0 = 0, nown = 0;
+        std::vector<int32_t> rownnz, cols;
+        std::vector<uint8_t> rec;
+        FeaBlock fb{};
+        int64_t nghost = 0, nown = 0;
         std::string err;
     };
     std::vector<BOut> bo(nb);
@@ -599,18 +600,8 @@ fea_status fea_build_pattern(fea_ctx c, int64_t* row_begin, int64_t* n_rows_loca
         for (int64_t r = ra; r < rb; ++r) E.insert(E.end(), inc.begin() + iptr[r], inc.begin() + iptr[r + 1]);
         std::sort(E.begin(), E.end());
         E.erase(std::unique(E.begin(), E.end()), E.end());
-        int64_t ng = 0;
-        while (ng < (int64_t)E.size() && c->elem_min[E[ng]] < ga) ++ng;
-        o.ghosts.assign(E.begin(), E.begin() + ng);
-        o.nown = (int32_t)(E.size() - ng);
-        o.own0 = o.nown ? E[ng] : 0;
-        for (int64_t k = ng; k < (int64_t)E.size(); ++k)
-            if (E[k] != o.own0 + (k - ng) || c->elem_min[E[k]] >= gb) {
-                o.err = "owned elements not contiguous";
-                return;
-            }
-        // records (row, col, le, t) generated in ascending le; stable sort by (row, col)
-        struct Rec { int32_t row, col; int32_t le; int32_t t; };
+        for (int32_t e : E) (c->elem_min[e] < ga ? o.nghost : o.nown)++;
+        struct Rec { int32_t row, col, le, t; };
         std::vector<Rec> recs;
         for (int64_t le = 0; le < (int64_t)E.size(); ++le) {
             const int32_t* d = &c->ed[(size_t)E[le] * np];
@@ -620,75 +611,91 @@ fea_status fea_build_pattern(fea_ctx c, int64_t* row_begin, int64_t* n_rows_loca
                     recs.push_back({d[i], d[j], (int32_t)le, tri_index(np, std::min(i, j), std::max(i, j))});
             }
         }
+        // stable: within a (row, col) slot the contributors stay in ascending le (= library element)
         std::stable_sort(recs.begin(), recs.end(), [](const Rec& x, const Rec& y) {
             return x.row != y.row ? x.row < y.row : x.col < y.col;
         });
+        std::vector<uint8_t> counts;
+        std::vector<uint16_t> contrib;
+        std::vector<int32_t> chunk;
         o.rownnz.assign(rb - ra, 0);
-        o.contrib.reserve(recs.size());
+        contrib.reserve(recs.size());
         size_t k = 0;
         int64_t nslot = 0;
         while (k < recs.size()) {
             size_t k2 = k;
             while (k2 < recs.size() && recs[k2].row == recs[k].row && recs[k2].col == recs[k].col) ++k2;
-            if (nslot % 32 == 0) o.chunk.push_back((int32_t)o.contrib.size());
+            if (nslot % 32 == 0) chunk.push_back((int32_t)contrib.size());
             o.cols.push_back(recs[k].col);
             o.rownnz[recs[k].row - ga]++;
-            o.counts.push_back((uint8_t)(k2 - k));
-            for (size_t m = k; m < k2; ++m) o.contrib.push_back((uint16_t)(recs[m].t * EM + recs[m].le));
+            counts.push_back((uint8_t)(k2 - k));
+            for (size_t m = k; m < k2; ++m) contrib.push_back((uint16_t)(recs[m].t * EM + recs[m].le));
             ++nslot;
             k = k2;
         }
+        FeaBlock& F = o.fb;
+        F.nslots = (int32_t)nslot;
+        F.ncontrib = (int32_t)contrib.size();
+        F.nE = (int32_t)E.size();
+        F.rec_bytes = fea_rec_bytes(F, np);
+        if (F.rec_bytes > rec_budget) {
+            o.err = "record exceeds the shared-memory budget";
+            return;
+        }
+        o.rec.assign(F.rec_bytes, 0);
+        std::memcpy(o.rec.data(), counts.data(), counts.size());
+        std::memcpy(o.rec.data() + fea_rec_off_contrib(F), contrib.data(), 2 * contrib.size());
+        std::memcpy(o.rec.data() + fea_rec_off_chunk(F), chunk.data(), 4 * chunk.size());
+        int32_t* dofs = reinterpret_cast<int32_t*>(o.rec.data() + fea_rec_off_dofs(F));
+        const int32_t nEp = fea_pad4(F.nE);
+        for (int64_t le = 0; le < (int64_t)E.size(); ++le)
+            for (int i = 0; i < np; ++i) dofs[i * nEp + le] = c->ed[(size_t)E[le] * np + i];
+        for (int64_t le = E.size(); le < nEp; ++le)  // padding lanes point at a valid DOF
+            for (int i = 0; i < np; ++i) dofs[i * nEp + le] = dofs[i * nEp];
     });
     for (auto& o : bo)
-        if (!o.err.empty()) return c->fail(FEA_E_MESH, "plan: %s", o.err.c_str());
+        if (!o.err.empty()) return c->fail(FEA_E_UNSUPPORTED, "plan: %s", o.err.c_str());
 
-    // concatenate
+    // ---- concatenate
     std::vector<FeaBlock> blocks(nb);
-    int64_t nnz = 0, ncon = 0, nch = 0, ngh = 0, visits = 0, owned = 0;
+    int64_t nnz = 0, rbytes = 0, ncon = 0, visits = 0, owned = 0, rec_max = 16;
     for (int64_t b = 0; b < nb; ++b) {
         FeaBlock& B = blocks[b];
+        B = bo[b].fb;
         B.slot0 = nnz;
-        B.contrib0 = ncon;
-        B.row0 = (int32_t)brow[b];
-        B.nslots = (int32_t)bo[b].cols.size();
-        B.own0 = bo[b].own0;
-        B.nown = bo[b].nown;
-        B.ghost0 = (int32_t)ngh;
-        B.nghost = (int32_t)bo[b].ghosts.size();
-        B.chunk0 = (int32_t)nch;
-        B.pad = 0;
+        B.rec_off = rbytes;
         nnz += B.nslots;
-        ncon += bo[b].contrib.size();
-        nch += bo[b].chunk.size();
-        ngh += bo[b].ghosts.size();
-        visits += B.nown + B.nghost;
-        owned += B.nown;
+        rbytes += B.rec_bytes;
+        ncon += B.ncontrib;
+        visits += B.nE;
+        owned += bo[b].nown;
+        rec_max = std::max<int64_t>(rec_max, B.rec_bytes);
     }
     if (nnz >= (1ll << 31)) return c->fail(FEA_E_UNSUPPORTED, "nnz %lld >= 2^31 on one rank", (long long)nnz);
     c->row_ptr.assign(nr + 1, 0);
     c->col_idx.resize(nnz);
-    std::vector<uint8_t> counts(nnz);
-    std::vector<uint16_t> contrib(std::max<int64_t>(ncon, 1));
-    std::vector<int32_t> chunk(std::max<int64_t>(nch, 1)), ghosts(std::max<int64_t>(ngh, 1));
+    std::vector<uint8_t> records(std::max<int64_t>(rbytes, 16));
     parallel_for(nb, [&](int64_t b) {
         const FeaBlock& B = blocks[b];
         std::copy(bo[b].cols.begin(), bo[b].cols.end(), c->col_idx.begin() + B.slot0);
-        std::copy(bo[b].counts.begin(), bo[b].counts.end(), counts.begin() + B.slot0);
-        std::copy(bo[b].contrib.begin(), bo[b].contrib.end(), contrib.begin() + B.contrib0);
-        std::copy(bo[b].chunk.begin(), bo[b].chunk.end(), chunk.begin() + B.chunk0);
-        std::copy(bo[b].ghosts.begin(), bo[b].ghosts.end(), ghosts.begin() + B.ghost0);
+        std::memcpy(records.data() + B.rec_off, bo[b].rec.data(), B.rec_bytes);
         for (int64_t r = brow[b]; r < brow[b + 1]; ++r) c->row_ptr[r + 1] = bo[b].rownnz[r - brow[b]];
+        std::vector<uint8_t>().swap(bo[b].rec);
     });
     for (int64_t r = 0; r < nr; ++r) c->row_ptr[r + 1] += c->row_ptr[r];
     bo.clear();
 
+    FeaSmemLayout L = fea_smem_layout((int)c->tables.size(), (int)rec_max, (int)e_max, np, nq, T, dm, dcm, c->staged);
     c->nblocks = (int)nb;
     c->e_max = (int)e_max;
+    c->rec_max = (int)rec_max;
     c->nnz = nnz;
-    c->smem_bytes = (int)(tab_bytes + e_max * per_el);
+    c->smem_bytes = L.total;
+    std::memcpy(c->lay, &L, sizeof(c->lay));
     c->stat_visits = visits;
     c->stat_owned = owned;
     c->stat_entries = ncon;
+    c->record_bytes = rbytes;
     if (c->host_only) {
         c->have_plan = true;
         if (row_begin) *row_begin = R0;
@@ -696,28 +703,18 @@ fea_status fea_build_pattern(fea_ctx c, int64_t* row_begin, int64_t* n_rows_loca
         if (nnz_local) *nnz_local = nnz;
         return FEA_OK;
     }
-    // device upload
-    auto up = [&](auto*& dst, const auto& v) -> fea_status {
-        using T_ = typename std::remove_reference<decltype(v)>::type::value_type;
-        FEA_CUDA(c, cudaMalloc((void**)&dst, std::max<size_t>(1, v.size()) * sizeof(T_)));
-        if (!v.empty()) FEA_CUDA(c, cudaMemcpy((void*)dst, v.data(), v.size() * sizeof(T_), cudaMemcpyHostToDevice));
-        return FEA_OK;
-    };
-    fea_status st;
-    if ((st = up(c->d_blocks, blocks)) != FEA_OK) return st;
-    if ((st = up(c->d_counts, counts)) != FEA_OK) return st;
-    if ((st = up(c->d_contrib, contrib)) != FEA_OK) return st;
-    if ((st = up(c->d_chunk, chunk)) != FEA_OK) return st;
-    if ((st = up(c->d_ghosts, ghosts)) != FEA_OK) return st;
+    // ---- device upload
+    FEA_CUDA(c, cudaMalloc((void**)&c->d_blocks, std::max<int64_t>(nb, 1) * sizeof(FeaBlock)));
+    if (nb) FEA_CUDA(c, cudaMemcpy(c->d_blocks, blocks.data(), nb * sizeof(FeaBlock), cudaMemcpyHostToDevice));
+    FEA_CUDA(c, cudaMalloc((void**)&c->d_records, records.size()));
+    FEA_CUDA(c, cudaMemcpy(c->d_records, records.data(), records.size(), cudaMemcpyHostToDevice));
     if (!c->d_ufull) FEA_CUDA(c, cudaMalloc(&c->d_ufull, (size_t)rpr * c->world * sizeof(double)));
     if (!c->d_usend) FEA_CUDA(c, cudaMalloc(&c->d_usend, (size_t)rpr * sizeof(double)));
-
     int tc = (int)c->tune_tchunks;
     if (tc <= 0) tc = c->order == 4 ? 4 : c->order == 3 ? 2 : 1;
     c->ntc = c->staged ? tc : 1;
     int occ = 0;
-    const int dm = (c->plan_which & FEA_MASS) ? 1 : 0, dc = (c->plan_which & FEA_STIFF) ? 1 : 0;
-    int rc = fea_kernel_occupancy(c->order, c->nq, dm, dc, c->staged, c->threads, c->smem_bytes, &occ);
+    int rc = fea_kernel_occupancy(c->order, c->nq, dm, dcm, c->staged, c->threads, c->smem_bytes, &occ);
     if (rc != 0) return c->fail(FEA_E_CUDA, "occupancy query: %s", cudaGetErrorString((cudaError_t)rc));
     if (occ < 1) return c->fail(FEA_E_UNSUPPORTED, "kernel does not fit: %d B shared memory", c->smem_bytes);
     c->grid = (int)std::min<int64_t>(std::max<int64_t>(nb, 1), (int64_t)occ * c->sm_count);
@@ -781,25 +778,22 @@ static bool same_coef(const FeaCoef& a, const FeaCoef& b) {
 static fea_status launch(fea_ctx c, const double* u, double* vm, double* vc) {
     FeaKParams prm{};
     prm.blocks = c->d_blocks;
+    prm.records = c->d_records;
     prm.nblocks = c->nblocks;
     prm.e_max = c->e_max;
-    prm.dofT = c->d_dofT;
-    prm.n_e = c->n_e;
+    prm.rec_max = c->rec_max;
+    prm.nq = c->nq;
     prm.xy = c->d_xy;
     prm.u = u;
-    prm.counts = c->d_counts;
-    prm.contrib = c->d_contrib;
-    prm.chunk_base = c->d_chunk;
-    prm.ghosts = c->d_ghosts;
     prm.tables = c->d_tables;
     prm.tables_doubles = (int32_t)c->tables.size();
-    prm.nq = c->nq;
     prm.ntc = c->ntc;
     prm.same_coef = same_coef(c->coef_m, c->coef_c) ? 1 : 0;
     prm.coef_m = c->coef_m;
     prm.coef_c = c->coef_c;
     prm.out_m = vm;
     prm.out_c = vc;
+    std::memcpy(prm.lay, c->lay, sizeof(prm.lay));
     if (c->nblocks == 0) return FEA_OK;
     const int rc = fea_launch_reassemble(prm, c->order, c->threads, c->smem_bytes, c->grid, c->staged, c->stream);
     if (rc != 0) return c->fail(FEA_E_CUDA, "k_reassemble launch: %s", cudaGetErrorString((cudaError_t)rc));
@@ -923,6 +917,8 @@ fea_status fea_get_stat(fea_ctx c, int key, int64_t* value) {
         case 6: *value = c->smem_bytes; break;
         case 7: *value = c->e_max; break;
         case 8: *value = c->grid; break;
+        case 9: *value = c->record_bytes; break;
+        case 10: *value = c->rec_max; break;
         default: return c->fail(FEA_E_ARG, "unknown stat key %d", key);
     }
     return FEA_OK;

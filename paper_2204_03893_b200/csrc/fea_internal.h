@@ -8,22 +8,36 @@
 #define FEA_MAX_NQ 16
 #define FEA_MAX_PAR 16
 
-// One unit of CTA work: a contiguous block of library rows [row0, row0 + nrows) whose
-// CSR slots [slot0, slot0 + nslots) are produced by exactly one CTA.  Its element set is
-// the ghost elements (library index < own0, listed in ghosts[ghost0 ...]) followed by the
-// owned contiguous range [own0, own0 + nown) -- i.e. ascending library element order.
+// One unit of CTA work: a contiguous block of library rows whose CSR slots
+// [slot0, slot0 + nslots) are produced by exactly one CTA.  Everything the block streams
+// from HBM sits in ONE contiguous, 16-byte aligned record at rec_off (one TMA bulk copy):
+//   counts   uint8  [nslots]                contributors per slot          (pad16)
+//   contrib  uint16 [ncontrib]              V offsets t * e_max + le       (pad16)
+//   chunk    int32  [ceil(nslots / 32)]     first contributor of each 32-slot chunk (pad16)
+//   dofs     int32  [n_p][pad4(nE)]         library DOFs of the block's elements (SoA)
+// The block's elements (le = 0 .. nE-1) are in ascending library element order: ghost
+// elements (owned by earlier blocks) first, then the block's own elements.
 struct FeaBlock {
-    int64_t slot0;     // first CSR slot (rank-local)
-    int64_t contrib0;  // first entry of this block's contributor stream
-    int32_t row0;      // first row (rank-local)
+    int64_t slot0;
+    int64_t rec_off;   // byte offset of the record
     int32_t nslots;
-    int32_t own0;      // first owned element (library element index)
-    int32_t nown;
-    int32_t ghost0;    // offset into the ghost list
-    int32_t nghost;
-    int32_t chunk0;    // offset into chunk_base (one entry per 32 slots)
-    int32_t pad;
+    int32_t ncontrib;
+    int32_t nE;
+    int32_t rec_bytes; // multiple of 16
 };
+
+__host__ __device__ inline int32_t fea_pad16(int32_t b) { return (b + 15) & ~15; }
+__host__ __device__ inline int32_t fea_pad4(int32_t n) { return (n + 3) & ~3; }
+__host__ __device__ inline int32_t fea_rec_off_contrib(const FeaBlock& b) { return fea_pad16(b.nslots); }
+__host__ __device__ inline int32_t fea_rec_off_chunk(const FeaBlock& b) {
+    return fea_rec_off_contrib(b) + fea_pad16(2 * b.ncontrib);
+}
+__host__ __device__ inline int32_t fea_rec_off_dofs(const FeaBlock& b) {
+    return fea_rec_off_chunk(b) + fea_pad16(4 * ((b.nslots + 31) / 32));
+}
+__host__ __device__ inline int32_t fea_rec_bytes(const FeaBlock& b, int np) {
+    return fea_rec_off_dofs(b) + 4 * np * fea_pad4(b.nE);
+}
 
 // Coefficient k(u) (fea.h FEA_K_*).
 struct FeaCoef {
@@ -35,26 +49,48 @@ struct FeaCoef {
 // Kernel parameters (passed by value as __grid_constant__).
 struct FeaKParams {
     const FeaBlock* blocks;
+    const uint8_t* records;  // all block records
     int32_t nblocks;
-    int32_t e_max;          // V row stride in shared memory (elements per block, max)
-    const int32_t* dofT;    // [n_p][n_e] library DOF ids, library element order (SoA)
-    int64_t n_e;
-    const double2* xy;      // [n_dof] DOF coordinates (vertex DOFs used for B_e)
-    const double* u;        // [n_dof] u_full, library numbering
-    const uint8_t* counts;  // [nslots_total] contributors per slot
-    const uint16_t* contrib;// contributor stream: smem V offsets t * e_max + le
-    const int32_t* chunk_base; // per 32-slot chunk: offset of its first contributor within the block
-    const int32_t* ghosts;  // ghost element ids
-    const double* tables;   // Phi [np][nq], w [nq], Q [T][4][nq]
-    int32_t tables_doubles;
+    int32_t e_max;           // V row stride (elements per block, max)
+    int32_t rec_max;         // record buffer size in shared memory (bytes, multiple of 16)
     int32_t nq;
-    int32_t ntc;            // number of t-chunks per element (STAGED kernels)
-    int32_t same_coef;      // mass and stiffness share k -> one Lambda
-    double* out_m;          // [nslots_total] (rank-local slot index) or nullptr
+    const double2* xy;       // [n_dof] DOF coordinates (vertex DOFs used for B_e)
+    const double* u;         // [n_dof] u_full, library numbering
+    const double* tables;    // Phi [np][nq], w [nq], Q [T][nq][4]
+    int32_t tables_doubles;
+    int32_t ntc;             // number of t-chunks per element (STAGED kernels)
+    int32_t same_coef;       // mass and stiffness share k -> one Lambda
+    int32_t pad_;
+    double* out_m;           // [nslots_total] (rank-local slot index) or nullptr
     double* out_c;
     FeaCoef coef_m;
     FeaCoef coef_c;
+    int32_t lay[10];         // FeaSmemLayout of the plan (byte offsets)
 };
+
+// Shared-memory layout (bytes) of k_reassemble for a plan; identical on host and device.
+struct FeaSmemLayout {
+    int32_t tab, rec0, rec1, gu, gx, vm, vc, lam, bars, total;
+};
+
+__host__ __device__ inline int32_t fea_align(int32_t v, int32_t a) { return (v + a - 1) / a * a; }
+
+__host__ __device__ inline FeaSmemLayout fea_smem_layout(int tables_doubles, int rec_max, int e_max, int np, int nq,
+                                                         int T, int do_m, int do_c, int staged) {
+    FeaSmemLayout L;
+    int32_t o = 0;
+    L.tab = o;  o = fea_align(o + 8 * tables_doubles, 16);
+    L.rec0 = o; o = fea_align(o + rec_max, 16);
+    L.rec1 = o; o = fea_align(o + rec_max, 16);
+    L.gu = o;   o = fea_align(o + 8 * np * e_max, 16);
+    L.gx = o;   o = fea_align(o + 16 * 3 * e_max, 16);
+    L.vm = o;   o = fea_align(o + (do_m ? 8 * T * e_max : 0), 16);
+    L.vc = o;   o = fea_align(o + (do_c ? 8 * T * e_max : 0), 16);
+    L.lam = o;  o = fea_align(o + (staged ? 8 * (2 * nq + 3) * e_max : 0), 16);
+    L.bars = o; o += 16;
+    L.total = o;
+    return L;
+}
 
 // Launch the fused reassembly kernel (defined in fea_kernels.cu).  Returns a cudaError_t.
 int fea_launch_reassemble(const FeaKParams& prm, int order, int threads, int smem_bytes, int grid,
