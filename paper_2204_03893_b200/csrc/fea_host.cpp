@@ -97,7 +97,7 @@ struct fea_ctx_s {
     FeaBlock* d_blocks = nullptr;
     uint8_t* d_records = nullptr;
     int nblocks = 0, e_max = 0, rec_max = 0, smem_bytes = 0, threads = 256, ntc = 1, staged = 0, grid = 0;
-    int32_t lay[10] = {0};
+    int32_t lay[12] = {0};
     int64_t record_bytes = 0;
     int64_t stat_visits = 0, stat_owned = 0, stat_entries = 0;
     int launches_per_call = 1;
@@ -106,7 +106,7 @@ struct fea_ctx_s {
     FeaCoef coef_m{}, coef_c{};
 
     // tuning
-    int64_t tune_smem = 0, tune_threads = 256, tune_tchunks = 0;
+    int64_t tune_smem = 0, tune_threads = 256, tune_tchunks = 0, tune_prefetch = 0;
 
     // reassemble buffers
     double* d_ufull = nullptr;
@@ -492,6 +492,10 @@ fea_status fea_set_tuning(fea_ctx c, int key, int64_t value) {
             if (value < 0 || value > 64) return c->fail(FEA_E_ARG, "tchunks out of range");
             c->tune_tchunks = value;
             break;
+        case 5:  // gathers of block j+1 issued during phase B of block j (double gather buffers)
+            if (value < 0 || value > 1) return c->fail(FEA_E_ARG, "prefetch must be 0 or 1");
+            c->tune_prefetch = value;
+            break;
         case 4:  // plan matrices bitmask (FEA_MASS | FEA_STIFF)
             if (value < 1 || value > 3) return c->fail(FEA_E_ARG, "plan matrices must be a nonzero MASS|STIFF mask");
             c->plan_which = (int)value;
@@ -523,9 +527,9 @@ fea_status fea_build_pattern(fea_ctx c, int64_t* row_begin, int64_t* n_rows_loca
     c->staged = c->order >= 3 ? 1 : 0;
     c->threads = (int)c->tune_threads;
     const int64_t budget = c->tune_smem ? c->tune_smem : (c->order >= 3 ? 225 * 1024 : 110 * 1024);
-    const int64_t tab_bytes = (int64_t)((c->tables.size() * 8 + 15) & ~size_t(15));
-    const int64_t per_el_smem = 8LL * T * nmat + 8LL * np + 48 + (c->staged ? 8LL * (2 * nq + 3) : 0);
-    const double rec_el = 1.3 * (3.125 * np * np + 4.0 * np);  // record bytes per element (estimate)
+    const int64_t tab_bytes = c->staged ? (int64_t)((c->tables.size() * 8 + 15) & ~size_t(15)) : 0;
+    const int64_t per_el_smem = 8LL * T * nmat + (c->tune_prefetch ? 2 : 1) * (8LL * np + 48) + (c->staged ? 8LL * (2 * nq + 3) : 0);
+    const double rec_el = 1.3 * (3.0 * np * np + 4.0 * np) + 8;  // record bytes per element (estimate)
     int64_t e_max = (int64_t)((budget - tab_bytes - 64) / (per_el_smem + 2.0 * rec_el));
     e_max = std::min<int64_t>(e_max, 65535 / T);
     const int64_t rec_budget = ((int64_t)(rec_el * e_max) + 15) & ~int64_t(15);
@@ -551,7 +555,7 @@ fea_status fea_build_pattern(fea_ctx c, int64_t* row_begin, int64_t* n_rows_loca
     for (int64_t r = 0; r < nr; ++r) max_inc = std::max(max_inc, iptr[r + 1] - iptr[r]);
     if (max_inc > 255) return c->fail(FEA_E_UNSUPPORTED, "a DOF belongs to %lld elements (> 255)", (long long)max_inc);
     // one row must fit a block: its elements and its record upper bound
-    const int64_t row_ub_max = max_inc * np * 7 + 4 * np * max_inc + 64;
+    const int64_t row_ub_max = max_inc * np * 4 + 4 * np * (max_inc + 3) + 12 * FEA_MAX_CLASSES + 64;
     if (e_max < std::max<int64_t>(max_inc, 1) || rec_budget < row_ub_max)
         return c->fail(FEA_E_UNSUPPORTED, "shared-memory budget too small: %lld elements per block", (long long)e_max);
 
@@ -566,7 +570,7 @@ fea_status fea_build_pattern(fea_ctx c, int64_t* row_begin, int64_t* n_rows_loca
             int64_t add = 0;
             for (int64_t k = iptr[r]; k < iptr[r + 1]; ++k) add += mark[inc[k]] != cur;
             const int64_t rent = (iptr[r + 1] - iptr[r]) * np;
-            const int64_t ub = 3 * (ent + rent) + (ent + rent) / 8 + 4 * np * (nE + add + 3) + 64;
+            const int64_t ub = 4 * (ent + rent) + 4 * np * (nE + add + 3) + 12 * FEA_MAX_CLASSES + 64;
             if (cur < 0 || nE + add > e_max || ub > rec_budget) {
                 ++cur;
                 brow.push_back(r);
@@ -615,37 +619,60 @@ fea_status fea_build_pattern(fea_ctx c, int64_t* row_begin, int64_t* n_rows_loca
         std::stable_sort(recs.begin(), recs.end(), [](const Rec& x, const Rec& y) {
             return x.row != y.row ? x.row < y.row : x.col < y.col;
         });
-        std::vector<uint8_t> counts;
-        std::vector<uint16_t> contrib;
-        std::vector<int32_t> chunk;
+        // slots (row, col) in CSR order, each with its contributors in ascending le
+        std::vector<int32_t> sstart, scount;  // per slot: first record, count
         o.rownnz.assign(rb - ra, 0);
-        contrib.reserve(recs.size());
         size_t k = 0;
-        int64_t nslot = 0;
         while (k < recs.size()) {
             size_t k2 = k;
             while (k2 < recs.size() && recs[k2].row == recs[k].row && recs[k2].col == recs[k].col) ++k2;
-            if (nslot % 32 == 0) chunk.push_back((int32_t)contrib.size());
+            sstart.push_back((int32_t)k);
+            scount.push_back((int32_t)(k2 - k));
             o.cols.push_back(recs[k].col);
             o.rownnz[recs[k].row - ga]++;
-            counts.push_back((uint8_t)(k2 - k));
-            for (size_t m = k; m < k2; ++m) contrib.push_back((uint16_t)(recs[m].t * EM + recs[m].le));
-            ++nslot;
             k = k2;
         }
+        const int32_t nslot = (int32_t)sstart.size();
+        // items: slots sorted by (count, slot); classes of equal count
+        std::vector<int32_t> order(nslot);
+        std::iota(order.begin(), order.end(), 0);
+        std::stable_sort(order.begin(), order.end(), [&](int32_t x, int32_t y) { return scount[x] < scount[y]; });
+        std::vector<int32_t> cls;
+        std::vector<uint16_t> items(nslot), contrib;
+        contrib.reserve(recs.size());
+        for (int32_t it = 0; it < nslot; ++it) {
+            const int32_t sl = order[it];
+            if (it == 0 || scount[sl] != scount[order[it - 1]]) {
+                cls.push_back(scount[sl]);
+                cls.push_back(it);
+                cls.push_back((int32_t)contrib.size());
+            }
+            if (sl > 65535) {
+                o.err = "more than 65536 slots in one block";
+                return;
+            }
+            items[it] = (uint16_t)sl;
+            for (int32_t m = sstart[sl]; m < sstart[sl] + scount[sl]; ++m)
+                contrib.push_back((uint16_t)(recs[m].t * EM + recs[m].le));
+        }
         FeaBlock& F = o.fb;
-        F.nslots = (int32_t)nslot;
+        F.nslots = nslot;
         F.ncontrib = (int32_t)contrib.size();
         F.nE = (int32_t)E.size();
+        F.ncls = (int32_t)(cls.size() / 3);
+        if (F.ncls > FEA_MAX_CLASSES) {
+            o.err = "too many contributor-count classes";
+            return;
+        }
         F.rec_bytes = fea_rec_bytes(F, np);
         if (F.rec_bytes > rec_budget) {
             o.err = "record exceeds the shared-memory budget";
             return;
         }
         o.rec.assign(F.rec_bytes, 0);
-        std::memcpy(o.rec.data(), counts.data(), counts.size());
+        std::memcpy(o.rec.data(), cls.data(), 4 * cls.size());
+        std::memcpy(o.rec.data() + fea_rec_off_items(F), items.data(), 2 * items.size());
         std::memcpy(o.rec.data() + fea_rec_off_contrib(F), contrib.data(), 2 * contrib.size());
-        std::memcpy(o.rec.data() + fea_rec_off_chunk(F), chunk.data(), 4 * chunk.size());
         int32_t* dofs = reinterpret_cast<int32_t*>(o.rec.data() + fea_rec_off_dofs(F));
         const int32_t nEp = fea_pad4(F.nE);
         for (int64_t le = 0; le < (int64_t)E.size(); ++le)
@@ -685,7 +712,8 @@ fea_status fea_build_pattern(fea_ctx c, int64_t* row_begin, int64_t* n_rows_loca
     for (int64_t r = 0; r < nr; ++r) c->row_ptr[r + 1] += c->row_ptr[r];
     bo.clear();
 
-    FeaSmemLayout L = fea_smem_layout((int)c->tables.size(), (int)rec_max, (int)e_max, np, nq, T, dm, dcm, c->staged);
+    FeaSmemLayout L = fea_smem_layout(c->staged ? (int)c->tables.size() : 0, (int)rec_max, (int)e_max, np, nq, T, dm, dcm,
+                                      c->staged, (int)c->tune_prefetch);
     c->nblocks = (int)nb;
     c->e_max = (int)e_max;
     c->rec_max = (int)rec_max;
@@ -787,6 +815,11 @@ static fea_status launch(fea_ctx c, const double* u, double* vm, double* vc) {
     prm.u = u;
     prm.tables = c->d_tables;
     prm.tables_doubles = (int32_t)c->tables.size();
+    prm.prefetch = (int32_t)c->tune_prefetch;
+    if (!c->staged) {
+        if (c->tables.size() > FEA_CTAB_MAX) return c->fail(FEA_E_UNSUPPORTED, "tables exceed the parameter bank");
+        std::memcpy(prm.ctab, c->tables.data(), c->tables.size() * sizeof(double));
+    }
     prm.ntc = c->ntc;
     prm.same_coef = same_coef(c->coef_m, c->coef_c) ? 1 : 0;
     prm.coef_m = c->coef_m;

@@ -7,14 +7,22 @@
 #define FEA_MAX_NP 15
 #define FEA_MAX_NQ 16
 #define FEA_MAX_PAR 16
+// Reference tables small enough to travel in the kernel parameters (constant bank): p <= 2
+// (P2 with 16 points: Phi 6x16 + w 16 + Q 21x16x4 = 1456 doubles).  Larger orders stage them
+// in shared memory.
+#define FEA_CTAB_MAX 1464
 
 // One unit of CTA work: a contiguous block of library rows whose CSR slots
 // [slot0, slot0 + nslots) are produced by exactly one CTA.  Everything the block streams
 // from HBM sits in ONE contiguous, 16-byte aligned record at rec_off (one TMA bulk copy):
-//   counts   uint8  [nslots]                contributors per slot          (pad16)
-//   contrib  uint16 [ncontrib]              V offsets t * e_max + le       (pad16)
-//   chunk    int32  [ceil(nslots / 32)]     first contributor of each 32-slot chunk (pad16)
-//   dofs     int32  [n_p][pad4(nE)]         library DOFs of the block's elements (SoA)
+//   classes  int32  [ncls][3]   (count c, first item, first contributor); slots with the
+//                               same contributor count form a class, so a warp's lanes all
+//                               run the same trip count                                (pad16)
+//   items    uint16 [nslots]    block-local slot of each item, sorted by (count, slot)   (pad16)
+//   contrib  uint16 [ncontrib]  V offsets t * e_max + le, item by item; within an item in
+//                               ascending library element order (the fixed summation order)
+//                                                                                        (pad16)
+//   dofs     int32  [n_p][pad4(nE)]  library DOFs of the block's elements (SoA)
 // The block's elements (le = 0 .. nE-1) are in ascending library element order: ghost
 // elements (owned by earlier blocks) first, then the block's own elements.
 struct FeaBlock {
@@ -24,16 +32,20 @@ struct FeaBlock {
     int32_t ncontrib;
     int32_t nE;
     int32_t rec_bytes; // multiple of 16
+    int32_t ncls;
+    int32_t pad_;
 };
+
+#define FEA_MAX_CLASSES 64
 
 __host__ __device__ inline int32_t fea_pad16(int32_t b) { return (b + 15) & ~15; }
 __host__ __device__ inline int32_t fea_pad4(int32_t n) { return (n + 3) & ~3; }
-__host__ __device__ inline int32_t fea_rec_off_contrib(const FeaBlock& b) { return fea_pad16(b.nslots); }
-__host__ __device__ inline int32_t fea_rec_off_chunk(const FeaBlock& b) {
-    return fea_rec_off_contrib(b) + fea_pad16(2 * b.ncontrib);
+__host__ __device__ inline int32_t fea_rec_off_items(const FeaBlock& b) { return fea_pad16(12 * b.ncls); }
+__host__ __device__ inline int32_t fea_rec_off_contrib(const FeaBlock& b) {
+    return fea_rec_off_items(b) + fea_pad16(2 * b.nslots);
 }
 __host__ __device__ inline int32_t fea_rec_off_dofs(const FeaBlock& b) {
-    return fea_rec_off_chunk(b) + fea_pad16(4 * ((b.nslots + 31) / 32));
+    return fea_rec_off_contrib(b) + fea_pad16(2 * b.ncontrib);
 }
 __host__ __device__ inline int32_t fea_rec_bytes(const FeaBlock& b, int np) {
     return fea_rec_off_dofs(b) + 4 * np * fea_pad4(b.nE);
@@ -65,18 +77,21 @@ struct FeaKParams {
     double* out_c;
     FeaCoef coef_m;
     FeaCoef coef_c;
-    int32_t lay[10];         // FeaSmemLayout of the plan (byte offsets)
+    int32_t lay[12];         // FeaSmemLayout of the plan (byte offsets)
+    int32_t prefetch;        // gathers of block j+1 issued before phase B of block j
+    int32_t pad2_;
+    double ctab[FEA_CTAB_MAX];  // tables for p <= 2 (same layout as `tables`)
 };
 
 // Shared-memory layout (bytes) of k_reassemble for a plan; identical on host and device.
 struct FeaSmemLayout {
-    int32_t tab, rec0, rec1, gu, gx, vm, vc, lam, bars, total;
+    int32_t tab, rec0, rec1, gu, gx, vm, vc, lam, bars, total, gu1, gx1;
 };
 
 __host__ __device__ inline int32_t fea_align(int32_t v, int32_t a) { return (v + a - 1) / a * a; }
 
 __host__ __device__ inline FeaSmemLayout fea_smem_layout(int tables_doubles, int rec_max, int e_max, int np, int nq,
-                                                         int T, int do_m, int do_c, int staged) {
+                                                         int T, int do_m, int do_c, int staged, int prefetch) {
     FeaSmemLayout L;
     int32_t o = 0;
     L.tab = o;  o = fea_align(o + 8 * tables_doubles, 16);
@@ -84,6 +99,8 @@ __host__ __device__ inline FeaSmemLayout fea_smem_layout(int tables_doubles, int
     L.rec1 = o; o = fea_align(o + rec_max, 16);
     L.gu = o;   o = fea_align(o + 8 * np * e_max, 16);
     L.gx = o;   o = fea_align(o + 16 * 3 * e_max, 16);
+    L.gu1 = o;  o = fea_align(o + (prefetch ? 8 * np * e_max : 0), 16);
+    L.gx1 = o;  o = fea_align(o + (prefetch ? 16 * 3 * e_max : 0), 16);
     L.vm = o;   o = fea_align(o + (do_m ? 8 * T * e_max : 0), 16);
     L.vc = o;   o = fea_align(o + (do_c ? 8 * T * e_max : 0), 16);
     L.lam = o;  o = fea_align(o + (staged ? 8 * (2 * nq + 3) * e_max : 0), 16);

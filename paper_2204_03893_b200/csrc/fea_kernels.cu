@@ -163,6 +163,118 @@ __device__ __forceinline__ void contract2(const double* __restrict__ sQ, int nq,
     }
 }
 
+// p <= 2 with the native rule: one element, tables read straight from the kernel parameters
+// (constant bank operands of DFMA, fully unrolled over t and q; no shared-memory loads).
+template <int NP, int NQ, bool DO_M, bool DO_C>
+__device__ __forceinline__ void element_const(const FeaKParams& prm, const double* __restrict__ gU,
+                                              const double2* __restrict__ gX, int e_max, int le, bool two_lam,
+                                              double* __restrict__ sVm, double* __restrict__ sVc) {
+    constexpr int T = NP * (NP + 1) / 2;
+    constexpr int oW = (NP * NQ + 1) & ~1;
+    constexpr int oQ = oW + ((NQ + 1) & ~1);
+    double absdet, A00, A11, A01;
+    geometry(gX, e_max, le, absdet, A00, A11, A01);
+    double ue[NP];
+#pragma unroll
+    for (int i = 0; i < NP; ++i) ue[i] = gU[i * e_max + le];
+    double lm[NQ], lc[NQ];
+#pragma unroll
+    for (int q = 0; q < NQ; ++q) {
+        double uq = 0.0;
+#pragma unroll
+        for (int i = 0; i < NP; ++i) uq = fma(prm.ctab[i * NQ + q], ue[i], uq);
+        const double wb = prm.ctab[oW + q] * absdet;
+        lm[q] = wb * keval(DO_M ? prm.coef_m : prm.coef_c, uq);
+        lc[q] = two_lam ? wb * keval(prm.coef_c, uq) : lm[q];
+    }
+#pragma unroll
+    for (int t = 0; t < T; ++t) {
+        double vm = 0.0, a = 0.0, b = 0.0, c = 0.0;
+#pragma unroll
+        for (int q = 0; q < NQ; ++q) {
+            const double* Qq = prm.ctab + oQ + (t * NQ + q) * 4;
+            if (DO_M) vm = fma(Qq[0], lm[q], vm);
+            if (DO_C) {
+                a = fma(Qq[1], lc[q], a);
+                b = fma(Qq[2], lc[q], b);
+                c = fma(Qq[3], lc[q], c);
+            }
+        }
+        if (DO_M) sVm[t * e_max + le] = vm;
+        if (DO_C) sVc[t * e_max + le] = fma(A00, a, fma(A11, b, A01 * c));
+    }
+}
+
+// Sum of the C contributors of one slot in the fixed (stored) order, all loads issued first.
+template <int C, bool DO_M, bool DO_C>
+__device__ __forceinline__ void slot_sum(const uint16_t* __restrict__ cp, const double* __restrict__ sVm,
+                                         const double* __restrict__ sVc, double& am, double& ac) {
+    int off[C];
+#pragma unroll
+    for (int q = 0; q < C; ++q) off[q] = cp[q];
+    double vm[C], vc[C];
+#pragma unroll
+    for (int q = 0; q < C; ++q) {
+        if (DO_M) vm[q] = sVm[off[q]];
+        if (DO_C) vc[q] = sVc[off[q]];
+    }
+    am = 0.0;
+    ac = 0.0;
+#pragma unroll
+    for (int q = 0; q < C; ++q) {
+        if (DO_M) am += vm[q];
+        if (DO_C) ac += vc[q];
+    }
+}
+
+template <int C, bool DO_M, bool DO_C>
+__device__ __forceinline__ void class_items(int i0, int i1, int cb, const uint16_t* __restrict__ items,
+                                            const uint16_t* __restrict__ con, const double* __restrict__ sVm,
+                                            const double* __restrict__ sVc, double* om, double* oc, int tid,
+                                            int nthr) {
+    int it = i0 + tid;
+    for (; it + nthr < i1; it += 2 * nthr) {  // two items per thread in flight
+        const int s0 = items[it], s1 = items[it + nthr];
+        double am0, ac0, am1, ac1;
+        slot_sum<C, DO_M, DO_C>(con + cb + (it - i0) * C, sVm, sVc, am0, ac0);
+        slot_sum<C, DO_M, DO_C>(con + cb + (it + nthr - i0) * C, sVm, sVc, am1, ac1);
+        if (DO_M) {
+            om[s0] = am0;
+            om[s1] = am1;
+        }
+        if (DO_C) {
+            oc[s0] = ac0;
+            oc[s1] = ac1;
+        }
+    }
+    if (it < i1) {
+        const int s0 = items[it];
+        double am0, ac0;
+        slot_sum<C, DO_M, DO_C>(con + cb + (it - i0) * C, sVm, sVc, am0, ac0);
+        if (DO_M) om[s0] = am0;
+        if (DO_C) oc[s0] = ac0;
+    }
+}
+
+template <bool DO_M, bool DO_C>
+__device__ __forceinline__ void class_items_generic(int c, int i0, int i1, int cb, const uint16_t* __restrict__ items,
+                                                    const uint16_t* __restrict__ con, const double* __restrict__ sVm,
+                                                    const double* __restrict__ sVc, double* om, double* oc, int tid,
+                                                    int nthr) {
+    for (int it = i0 + tid; it < i1; it += nthr) {
+        const uint16_t* cp = con + cb + (it - i0) * c;
+        double am = 0.0, ac = 0.0;
+        for (int q = 0; q < c; ++q) {
+            const int off = cp[q];
+            if (DO_M) am += sVm[off];
+            if (DO_C) ac += sVc[off];
+        }
+        const int s = items[it];
+        if (DO_M) om[s] = am;
+        if (DO_C) oc[s] = ac;
+    }
+}
+
 template <int P, int NQ_T, bool DO_M, bool DO_C, bool STAGED>
 __global__ void __launch_bounds__(256, STAGED ? 1 : 2) k_reassemble(const __grid_constant__ FeaKParams prm) {
     constexpr int NP = (P + 1) * (P + 2) / 2;
@@ -171,17 +283,19 @@ __global__ void __launch_bounds__(256, STAGED ? 1 : 2) k_reassemble(const __grid
     const int nq = NQ_T > 0 ? NQ_T : prm.nq;
     const int e_max = prm.e_max;
     const int tid = threadIdx.x, nthr = blockDim.x;
-    const int lane = tid & 31, warp = tid >> 5, nwarp = nthr >> 5;
 
     extern __shared__ __align__(128) uint8_t smem[];
+    // p >= 3: tables in shared memory; p <= 2: tables in the kernel parameters (prm.ctab)
     double* sTab = reinterpret_cast<double*>(smem + prm.lay[0]);
-    const double* sPhi = sTab;
-    const double* sW = sTab + ((NP * nq + 1) & ~1);
+    const double* tab = STAGED ? static_cast<const double*>(sTab) : prm.ctab;
+    const double* sPhi = tab;
+    const double* sW = tab + ((NP * nq + 1) & ~1);
     const double* sQ = sW + ((nq + 1) & ~1);
     uint8_t* sRec0 = smem + prm.lay[1];
     uint8_t* sRec1 = smem + prm.lay[2];
-    double* gU = reinterpret_cast<double*>(smem + prm.lay[3]);
-    double2* gX = reinterpret_cast<double2*>(smem + prm.lay[4]);
+    const bool pf = prm.prefetch != 0;
+    double* gUb[2] = {reinterpret_cast<double*>(smem + prm.lay[3]), reinterpret_cast<double*>(smem + prm.lay[pf ? 10 : 3])};
+    double2* gXb[2] = {reinterpret_cast<double2*>(smem + prm.lay[4]), reinterpret_cast<double2*>(smem + prm.lay[pf ? 11 : 4])};
     double* sVm = reinterpret_cast<double*>(smem + prm.lay[5]);
     double* sVc = reinterpret_cast<double*>(smem + prm.lay[6]);
     double* sLam = reinterpret_cast<double*>(smem + prm.lay[7]);
@@ -193,7 +307,8 @@ __global__ void __launch_bounds__(256, STAGED ? 1 : 2) k_reassemble(const __grid
         mbar_init(&bars[1], 1);
         fence_mbar_init();
     }
-    for (int i = tid; i < prm.tables_doubles; i += nthr) sTab[i] = __ldg(prm.tables + i);
+    if constexpr (STAGED)
+        for (int i = tid; i < prm.tables_doubles; i += nthr) sTab[i] = __ldg(prm.tables + i);
     __syncthreads();
 
     auto issue = [&](int b, int buf) {
@@ -203,30 +318,49 @@ __global__ void __launch_bounds__(256, STAGED ? 1 : 2) k_reassemble(const __grid
         mbar_expect_tx(&bars[buf], (uint32_t)nb.rec_bytes);
         tma_load_1d(dst, prm.records + nb.rec_off, (uint32_t)nb.rec_bytes, &bars[buf]);
     };
+    // gathers of u(N_e) and the vertex coordinates of a block into gather buffer g (async)
+    auto gather = [&](const FeaBlock& gb, const uint8_t* grec, int g) {
+        const int nEp_ = fea_pad4(gb.nE);
+        const int32_t* gd = reinterpret_cast<const int32_t*>(grec + fea_rec_off_dofs(gb));
+        double* gu = gUb[g];
+        double2* gx = gXb[g];
+        for (int le = tid; le < gb.nE; le += nthr) {
+#pragma unroll
+            for (int i = 0; i < NP; ++i) cp_async8(gu + i * e_max + le, prm.u + gd[i * nEp_ + le]);
+#pragma unroll
+            for (int v = 0; v < 3; ++v) cp_async16(gx + v * e_max + le, prm.xy + gd[v * nEp_ + le]);
+        }
+        asm volatile("cp.async.commit_group;" ::: "memory");
+    };
+    // prologue: records of the first two blocks in flight
     if (tid == 0 && (int)blockIdx.x < prm.nblocks) issue(blockIdx.x, 0);
+    if (tid == 0 && (int)(blockIdx.x + gridDim.x) < prm.nblocks) issue(blockIdx.x + gridDim.x, 1);
+    if (pf && (int)blockIdx.x < prm.nblocks) {
+        mbar_wait(&bars[0], 0);
+        gather(prm.blocks[blockIdx.x], sRec0, 0);
+    }
 
     int j = 0;
     for (int bi = blockIdx.x; bi < prm.nblocks; bi += gridDim.x, ++j) {
         const int buf = j & 1;
         const FeaBlock blk = prm.blocks[bi];
-        if (tid == 0 && bi + (int)gridDim.x < prm.nblocks) issue(bi + gridDim.x, buf ^ 1);
-        mbar_wait(&bars[buf], (uint32_t)((j >> 1) & 1));
         const uint8_t* rec = buf ? sRec1 : sRec0;
-        const int nE = blk.nE, nEp = fea_pad4(nE);
-        const int32_t* dofs = reinterpret_cast<const int32_t*>(rec + fea_rec_off_dofs(blk));
-
-        // ---------------- gathers: u(N_e) and the vertex coordinates, all in flight at once
-        for (int le = tid; le < nE; le += nthr) {
-#pragma unroll
-            for (int i = 0; i < NP; ++i) cp_async8(gU + i * e_max + le, prm.u + dofs[i * nEp + le]);
-#pragma unroll
-            for (int v = 0; v < 3; ++v) cp_async16(gX + v * e_max + le, prm.xy + dofs[v * nEp + le]);
+        const int nE = blk.nE;
+        const int g = pf ? buf : 0;
+        if (!pf) {
+            mbar_wait(&bars[buf], (uint32_t)((j >> 1) & 1));
+            gather(blk, rec, 0);
         }
-        cp_async_wait_all();
+        const double* gU = gUb[g];
+        const double2* gX = gXb[g];
+        asm volatile("cp.async.wait_group 0;" ::: "memory");  // this block's gathers landed
         __syncthreads();
 
         // ---------------- Phase A: element values V[t][le] in shared memory
-        if constexpr (!STAGED) {
+        if constexpr (!STAGED && NQ_T > 0) {
+            for (int le = tid; le < nE; le += nthr)
+                element_const<NP, NQ_T, DO_M, DO_C>(prm, gU, gX, e_max, le, two_lam, sVm, sVc);
+        } else if constexpr (!STAGED) {
             for (int le0 = tid; le0 < nE; le0 += 2 * nthr) {
                 const int le1 = le0 + nthr;
                 const bool has1 = le1 < nE;
@@ -298,36 +432,37 @@ __global__ void __launch_bounds__(256, STAGED ? 1 : 2) k_reassemble(const __grid
                 contract2<NQM, DO_M, DO_C>(sQ, nq, t0, t1, lm0, lc0, lm1, lc1, W0, W1, sVm, sVc, e_max, le0, le1, has1);
             }
         }
+        // with prefetch, the next block's gathers fly during phase B
+        const int bn = bi + gridDim.x;
+        if (pf && bn < prm.nblocks) {
+            mbar_wait(&bars[buf ^ 1], (uint32_t)(((j + 1) >> 1) & 1));
+            gather(prm.blocks[bn], buf ? sRec0 : sRec1, buf ^ 1);
+        }
         __syncthreads();
 
-        // ---------------- Phase B: fixed-order segmented reduction into the CSR slots
-        const uint8_t* cnt = rec;
+        // ---------------- Phase B: fixed-order segmented reduction into the CSR slots.
+        // Items (slots) come grouped by contributor count c, so every lane of a warp runs the
+        // same trip count and the contributor base is arithmetic (no scan).
+        const int32_t* cls = reinterpret_cast<const int32_t*>(rec);
+        const uint16_t* items = reinterpret_cast<const uint16_t*>(rec + fea_rec_off_items(blk));
         const uint16_t* con = reinterpret_cast<const uint16_t*>(rec + fea_rec_off_contrib(blk));
-        const int32_t* chk = reinterpret_cast<const int32_t*>(rec + fea_rec_off_chunk(blk));
-        const int nchunks = (blk.nslots + 31) >> 5;
-        for (int ch = warp; ch < nchunks; ch += nwarp) {
-            const int s = ch * 32 + lane;
-            const bool valid = s < blk.nslots;
-            const int c = valid ? (int)cnt[s] : 0;
-            int incl = c;
-#pragma unroll
-            for (int d = 1; d < 32; d <<= 1) {
-                const int v = __shfl_up_sync(0xffffffffu, incl, d);
-                if (lane >= d) incl += v;
-            }
-            const int base = chk[ch] + incl - c;
-            double am = 0.0, ac = 0.0;
-            for (int k = 0; k < c; ++k) {
-                const int off = con[base + k];
-                if (DO_M) am += sVm[off];
-                if (DO_C) ac += sVc[off];
-            }
-            if (valid) {
-                if (DO_M) prm.out_m[blk.slot0 + s] = am;
-                if (DO_C) prm.out_c[blk.slot0 + s] = ac;
+        double* om = DO_M ? prm.out_m + blk.slot0 : nullptr;
+        double* oc = DO_C ? prm.out_c + blk.slot0 : nullptr;
+        for (int k = 0; k < blk.ncls; ++k) {
+            const int c = cls[3 * k], i0 = cls[3 * k + 1], cb = cls[3 * k + 2];
+            const int i1 = k + 1 < blk.ncls ? cls[3 * k + 4] : blk.nslots;
+            switch (c) {
+                case 1: class_items<1, DO_M, DO_C>(i0, i1, cb, items, con, sVm, sVc, om, oc, tid, nthr); break;
+                case 2: class_items<2, DO_M, DO_C>(i0, i1, cb, items, con, sVm, sVc, om, oc, tid, nthr); break;
+                case 3: class_items<3, DO_M, DO_C>(i0, i1, cb, items, con, sVm, sVc, om, oc, tid, nthr); break;
+                case 4: class_items<4, DO_M, DO_C>(i0, i1, cb, items, con, sVm, sVc, om, oc, tid, nthr); break;
+                case 6: class_items<6, DO_M, DO_C>(i0, i1, cb, items, con, sVm, sVc, om, oc, tid, nthr); break;
+                default: class_items_generic<DO_M, DO_C>(c, i0, i1, cb, items, con, sVm, sVc, om, oc, tid, nthr);
             }
         }
         __syncthreads();
+        // this block's record buffer is free: request the record two blocks ahead
+        if (tid == 0 && bi + 2 * (int)gridDim.x < prm.nblocks) issue(bi + 2 * gridDim.x, buf);
     }
 }
 
