@@ -212,8 +212,10 @@ def run_ours(args):
     wl = make_workload(cfg)
     m = wl.mesh
     coef = (cfg.k_kind, tuple(cfg.k_par))
+    tuning = {int(kv.split("=")[0]): int(kv.split("=")[1]) for kv in args.tune}
     asm = Assembler(cfg.p, wl.q_xy, wl.q_w, m.vert_xy, m.elem_vert, m.n_dof, m.elem_dof, device=local,
-                    reorder=cfg.reorder, which=cfg.which, coef_m=coef, coef_c=coef, rank=rank, world=world)
+                    reorder=cfg.reorder, which=cfg.which, coef_m=coef, coef_c=coef, rank=rank, world=world,
+                    tuning=tuning)
     t_setup = time.perf_counter() - t_setup
     nmat = cfg.n_matrices
     # distinct u per step (library numbering, owned rows), resident in HBM
@@ -301,7 +303,12 @@ def run_ours(args):
         desc.update({"l2": "flushed (256 MiB write) before every timed step", "parallelism": f"rows{world}",
                      "nnz": int(nnz_local) if world == 1 else None, "setup_s": round(t_setup, 3),
                      "blocks": asm.ctx.stat(1), "elem_visits_over_owned": round(asm.ctx.stat(2) / max(1, asm.ctx.stat(3)), 4),
-                     "smem_per_cta": asm.ctx.stat(6), "grid": asm.ctx.stat(8)})
+                     "smem_per_cta": asm.ctx.stat(6), "grid": asm.ctx.stat(8), "tuning": tuning})
+        if os.environ.get("FEA_DEBUG_TIMING"):
+            ph = [asm.ctx.stat(20 + i) for i in range(6)]
+            tot = sum(ph) or 1
+            desc["phase_cycles_pct"] = dict(zip(["rec_wait", "gather", "phaseA", "phaseB", "issue", "barriers"],
+                                                [round(100.0 * x / tot, 1) for x in ph]))
         line = {
             "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
             "warmup": args.warmup, "ms_per_step": ms_per_step, "higher_is_better": True,
@@ -332,6 +339,7 @@ def main():
     ap.add_argument("--config", default=os.environ.get("FEA_BENCH_CONFIG", DEFAULT_CONFIG), choices=sorted(CONFIGS))
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--tune", action="append", default=[], help="libfea tuning key=value (fea.h FEA_TUNE_*)")
     args = ap.parse_args()
     if args.warmup < 3:
         args.warmup = 3  # timing rule: at least 3 warm-up steps

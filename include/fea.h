@@ -62,9 +62,12 @@ enum { FEA_K_POLY = 0, FEA_K_EXP = 1, FEA_K_PWL = 2 };
 
 /* Tuning keys for fea_set_tuning (before fea_build_pattern). */
 enum {
-    FEA_TUNE_SMEM_BUDGET = 1,   /* bytes of shared memory per CTA for element values (default 96 KiB) */
-    FEA_TUNE_THREADS = 2,       /* threads per CTA (default 256)                                     */
-    FEA_TUNE_TCHUNKS = 3        /* split of the symmetric rows per element across threads (0 = auto) */
+    FEA_TUNE_SMEM_BUDGET = 1,   /* bytes of shared memory per CTA (0 = default: 113 KiB for p <= 2,
+                                   two CTAs per SM; 226 KiB for p >= 3).  Smaller budgets give
+                                   smaller row blocks (more, finer CTA tiles)                        */
+    FEA_TUNE_PLAN_WHICH = 4     /* FEA_MASS | FEA_STIFF: matrices the plan's shared memory is sized
+                                   for (default both); assembling more than planned runs one pass
+                                   per matrix                                                        */
 };
 
 /* Create a context on CUDA device `cuda_device`.  `stream` is a cudaStream_t (NULL = the

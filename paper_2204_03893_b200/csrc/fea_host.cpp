@@ -14,6 +14,7 @@
 #include <cmath>
 #include <cstdarg>
 #include <cstdio>
+#include <cstdlib>
 #include <cstring>
 #include <numeric>
 #include <string>
@@ -76,7 +77,7 @@ struct fea_ctx_s {
 
     // reference element
     int order = 0, np = 0, nq = 0, T = 0;
-    std::vector<double> qxy, qw, tables;
+    std::vector<double> qxy, qw, tables, qfrag;  // tables = Phi, w (kernel parameters)
 
     // mesh, library numbering
     bool have_mesh = false;
@@ -96,8 +97,8 @@ struct fea_ctx_s {
     std::vector<int32_t> col_idx;
     FeaBlock* d_blocks = nullptr;
     uint8_t* d_records = nullptr;
-    int nblocks = 0, e_max = 0, rec_max = 0, smem_bytes = 0, threads = 256, ntc = 1, staged = 0, grid = 0;
-    int32_t lay[12] = {0};
+    int nblocks = 0, e_max = 0, rec_max = 0, smem_bytes = 0, threads = 0, grid = 0;
+    int32_t lay[FEA_L_N] = {0};
     int64_t record_bytes = 0;
     int64_t stat_visits = 0, stat_owned = 0, stat_entries = 0;
     int launches_per_call = 1;
@@ -106,7 +107,7 @@ struct fea_ctx_s {
     FeaCoef coef_m{}, coef_c{};
 
     // tuning
-    int64_t tune_smem = 0, tune_threads = 256, tune_tchunks = 0, tune_prefetch = 0;
+    int64_t tune_smem = 0;
 
     // reassemble buffers
     double* d_ufull = nullptr;
@@ -114,6 +115,7 @@ struct fea_ctx_s {
     double* d_vm = nullptr;
     double* d_vc = nullptr;
     void* comm = nullptr;
+    unsigned long long* d_dbg = nullptr;  // FEA_DEBUG_TIMING phase counters
 
     fea_status fail(fea_status s, const char* fmt, ...) {
         char buf[512];
@@ -200,13 +202,9 @@ bool invert(std::vector<long double>& A, int n) {
 }
 
 // Tables (Algorithm 2 lines 1-3), symmetric rows only:
-//   Phi[i][q]             = phi_i(x_q)
-//   w[q]
-//   Q[t][q][0] = Phi_i Phi_j                      (rows of Q_m = Phi (.) Phi)
-//   Q[t][q][1] = J_i0 J_j0, Q[t][q][2] = J_i1 J_j1, Q[t][q][3] = J_i0 J_j1 + J_i1 J_j0
-//                                                 (rows of Q_c = [J_q (x) J_q], columns of vec A
-//                                                  merged by the symmetry A01 = A10)
-bool build_tables(int p, int nq, const double* qxy, const double* qw, std::vector<double>& tab) {
+//   Phi[i][q] = phi_i(x_q), w[q], and the rows t = (i <= j) of Q_m and Q_c (below).
+bool build_tables(int p, int nq, const double* qxy, const double* qw, std::vector<double>& ctab,
+                  std::vector<double>& qfrag) {
     int kk[FEA_MAX_NP][3];
     const int np = lib_nodes(p, kk);
     std::vector<std::pair<int, int>> mono;
@@ -236,24 +234,45 @@ bool build_tables(int p, int nq, const double* qxy, const double* qw, std::vecto
         }
     }
     const int T = np * (np + 1) / 2;
-    // layout (kernel view): Phi at 0, w at pad2(np nq), Q[T][nq][4] at pad2(np nq) + pad2(nq)
-    const size_t oW = ((size_t)np * nq + 1) & ~size_t(1), oQ = oW + (((size_t)nq + 1) & ~size_t(1));
-    tab.assign(oQ + (size_t)T * nq * 4, 0.0);
-    for (int i = 0; i < np * nq; ++i) tab[i] = (double)phi[i];
-    for (int q = 0; q < nq; ++q) tab[oW + q] = qw[q];
-    double* Q = tab.data() + oQ;
+    // (1) ctab: Phi [np][nq] at 0, w [nq] at pad2(np nq)   (kernel parameters)
+    const size_t oW = ((size_t)np * nq + 1) & ~size_t(1);
+    ctab.assign(oW + nq, 0.0);
+    for (int i = 0; i < np * nq; ++i) ctab[i] = (double)phi[i];
+    for (int q = 0; q < nq; ++q) ctab[oW + q] = qw[q];
+    // (2) qfrag: Q_f as DMMA A-fragments [4][NTT][NK][32]: lane (g, c) holds Q_f[t = 8 tt + g][q = 4 kk + c]
+    //     f = 0: Phi_i Phi_j (rows of Q_m = Phi (.) Phi); f = 1, 2, 3: J_i0 J_j0, J_i1 J_j1,
+    //     J_i0 J_j1 + J_i1 J_j0 (rows of Q_c = [J_q (x) J_q], columns of vec A merged by A01 = A10)
+    const int NTT = (T + 7) / 8, NK = fea_nk_kernel(p, nq);
+    qfrag.assign((size_t)4 * NTT * NK * 32, 0.0);
+    std::vector<int> ti(T), tj(T);
     for (int i = 0; i < np; ++i)
         for (int j = i; j < np; ++j) {
-            const int t = tri_index(np, i, j);
-            for (int q = 0; q < nq; ++q) {
-                const int a = i * nq + q, b = j * nq + q;
-                double* o = Q + ((size_t)t * nq + q) * 4;
-                o[0] = (double)(phi[a] * phi[b]);
-                o[1] = (double)(gx[a] * gx[b]);
-                o[2] = (double)(gy[a] * gy[b]);
-                o[3] = (double)(gx[a] * gy[b] + gy[a] * gx[b]);
-            }
+            ti[tri_index(np, i, j)] = i;
+            tj[tri_index(np, i, j)] = j;
         }
+    for (int f = 0; f < 4; ++f)
+        for (int tt = 0; tt < NTT; ++tt)
+            for (int kk = 0; kk < NK; ++kk)
+                for (int lane = 0; lane < 32; ++lane) {
+                    const int t = tt * 8 + (lane >> 2), q = kk * 4 + (lane & 3);
+                    double v = 0.0;
+                    if (t < T && q < nq) {
+                        const int a = ti[t] * nq + q, b = tj[t] * nq + q;
+                        if (f == 0) v = (double)(phi[a] * phi[b]);
+                        if (f == 1) v = (double)(gx[a] * gx[b]);
+                        if (f == 2) v = (double)(gy[a] * gy[b]);
+                        if (f == 3) v = (double)(gx[a] * gy[b] + gy[a] * gx[b]);
+                    }
+                    qfrag[(((size_t)f * NTT + tt) * NK + kk) * 32 + lane] = v;
+                }
+    // (3) Phi^T as DMMA A-fragments [MT][KT][32]: lane (g, c) holds Phi[i = 4 kt + c][q = 8 mt + g]
+    const int MT = (4 * NK + 7) / 8, KT = (np + 3) / 4;
+    for (int mt = 0; mt < MT; ++mt)
+        for (int kt = 0; kt < KT; ++kt)
+            for (int lane = 0; lane < 32; ++lane) {
+                const int q = mt * 8 + (lane >> 2), i = kt * 4 + (lane & 3);
+                qfrag.push_back(q < nq && i < np ? (double)phi[i * nq + q] : 0.0);
+            }
     return true;
 }
 
@@ -329,6 +348,7 @@ void fea_destroy(fea_ctx c) {
     if (!c->host_only) cudaSetDevice(c->device);
     c->free_mesh();
     dfree(c->d_tables);
+    dfree(c->d_dbg);
     if (c->comm && nccl().ok) nccl().commDestroy((ncclComm_t)c->comm);
     delete c;
 }
@@ -348,8 +368,9 @@ fea_status fea_set_element(fea_ctx c, int order, int n_q, const double* q_xy, co
     }
     if (fabsl(s - 0.5L) > 1e-14L)
         return c->fail(FEA_E_ARG, "quadrature weights sum to %.17g, expected 1/2 (reference-triangle measure)", (double)s);
-    std::vector<double> tab;
-    if (!build_tables(order, n_q, q_xy, q_w, tab)) return c->fail(FEA_E_UNSUPPORTED, "singular Vandermonde");
+    std::vector<double> ctab, qfrag;
+    if (!build_tables(order, n_q, q_xy, q_w, ctab, qfrag)) return c->fail(FEA_E_UNSUPPORTED, "singular Vandermonde");
+    if (ctab.size() > FEA_CTAB_MAX) return c->fail(FEA_E_UNSUPPORTED, "tables exceed the parameter bank");
     if (!c->host_only) cudaSetDevice(c->device);
     c->free_mesh();
     dfree(c->d_tables);
@@ -359,10 +380,11 @@ fea_status fea_set_element(fea_ctx c, int order, int n_q, const double* q_xy, co
     c->T = c->np * (c->np + 1) / 2;
     c->qxy.assign(q_xy, q_xy + 2 * n_q);
     c->qw.assign(q_w, q_w + n_q);
-    c->tables = tab;
+    c->tables = ctab;
+    c->qfrag = qfrag;
     if (c->host_only) return FEA_OK;
-    FEA_CUDA(c, cudaMalloc(&c->d_tables, tab.size() * sizeof(double)));
-    FEA_CUDA(c, cudaMemcpy(c->d_tables, tab.data(), tab.size() * sizeof(double), cudaMemcpyHostToDevice));
+    FEA_CUDA(c, cudaMalloc(&c->d_tables, qfrag.size() * sizeof(double)));
+    FEA_CUDA(c, cudaMemcpy(c->d_tables, qfrag.data(), qfrag.size() * sizeof(double), cudaMemcpyHostToDevice));
     return FEA_OK;
 }
 
@@ -484,18 +506,6 @@ fea_status fea_set_tuning(fea_ctx c, int key, int64_t value) {
             if (value != 0 && (value < 4096 || value > 232448)) return c->fail(FEA_E_ARG, "smem budget out of range");
             c->tune_smem = value;
             break;
-        case FEA_TUNE_THREADS:
-            if (value < 64 || value > 256 || value % 32) return c->fail(FEA_E_ARG, "threads must be 64..256, multiple of 32");
-            c->tune_threads = value;
-            break;
-        case FEA_TUNE_TCHUNKS:
-            if (value < 0 || value > 64) return c->fail(FEA_E_ARG, "tchunks out of range");
-            c->tune_tchunks = value;
-            break;
-        case 5:  // gathers of block j+1 issued during phase B of block j (double gather buffers)
-            if (value < 0 || value > 1) return c->fail(FEA_E_ARG, "prefetch must be 0 or 1");
-            c->tune_prefetch = value;
-            break;
         case 4:  // plan matrices bitmask (FEA_MASS | FEA_STIFF)
             if (value < 1 || value > 3) return c->fail(FEA_E_ARG, "plan matrices must be a nonzero MASS|STIFF mask");
             c->plan_which = (int)value;
@@ -524,14 +534,15 @@ fea_status fea_build_pattern(fea_ctx c, int64_t* row_begin, int64_t* n_rows_loca
     // ---- shared-memory budget -> elements per block (e_max) and record budget
     const int dm = (c->plan_which & FEA_MASS) ? 1 : 0, dcm = (c->plan_which & FEA_STIFF) ? 1 : 0;
     const int nmat = dm + dcm;
-    c->staged = c->order >= 3 ? 1 : 0;
-    c->threads = (int)c->tune_threads;
-    const int64_t budget = c->tune_smem ? c->tune_smem : (c->order >= 3 ? 225 * 1024 : 110 * 1024);
-    const int64_t tab_bytes = c->staged ? (int64_t)((c->tables.size() * 8 + 15) & ~size_t(15)) : 0;
-    const int64_t per_el_smem = 8LL * T * nmat + (c->tune_prefetch ? 2 : 1) * (8LL * np + 48) + (c->staged ? 8LL * (2 * nq + 3) : 0);
+    const int rstages = c->order <= 2 ? 3 : 2;  // fea_rstages
+    const int ctas = c->order <= 2 ? 2 : 1;     // fea_ctas
+    const int64_t budget = c->tune_smem ? c->tune_smem : (ctas == 2 ? 113 * 1024 : 226 * 1024);
+    const int nqp = 4 * fea_nk_kernel(c->order, nq);
+    const int64_t per_el_smem = 8LL * T * nmat + 2 * (8LL * np + 48) + 2 * 8LL * nqp + 32;
     const double rec_el = 1.3 * (3.0 * np * np + 4.0 * np) + 8;  // record bytes per element (estimate)
-    int64_t e_max = (int64_t)((budget - tab_bytes - 64) / (per_el_smem + 2.0 * rec_el));
+    int64_t e_max = (int64_t)((budget - 256 - 3 * 128) / (per_el_smem + rstages * rec_el));
     e_max = std::min<int64_t>(e_max, 65535 / T);
+    e_max = e_max >= 8 ? ((e_max - 8) / 16) * 16 + 8 : 0;  // multiple of 8, == 8 mod 16
     const int64_t rec_budget = ((int64_t)(rec_el * e_max) + 15) & ~int64_t(15);
 
     // ---- incidence of this rank's rows (ascending library element per row)
@@ -712,14 +723,14 @@ fea_status fea_build_pattern(fea_ctx c, int64_t* row_begin, int64_t* n_rows_loca
     for (int64_t r = 0; r < nr; ++r) c->row_ptr[r + 1] += c->row_ptr[r];
     bo.clear();
 
-    FeaSmemLayout L = fea_smem_layout(c->staged ? (int)c->tables.size() : 0, (int)rec_max, (int)e_max, np, nq, T, dm, dcm,
-                                      c->staged, (int)c->tune_prefetch);
+    int32_t L[FEA_L_N];
+    fea_smem_layout(L, rstages, (int)rec_max, (int)e_max, c->order, nq, dm, dcm);
     c->nblocks = (int)nb;
     c->e_max = (int)e_max;
     c->rec_max = (int)rec_max;
     c->nnz = nnz;
-    c->smem_bytes = L.total;
-    std::memcpy(c->lay, &L, sizeof(c->lay));
+    c->smem_bytes = L[FEA_L_TOTAL];
+    std::memcpy(c->lay, L, sizeof(c->lay));
     c->stat_visits = visits;
     c->stat_owned = owned;
     c->stat_entries = ncon;
@@ -738,11 +749,8 @@ fea_status fea_build_pattern(fea_ctx c, int64_t* row_begin, int64_t* n_rows_loca
     FEA_CUDA(c, cudaMemcpy(c->d_records, records.data(), records.size(), cudaMemcpyHostToDevice));
     if (!c->d_ufull) FEA_CUDA(c, cudaMalloc(&c->d_ufull, (size_t)rpr * c->world * sizeof(double)));
     if (!c->d_usend) FEA_CUDA(c, cudaMalloc(&c->d_usend, (size_t)rpr * sizeof(double)));
-    int tc = (int)c->tune_tchunks;
-    if (tc <= 0) tc = c->order == 4 ? 4 : c->order == 3 ? 2 : 1;
-    c->ntc = c->staged ? tc : 1;
     int occ = 0;
-    int rc = fea_kernel_occupancy(c->order, c->nq, dm, dcm, c->staged, c->threads, c->smem_bytes, &occ);
+    int rc = fea_kernel_occupancy(c->order, c->nq, dm, dcm, c->smem_bytes, &occ, &c->threads);
     if (rc != 0) return c->fail(FEA_E_CUDA, "occupancy query: %s", cudaGetErrorString((cudaError_t)rc));
     if (occ < 1) return c->fail(FEA_E_UNSUPPORTED, "kernel does not fit: %d B shared memory", c->smem_bytes);
     c->grid = (int)std::min<int64_t>(std::max<int64_t>(nb, 1), (int64_t)occ * c->sm_count);
@@ -807,28 +815,28 @@ static fea_status launch(fea_ctx c, const double* u, double* vm, double* vc) {
     FeaKParams prm{};
     prm.blocks = c->d_blocks;
     prm.records = c->d_records;
-    prm.nblocks = c->nblocks;
-    prm.e_max = c->e_max;
-    prm.rec_max = c->rec_max;
-    prm.nq = c->nq;
     prm.xy = c->d_xy;
     prm.u = u;
-    prm.tables = c->d_tables;
-    prm.tables_doubles = (int32_t)c->tables.size();
-    prm.prefetch = (int32_t)c->tune_prefetch;
-    if (!c->staged) {
-        if (c->tables.size() > FEA_CTAB_MAX) return c->fail(FEA_E_UNSUPPORTED, "tables exceed the parameter bank");
-        std::memcpy(prm.ctab, c->tables.data(), c->tables.size() * sizeof(double));
-    }
-    prm.ntc = c->ntc;
-    prm.same_coef = same_coef(c->coef_m, c->coef_c) ? 1 : 0;
-    prm.coef_m = c->coef_m;
-    prm.coef_c = c->coef_c;
+    prm.qfrag = c->d_tables;
     prm.out_m = vm;
     prm.out_c = vc;
+    prm.nblocks = c->nblocks;
+    prm.e_max = c->e_max;
+    prm.nq = c->nq;
+    prm.same_coef = same_coef(c->coef_m, c->coef_c) ? 1 : 0;
     std::memcpy(prm.lay, c->lay, sizeof(prm.lay));
+    prm.coef_m = c->coef_m;
+    prm.coef_c = c->coef_c;
+    std::memcpy(prm.ctab, c->tables.data(), c->tables.size() * sizeof(double));
+    if (getenv("FEA_DEBUG_TIMING")) {
+        if (!c->d_dbg) {
+            FEA_CUDA(c, cudaMalloc(&c->d_dbg, 8 * sizeof(unsigned long long)));
+            FEA_CUDA(c, cudaMemset(c->d_dbg, 0, 8 * sizeof(unsigned long long)));
+        }
+        prm.dbg = c->d_dbg;
+    }
     if (c->nblocks == 0) return FEA_OK;
-    const int rc = fea_launch_reassemble(prm, c->order, c->threads, c->smem_bytes, c->grid, c->staged, c->stream);
+    const int rc = fea_launch_reassemble(prm, c->order, c->smem_bytes, c->grid, c->stream);
     if (rc != 0) return c->fail(FEA_E_CUDA, "k_reassemble launch: %s", cudaGetErrorString((cudaError_t)rc));
     return FEA_OK;
 }
@@ -951,6 +959,12 @@ fea_status fea_get_stat(fea_ctx c, int key, int64_t* value) {
         case 7: *value = c->e_max; break;
         case 8: *value = c->grid; break;
         case 9: *value = c->record_bytes; break;
+        case 20: case 21: case 22: case 23: case 24: case 25: {  // FEA_DEBUG_TIMING cycle sums
+            unsigned long long v = 0;
+            if (c->d_dbg) FEA_CUDA(c, cudaMemcpy(&v, c->d_dbg + (key - 20), sizeof(v), cudaMemcpyDeviceToHost));
+            *value = (int64_t)v;
+            break;
+        }
         case 10: *value = c->rec_max; break;
         default: return c->fail(FEA_E_ARG, "unknown stat key %d", key);
     }

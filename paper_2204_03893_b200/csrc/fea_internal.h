@@ -7,10 +7,31 @@
 #define FEA_MAX_NP 15
 #define FEA_MAX_NQ 16
 #define FEA_MAX_PAR 16
-// Reference tables small enough to travel in the kernel parameters (constant bank): p <= 2
-// (P2 with 16 points: Phi 6x16 + w 16 + Q 21x16x4 = 1456 doubles).  Larger orders stage them
-// in shared memory.
-#define FEA_CTAB_MAX 1464
+#define FEA_MAX_CLASSES 64
+// Phi [np][nq] (pad2) + w [nq] travel in the kernel parameters (constant bank).
+#define FEA_CTAB_MAX 272
+
+// Tiling of the B.W contraction on the FP64 tensor cores (mma.sync.m8n8k4.f64 = DMMA):
+// the symmetric rows t (T = n_p (n_p + 1) / 2) in tiles of 8, the quadrature points in
+// k-steps of 4, 8 elements per n-tile.  Consumer warp w owns row tile w % NTT and every
+// S-th element tile.
+__host__ __device__ constexpr int fea_np(int p) { return (p + 1) * (p + 2) / 2; }
+__host__ __device__ constexpr int fea_T(int p) { return fea_np(p) * (fea_np(p) + 1) / 2; }
+__host__ __device__ constexpr int fea_ntt(int p) { return (fea_T(p) + 7) / 8; }
+__host__ __device__ constexpr int fea_nk(int nq) { return (nq + 3) / 4; }
+// rules with a specialised kernel (the configs' minimal Dunavant rules); other n_q run the
+// generic kernel, which pads the quadrature dimension to 16 (4 k-steps)
+__host__ __device__ constexpr int fea_nq_native(int p) { return p == 1 ? 3 : p == 2 ? 6 : p == 3 ? 12 : 16; }
+__host__ __device__ constexpr int fea_nk_kernel(int p, int nq) { return nq == fea_nq_native(p) ? fea_nk(nq) : 4; }
+// element-tile subsets per row tile (consumer warps = NTT * S)
+__host__ __device__ constexpr int fea_S(int p) { return p == 1 ? 8 : p == 2 ? 3 : p == 3 ? 2 : 1; }
+__host__ __device__ constexpr int fea_ctas(int p) { return p <= 2 ? 2 : 1; }
+__host__ __device__ constexpr int fea_rstages(int p) { return p <= 2 ? 3 : 2; }
+__host__ __device__ constexpr int fea_threads(int p) { return (fea_ntt(p) * fea_S(p) + 1) * 32; }
+// p >= 2: the interpolation U = Phi^T U_e also runs on DMMA (M = quadrature points in tiles of
+// 8, K = element nodes in k-steps of 4); A-fragments of Phi^T [MT][KT][32] follow Q_f in qfrag.
+__host__ __device__ constexpr bool fea_interp_mma(int p) { return p >= 2; }
+__host__ __device__ constexpr int fea_kt(int p) { return (fea_np(p) + 3) / 4; }
 
 // One unit of CTA work: a contiguous block of library rows whose CSR slots
 // [slot0, slot0 + nslots) are produced by exactly one CTA.  Everything the block streams
@@ -36,8 +57,6 @@ struct FeaBlock {
     int32_t pad_;
 };
 
-#define FEA_MAX_CLASSES 64
-
 __host__ __device__ inline int32_t fea_pad16(int32_t b) { return (b + 15) & ~15; }
 __host__ __device__ inline int32_t fea_pad4(int32_t n) { return (n + 3) & ~3; }
 __host__ __device__ inline int32_t fea_rec_off_items(const FeaBlock& b) { return fea_pad16(12 * b.ncls); }
@@ -58,60 +77,53 @@ struct FeaCoef {
     double par[FEA_MAX_PAR];
 };
 
-// Kernel parameters (passed by value as __grid_constant__).
-struct FeaKParams {
-    const FeaBlock* blocks;
-    const uint8_t* records;  // all block records
-    int32_t nblocks;
-    int32_t e_max;           // V row stride (elements per block, max)
-    int32_t rec_max;         // record buffer size in shared memory (bytes, multiple of 16)
-    int32_t nq;
-    const double2* xy;       // [n_dof] DOF coordinates (vertex DOFs used for B_e)
-    const double* u;         // [n_dof] u_full, library numbering
-    const double* tables;    // Phi [np][nq], w [nq], Q [T][nq][4]
-    int32_t tables_doubles;
-    int32_t ntc;             // number of t-chunks per element (STAGED kernels)
-    int32_t same_coef;       // mass and stiffness share k -> one Lambda
-    int32_t pad_;
-    double* out_m;           // [nslots_total] (rank-local slot index) or nullptr
-    double* out_c;
-    FeaCoef coef_m;
-    FeaCoef coef_c;
-    int32_t lay[12];         // FeaSmemLayout of the plan (byte offsets)
-    int32_t prefetch;        // gathers of block j+1 issued before phase B of block j
-    int32_t pad2_;
-    double ctab[FEA_CTAB_MAX];  // tables for p <= 2 (same layout as `tables`)
-};
-
-// Shared-memory layout (bytes) of k_reassemble for a plan; identical on host and device.
-struct FeaSmemLayout {
-    int32_t tab, rec0, rec1, gu, gx, vm, vc, lam, bars, total, gu1, gx1;
-};
+// Shared-memory layout (byte offsets) of k_reassemble for a plan; identical on host and device.
+enum { FEA_L_REC = 0, FEA_L_GU = 3, FEA_L_GX = 5, FEA_L_LAMM = 7, FEA_L_LAMC = 8, FEA_L_W = 9, FEA_L_VM = 10,
+       FEA_L_VC = 11, FEA_L_BARS = 12, FEA_L_TOTAL = 13, FEA_L_N = 14 };
 
 __host__ __device__ inline int32_t fea_align(int32_t v, int32_t a) { return (v + a - 1) / a * a; }
 
-__host__ __device__ inline FeaSmemLayout fea_smem_layout(int tables_doubles, int rec_max, int e_max, int np, int nq,
-                                                         int T, int do_m, int do_c, int staged, int prefetch) {
-    FeaSmemLayout L;
+// e_max is a multiple of 8 (element tiles) and == 8 mod 16 (conflict-free 16-byte V stores).
+__host__ __device__ inline void fea_smem_layout(int32_t* L, int rstages, int rec_max, int e_max, int p, int nq,
+                                                int do_m, int do_c) {
+    const int np = fea_np(p), T = fea_T(p);
+    const int nqp = 4 * fea_nk_kernel(p, nq);
     int32_t o = 0;
-    L.tab = o;  o = fea_align(o + 8 * tables_doubles, 16);
-    L.rec0 = o; o = fea_align(o + rec_max, 16);
-    L.rec1 = o; o = fea_align(o + rec_max, 16);
-    L.gu = o;   o = fea_align(o + 8 * np * e_max, 16);
-    L.gx = o;   o = fea_align(o + 16 * 3 * e_max, 16);
-    L.gu1 = o;  o = fea_align(o + (prefetch ? 8 * np * e_max : 0), 16);
-    L.gx1 = o;  o = fea_align(o + (prefetch ? 16 * 3 * e_max : 0), 16);
-    L.vm = o;   o = fea_align(o + (do_m ? 8 * T * e_max : 0), 16);
-    L.vc = o;   o = fea_align(o + (do_c ? 8 * T * e_max : 0), 16);
-    L.lam = o;  o = fea_align(o + (staged ? 8 * (2 * nq + 3) * e_max : 0), 16);
-    L.bars = o; o += 16;
-    L.total = o;
-    return L;
+    for (int s = 0; s < 3; ++s) { L[FEA_L_REC + s] = o; o = fea_align(o + (s < rstages ? rec_max : 0), 128); }
+    for (int s = 0; s < 2; ++s) {
+        L[FEA_L_GU + s] = o; o = fea_align(o + 8 * np * e_max, 16);
+        L[FEA_L_GX + s] = o; o = fea_align(o + 16 * 3 * e_max, 16);
+    }
+    L[FEA_L_LAMM] = o; o = fea_align(o + 8 * nqp * e_max, 16);
+    L[FEA_L_LAMC] = o; o = fea_align(o + 8 * nqp * e_max, 16);
+    L[FEA_L_W] = o;    o = fea_align(o + 8 * 4 * e_max, 16);  // A00, A11, A01, |det B_e|
+    L[FEA_L_VM] = o;   o = fea_align(o + (do_m ? 8 * T * e_max : 0), 16);
+    L[FEA_L_VC] = o;   o = fea_align(o + (do_c ? 8 * T * e_max : 0), 16);
+    L[FEA_L_BARS] = o; o += 16 * 8;
+    L[FEA_L_TOTAL] = o;
 }
 
+// Kernel parameters (passed by value as __grid_constant__).
+struct FeaKParams {
+    const FeaBlock* blocks;
+    const uint8_t* records;   // all block records
+    const double2* xy;        // [n_dof] DOF coordinates (vertex DOFs give B_e)
+    const double* u;          // [n_dof] u_full, library numbering
+    const double* qfrag;      // Q_f A-fragments [4][NTT][NK][32] (lane order), zero padded
+    double* out_m;            // [nslots_total] (rank-local slot index) or nullptr
+    double* out_c;
+    unsigned long long* dbg;  // optional per-phase cycle counters (FEA_DEBUG_TIMING), else nullptr
+    int32_t nblocks;
+    int32_t e_max;            // V / Lambda row stride (elements per block, max)
+    int32_t nq;
+    int32_t same_coef;        // mass and stiffness share k -> one Lambda
+    int32_t lay[FEA_L_N];     // shared-memory layout (byte offsets)
+    FeaCoef coef_m;
+    FeaCoef coef_c;
+    double ctab[FEA_CTAB_MAX];  // Phi [np][nq] at 0, w [nq] at pad2(np nq)
+};
+
 // Launch the fused reassembly kernel (defined in fea_kernels.cu).  Returns a cudaError_t.
-int fea_launch_reassemble(const FeaKParams& prm, int order, int threads, int smem_bytes, int grid,
-                          int staged, void* stream);
-// Query the per-SM CTA occupancy for the kernel variant (for persistent grid sizing).
-int fea_kernel_occupancy(int order, int nq, int do_m, int do_c, int staged, int threads, int smem_bytes,
-                         int* ctas_per_sm);
+int fea_launch_reassemble(const FeaKParams& prm, int order, int smem_bytes, int grid, void* stream);
+// Per-SM CTA occupancy of the kernel variant and its block size (threads).
+int fea_kernel_occupancy(int order, int nq, int do_m, int do_c, int smem_bytes, int* ctas_per_sm, int* threads);

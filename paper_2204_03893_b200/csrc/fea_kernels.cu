@@ -1,25 +1,27 @@
-// fea_kernels.cu -- sm_100a kernels of the per-iteration hot path.
+// fea_kernels.cu -- sm_100a kernel of the per-iteration hot path.
 //
-// k_reassemble: ONE persistent kernel per reassembly.  Each CTA loops over row blocks
-// (FeaBlock, grid-strided).  Pipeline per block j of a CTA:
-//   * TMA bulk copy (cp.async.bulk, mbarrier complete_tx) of block j+1's contiguous record
-//     (counts, contributor stream, chunk bases, element DOFs) into the other of two record
-//     buffers -- issued before block j is processed, so HBM streams while block j computes;
-//   * cp.async gathers of u(N_e) and the vertex coordinates of block j's elements into
-//     shared memory (all issued at once: deep memory-level parallelism);
-//   * Phase A  (Algorithm 2 lines 5-11) per element:
-//              b_e = |det B_e|, A_e = (B_e^T B_e)^{-1}
-//              u_q = Phi^T u_e ; S_qe = k(u_q)
-//              lambda_q = w_q S_qe b_e
-//              V_m[t] = sum_q Q_m[t,q] lambda_q
-//              V_c[t] = sum_f W_f sum_q Q_c[t,(q,f)] lambda_q
-//            for the symmetric rows t = (i <= j) only, into shared memory.
-//            (The stiffness sum over f = {A00, A11, A01} of X_c = Lambda (.) W is taken
-//            after the q-sum -- a reassociation of Q_c (Lambda (.) W).)
-//   * Phase B  (Algorithm 2 line 12): every CSR slot of the block is the sum of
-//            its contributors V[t, e] in ascending library element order (fixed-order
-//            segmented reduction over the contributor stream, no atomics); coalesced stores
-//            of the block's contiguous slot range.
+// k_reassemble<P, NQ, DO_M, DO_C>: ONE persistent, warp-specialised kernel per reassembly.
+// Each CTA loops over row blocks (FeaBlock, grid-strided).
+//
+//   PRODUCER warp (the last warp), up to two blocks ahead of the consumers:
+//     * one TMA bulk copy (cp.async.bulk + mbarrier complete_tx) per block of its contiguous
+//       record (count classes, slot items, contributor stream, element DOFs);
+//     * cp.async gathers of u(N_e) and the vertex coordinates of every element of the block
+//       into a shared-memory stage, completion signalled with cp.async.mbarrier.arrive.
+//   CONSUMER warps, per block:
+//     A1 (Algorithm 2 lines 4-9), one thread per element:
+//          b_e = |det B_e|, W_e = vec A_e, A_e = (B_e^T B_e)^{-1}
+//          u_q = Phi^T u_e ; S_qe = k(u_q)
+//          Lambda_qe = w_q S_qe b_e                                    (Eq. def_lambda)
+//     A2 (Algorithm 2 lines 10-11) on the FP64 tensor cores (DMMA):
+//          V_m = Q_m Lambda ; V_c = sum_f W_f (Q_c,f Lambda),  f in {A00, A11, A01}
+//          for the symmetric rows t = (i <= j) only.  The sum over f of
+//          Q_c (Lambda (.) W) is taken after the q-contraction (a reassociation);
+//          each warp keeps its row tile of Q_f as DMMA A-fragments in registers.
+//     B  (Algorithm 2 line 12): every CSR slot of the block = sum of its
+//          contributors V[t, e] in ascending library element order (fixed-order segmented
+//          reduction over the contributor stream, no atomics); slots grouped by contributor
+//          count so warps run uniform trip counts.
 #include <cuda_runtime.h>
 #include <cstdint>
 
@@ -33,14 +35,13 @@ __device__ __forceinline__ uint32_t smem_u32(const void* p) { return (uint32_t)_
 __device__ __forceinline__ void mbar_init(uint64_t* bar, uint32_t count) {
     asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_u32(bar)), "r"(count) : "memory");
 }
-__device__ __forceinline__ void fence_mbar_init() {
-    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
-}
-__device__ __forceinline__ void fence_proxy_async() {
-    asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
-}
+__device__ __forceinline__ void fence_mbar_init() { asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory"); }
+__device__ __forceinline__ void fence_proxy_async() { asm volatile("fence.proxy.async.shared::cta;" ::: "memory"); }
 __device__ __forceinline__ void mbar_expect_tx(uint64_t* bar, uint32_t bytes) {
     asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(bar)), "r"(bytes) : "memory");
+}
+__device__ __forceinline__ void mbar_arrive(uint64_t* bar) {
+    asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(smem_u32(bar)) : "memory");
 }
 __device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity) {
     asm volatile(
@@ -64,16 +65,44 @@ __device__ __forceinline__ void cp_async8(void* dst, const void* src) {
 __device__ __forceinline__ void cp_async16(void* dst, const void* src) {
     asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(smem_u32(dst)), "l"(src) : "memory");
 }
-__device__ __forceinline__ void cp_async_wait_all() {
-    asm volatile("cp.async.commit_group;\n\tcp.async.wait_group 0;" ::: "memory");
+// arrive on `bar` once all prior cp.async of this thread have completed
+__device__ __forceinline__ void cp_async_mbar_arrive(uint64_t* bar) {
+    asm volatile("cp.async.mbarrier.arrive.noinc.shared::cta.b64 [%0];" ::"r"(smem_u32(bar)) : "memory");
+}
+__device__ __forceinline__ void consumer_sync(int nct) {  // named barrier 1: consumer warps only
+    asm volatile("bar.sync 1, %0;" ::"r"(nct) : "memory");
+}
+// D = A (8x4, row) * B (4x8, col) + D on the FP64 tensor core; fragment ownership per lane
+// (g = lane / 4, c = lane % 4): a = A[g][c], b = B[c][g], d = D[g][2c .. 2c+1].
+__device__ __forceinline__ void dmma(double& d0, double& d1, double a, double b) {
+    asm volatile("mma.sync.aligned.m8n8k4.row.col.f64.f64.f64.f64 {%0,%1}, {%2}, {%3}, {%0,%1};"
+                 : "+d"(d0), "+d"(d1)
+                 : "d"(a), "d"(b));
 }
 
 // ------------------------------------------------------------------ math
+template <int N>
+__device__ __forceinline__ double horner(const double* par, double u) {  // sum_{i<N} par[i] u^i
+    double r = par[N - 1];
+#pragma unroll
+    for (int i = N - 2; i >= 0; --i) r = fma(r, u, par[i]);
+    return r;
+}
+
+// k(u); the branch is warp-uniform (one coefficient per launch), each case straight-line.
 __device__ __forceinline__ double keval(const FeaCoef& c, double u) {
-    if (c.kind == 0) {  // sum_i par[i] u^i (Horner)
-        double r = c.par[c.npar - 1];
-        for (int i = c.npar - 2; i >= 0; --i) r = fma(r, u, c.par[i]);
-        return r;
+    if (c.kind == 0) {
+        switch (c.npar) {
+            case 1: return c.par[0];
+            case 2: return horner<2>(c.par, u);
+            case 3: return horner<3>(c.par, u);
+            case 4: return horner<4>(c.par, u);
+            case 5: return horner<5>(c.par, u);
+            case 6: return horner<6>(c.par, u);
+            case 7: return horner<7>(c.par, u);
+            case 8: return horner<8>(c.par, u);
+            default: return horner<9>(c.par, u);
+        }
     }
     if (c.kind == 1) return c.par[0] * exp(c.par[1] * u);
     // piecewise linear, segment s covers (T_s, T_{s+1}]
@@ -91,120 +120,13 @@ __device__ __forceinline__ void geometry(const double2* __restrict__ gX, int e_m
     const double B00 = b.x - a.x, B10 = b.y - a.y, B01 = c.x - a.x, B11 = c.y - a.y;
     const double det = B00 * B11 - B01 * B10;
     absdet = fabs(det);
-    const double G00 = B00 * B00 + B10 * B10;
-    const double G01 = B00 * B01 + B10 * B11;
-    const double G11 = B01 * B01 + B11 * B11;
     const double inv = 1.0 / (det * det);  // det(B^T B) = det(B)^2
-    A00 = G11 * inv;
-    A11 = G00 * inv;
-    A01 = -G01 * inv;
+    A00 = (B01 * B01 + B11 * B11) * inv;
+    A11 = (B00 * B00 + B10 * B10) * inv;
+    A01 = -(B00 * B01 + B10 * B11) * inv;
 }
 
-// lambda_q = w_q * k(u_q) * |det B_e|, u_q = sum_i Phi[i,q] u_i
-template <int NP, int NQM>
-__device__ __forceinline__ void form_lambda(const double* __restrict__ sPhi, const double* __restrict__ sW, int nq,
-                                            const double* __restrict__ gU, int e_max, int le, double absdet,
-                                            const FeaCoef& coef, double (&lam)[NQM]) {
-    double ue[NP];
-#pragma unroll
-    for (int i = 0; i < NP; ++i) ue[i] = gU[i * e_max + le];
-#pragma unroll
-    for (int q = 0; q < NQM; ++q) {
-        if (q < nq) {
-            double uq = 0.0;
-#pragma unroll
-            for (int i = 0; i < NP; ++i) uq = fma(sPhi[i * nq + q], ue[i], uq);
-            lam[q] = sW[q] * keval(coef, uq) * absdet;
-        } else {
-            lam[q] = 0.0;
-        }
-    }
-}
-
-// V rows [t0, t1) of two elements (le0, le1) from Lambda (registers) and the Q table
-// (shared memory, [T][nq][4] = m, c00, c11, c01 -> two 16-byte broadcast loads per q).
-template <int NQM, bool DO_M, bool DO_C>
-__device__ __forceinline__ void contract2(const double* __restrict__ sQ, int nq, int t0, int t1,
-                                          const double (&lm0)[NQM], const double (&lc0)[NQM],
-                                          const double (&lm1)[NQM], const double (&lc1)[NQM],
-                                          const double (&W0)[3], const double (&W1)[3], double* __restrict__ sVm,
-                                          double* __restrict__ sVc, int e_max, int le0, int le1, bool has1) {
-#pragma unroll 1
-    for (int t = t0; t < t1; ++t) {
-        const double2* Qt = reinterpret_cast<const double2*>(sQ + t * nq * 4);
-        double vm0 = 0.0, a0 = 0.0, b0 = 0.0, c0 = 0.0;
-        double vm1 = 0.0, a1 = 0.0, b1 = 0.0, c1 = 0.0;
-#pragma unroll
-        for (int q = 0; q < NQM; ++q) {
-            if (q < nq) {
-                const double2 qa = Qt[2 * q], qb = Qt[2 * q + 1];  // (m, c00), (c11, c01)
-                if (DO_M) {
-                    vm0 = fma(qa.x, lm0[q], vm0);
-                    vm1 = fma(qa.x, lm1[q], vm1);
-                }
-                if (DO_C) {
-                    a0 = fma(qa.y, lc0[q], a0);
-                    b0 = fma(qb.x, lc0[q], b0);
-                    c0 = fma(qb.y, lc0[q], c0);
-                    a1 = fma(qa.y, lc1[q], a1);
-                    b1 = fma(qb.x, lc1[q], b1);
-                    c1 = fma(qb.y, lc1[q], c1);
-                }
-            }
-        }
-        if (DO_M) {
-            sVm[t * e_max + le0] = vm0;
-            if (has1) sVm[t * e_max + le1] = vm1;
-        }
-        if (DO_C) {
-            sVc[t * e_max + le0] = fma(W0[0], a0, fma(W0[1], b0, W0[2] * c0));
-            if (has1) sVc[t * e_max + le1] = fma(W1[0], a1, fma(W1[1], b1, W1[2] * c1));
-        }
-    }
-}
-
-// p <= 2 with the native rule: one element, tables read straight from the kernel parameters
-// (constant bank operands of DFMA, fully unrolled over t and q; no shared-memory loads).
-template <int NP, int NQ, bool DO_M, bool DO_C>
-__device__ __forceinline__ void element_const(const FeaKParams& prm, const double* __restrict__ gU,
-                                              const double2* __restrict__ gX, int e_max, int le, bool two_lam,
-                                              double* __restrict__ sVm, double* __restrict__ sVc) {
-    constexpr int T = NP * (NP + 1) / 2;
-    constexpr int oW = (NP * NQ + 1) & ~1;
-    constexpr int oQ = oW + ((NQ + 1) & ~1);
-    double absdet, A00, A11, A01;
-    geometry(gX, e_max, le, absdet, A00, A11, A01);
-    double ue[NP];
-#pragma unroll
-    for (int i = 0; i < NP; ++i) ue[i] = gU[i * e_max + le];
-    double lm[NQ], lc[NQ];
-#pragma unroll
-    for (int q = 0; q < NQ; ++q) {
-        double uq = 0.0;
-#pragma unroll
-        for (int i = 0; i < NP; ++i) uq = fma(prm.ctab[i * NQ + q], ue[i], uq);
-        const double wb = prm.ctab[oW + q] * absdet;
-        lm[q] = wb * keval(DO_M ? prm.coef_m : prm.coef_c, uq);
-        lc[q] = two_lam ? wb * keval(prm.coef_c, uq) : lm[q];
-    }
-#pragma unroll
-    for (int t = 0; t < T; ++t) {
-        double vm = 0.0, a = 0.0, b = 0.0, c = 0.0;
-#pragma unroll
-        for (int q = 0; q < NQ; ++q) {
-            const double* Qq = prm.ctab + oQ + (t * NQ + q) * 4;
-            if (DO_M) vm = fma(Qq[0], lm[q], vm);
-            if (DO_C) {
-                a = fma(Qq[1], lc[q], a);
-                b = fma(Qq[2], lc[q], b);
-                c = fma(Qq[3], lc[q], c);
-            }
-        }
-        if (DO_M) sVm[t * e_max + le] = vm;
-        if (DO_C) sVc[t * e_max + le] = fma(A00, a, fma(A11, b, A01 * c));
-    }
-}
-
+// ------------------------------------------------------------------ phase B helpers
 // Sum of the C contributors of one slot in the fixed (stored) order, all loads issued first.
 template <int C, bool DO_M, bool DO_C>
 __device__ __forceinline__ void slot_sum(const uint16_t* __restrict__ cp, const double* __restrict__ sVm,
@@ -275,174 +197,260 @@ __device__ __forceinline__ void class_items_generic(int c, int i0, int i1, int c
     }
 }
 
-template <int P, int NQ_T, bool DO_M, bool DO_C, bool STAGED>
-__global__ void __launch_bounds__(256, STAGED ? 1 : 2) k_reassemble(const __grid_constant__ FeaKParams prm) {
-    constexpr int NP = (P + 1) * (P + 2) / 2;
-    constexpr int T = NP * (NP + 1) / 2;
-    constexpr int NQM = NQ_T > 0 ? NQ_T : FEA_MAX_NQ;
+// ------------------------------------------------------------------ the kernel
+template <int P, int NQ_T, bool DO_M, bool DO_C>
+__global__ void __launch_bounds__(fea_threads(P), fea_ctas(P)) k_reassemble(const __grid_constant__ FeaKParams prm) {
+    constexpr int NP = fea_np(P);
+    constexpr int T = fea_T(P);
+    constexpr int NTT = fea_ntt(P);
+    constexpr int S = fea_S(P);
+    constexpr int RS = fea_rstages(P);
+    constexpr int NK = NQ_T > 0 ? fea_nk(NQ_T) : fea_nk(FEA_MAX_NQ);  // k-steps (generic rule: 4, zero padded)
+    constexpr int NQP = 4 * NK;                                       // padded quadrature count
     const int nq = NQ_T > 0 ? NQ_T : prm.nq;
     const int e_max = prm.e_max;
-    const int tid = threadIdx.x, nthr = blockDim.x;
+    const int tid = threadIdx.x;
+    constexpr int NCT = NTT * S * 32;  // consumer threads
+    const bool producer = tid >= NCT;
+    const int lane = tid & 31, warp = tid >> 5;
 
     extern __shared__ __align__(128) uint8_t smem[];
-    // p >= 3: tables in shared memory; p <= 2: tables in the kernel parameters (prm.ctab)
-    double* sTab = reinterpret_cast<double*>(smem + prm.lay[0]);
-    const double* tab = STAGED ? static_cast<const double*>(sTab) : prm.ctab;
-    const double* sPhi = tab;
-    const double* sW = tab + ((NP * nq + 1) & ~1);
-    const double* sQ = sW + ((nq + 1) & ~1);
-    uint8_t* sRec0 = smem + prm.lay[1];
-    uint8_t* sRec1 = smem + prm.lay[2];
-    const bool pf = prm.prefetch != 0;
-    double* gUb[2] = {reinterpret_cast<double*>(smem + prm.lay[3]), reinterpret_cast<double*>(smem + prm.lay[pf ? 10 : 3])};
-    double2* gXb[2] = {reinterpret_cast<double2*>(smem + prm.lay[4]), reinterpret_cast<double2*>(smem + prm.lay[pf ? 11 : 4])};
-    double* sVm = reinterpret_cast<double*>(smem + prm.lay[5]);
-    double* sVc = reinterpret_cast<double*>(smem + prm.lay[6]);
-    double* sLam = reinterpret_cast<double*>(smem + prm.lay[7]);
-    uint64_t* bars = reinterpret_cast<uint64_t*>(smem + prm.lay[8]);
+    // stage pointers (computed, not arrays: no local-memory indexing)
+    auto sRec = [&](int s) { return smem + prm.lay[FEA_L_REC + s]; };
+    auto gUb = [&](int s) { return reinterpret_cast<double*>(smem + prm.lay[FEA_L_GU + s]); };
+    auto gXb = [&](int s) { return reinterpret_cast<double2*>(smem + prm.lay[FEA_L_GX + s]); };
+    double* sLm = reinterpret_cast<double*>(smem + prm.lay[FEA_L_LAMM]);
+    double* sLc = reinterpret_cast<double*>(smem + prm.lay[FEA_L_LAMC]);
+    double* sW = reinterpret_cast<double*>(smem + prm.lay[FEA_L_W]);
+    double* sVm = reinterpret_cast<double*>(smem + prm.lay[FEA_L_VM]);
+    double* sVc = reinterpret_cast<double*>(smem + prm.lay[FEA_L_VC]);
+    uint64_t* bars = reinterpret_cast<uint64_t*>(smem + prm.lay[FEA_L_BARS]);
+    uint64_t* full_rec = bars;      // [3] record landed (TMA transactions)
+    uint64_t* full_gat = bars + 3;  // [2] gathers landed (32 producer lanes)
+    uint64_t* rdone = bars + 5;     // [3] consumers finished with the record stage
+    uint64_t* gdone = bars + 8;     // [2] consumers finished with the gather stage
     const bool two_lam = DO_M && DO_C && !prm.same_coef;
+    const int ncta_blocks = prm.nblocks > (int)blockIdx.x ? (prm.nblocks - 1 - (int)blockIdx.x) / (int)gridDim.x + 1 : 0;
 
     if (tid == 0) {
-        mbar_init(&bars[0], 1);
-        mbar_init(&bars[1], 1);
+        for (int s = 0; s < 3; ++s) {
+            mbar_init(&full_rec[s], 1);
+            mbar_init(&rdone[s], 1);
+        }
+        for (int s = 0; s < 2; ++s) {
+            mbar_init(&full_gat[s], 32);
+            mbar_init(&gdone[s], 1);
+        }
         fence_mbar_init();
     }
-    if constexpr (STAGED)
-        for (int i = tid; i < prm.tables_doubles; i += nthr) sTab[i] = __ldg(prm.tables + i);
     __syncthreads();
 
-    auto issue = [&](int b, int buf) {
-        const FeaBlock nb = prm.blocks[b];
-        uint8_t* dst = buf ? sRec1 : sRec0;
-        fence_proxy_async();
-        mbar_expect_tx(&bars[buf], (uint32_t)nb.rec_bytes);
-        tma_load_1d(dst, prm.records + nb.rec_off, (uint32_t)nb.rec_bytes, &bars[buf]);
-    };
-    // gathers of u(N_e) and the vertex coordinates of a block into gather buffer g (async)
-    auto gather = [&](const FeaBlock& gb, const uint8_t* grec, int g) {
-        const int nEp_ = fea_pad4(gb.nE);
-        const int32_t* gd = reinterpret_cast<const int32_t*>(grec + fea_rec_off_dofs(gb));
-        double* gu = gUb[g];
-        double2* gx = gXb[g];
-        for (int le = tid; le < gb.nE; le += nthr) {
+    if (producer) {
+        auto issue_rec = [&](int jj) {  // TMA of the record of the CTA's jj-th block
+            const FeaBlock b = prm.blocks[blockIdx.x + jj * gridDim.x];
+            const int s = jj % RS;
+            fence_proxy_async();
+            mbar_expect_tx(&full_rec[s], (uint32_t)b.rec_bytes);
+            tma_load_1d(sRec(s), prm.records + b.rec_off, (uint32_t)b.rec_bytes, &full_rec[s]);
+        };
+        if (lane == 0)
+            for (int jj = 0; jj < RS - 1 && jj < ncta_blocks; ++jj) issue_rec(jj);
+        for (int j = 0; j < ncta_blocks; ++j) {
+            const FeaBlock blk = prm.blocks[blockIdx.x + j * gridDim.x];
+            const int rs = j % RS, gs = j & 1;
+            if (j >= 2) mbar_wait(&gdone[gs], (uint32_t)(((j >> 1) - 1) & 1));  // stage free (block j-2)
+            mbar_wait(&full_rec[rs], (uint32_t)((j / RS) & 1));                   // record j landed
+            const int nEp = fea_pad4(blk.nE);
+            const int32_t* gd = reinterpret_cast<const int32_t*>(sRec(rs) + fea_rec_off_dofs(blk));
+            double* gu = gUb(gs);
+            double2* gx = gXb(gs);
+            for (int le = lane; le < blk.nE; le += 32) {
 #pragma unroll
-            for (int i = 0; i < NP; ++i) cp_async8(gu + i * e_max + le, prm.u + gd[i * nEp_ + le]);
+                for (int i = 0; i < NP; ++i) cp_async8(gu + i * e_max + le, prm.u + gd[i * nEp + le]);
 #pragma unroll
-            for (int v = 0; v < 3; ++v) cp_async16(gx + v * e_max + le, prm.xy + gd[v * nEp_ + le]);
+                for (int v = 0; v < 3; ++v) cp_async16(gx + v * e_max + le, prm.xy + gd[v * nEp + le]);
+            }
+            cp_async_mbar_arrive(&full_gat[gs]);
+            // record of block j + RS - 1 into the stage of block j - 1 once that block is done
+            const int jn = j + RS - 1;
+            if (jn < ncta_blocks) {
+                if (j >= 1) mbar_wait(&rdone[(j - 1) % RS], (uint32_t)(((j - 1) / RS) & 1));
+                if (lane == 0) issue_rec(jn);
+            }
         }
-        asm volatile("cp.async.commit_group;" ::: "memory");
-    };
-    // prologue: records of the first two blocks in flight
-    if (tid == 0 && (int)blockIdx.x < prm.nblocks) issue(blockIdx.x, 0);
-    if (tid == 0 && (int)(blockIdx.x + gridDim.x) < prm.nblocks) issue(blockIdx.x + gridDim.x, 1);
-    if (pf && (int)blockIdx.x < prm.nblocks) {
-        mbar_wait(&bars[0], 0);
-        gather(prm.blocks[blockIdx.x], sRec0, 0);
+        asm volatile("cp.async.wait_all;" ::: "memory");
+        return;
     }
 
-    int j = 0;
-    for (int bi = blockIdx.x; bi < prm.nblocks; bi += gridDim.x, ++j) {
-        const int buf = j & 1;
-        const FeaBlock blk = prm.blocks[bi];
-        const uint8_t* rec = buf ? sRec1 : sRec0;
-        const int nE = blk.nE;
-        const int g = pf ? buf : 0;
-        if (!pf) {
-            mbar_wait(&bars[buf], (uint32_t)((j >> 1) & 1));
-            gather(blk, rec, 0);
-        }
-        const double* gU = gUb[g];
-        const double2* gX = gXb[g];
-        asm volatile("cp.async.wait_group 0;" ::: "memory");  // this block's gathers landed
-        __syncthreads();
-
-        // ---------------- Phase A: element values V[t][le] in shared memory
-        if constexpr (!STAGED && NQ_T > 0) {
-            for (int le = tid; le < nE; le += nthr)
-                element_const<NP, NQ_T, DO_M, DO_C>(prm, gU, gX, e_max, le, two_lam, sVm, sVc);
-        } else if constexpr (!STAGED) {
-            for (int le0 = tid; le0 < nE; le0 += 2 * nthr) {
-                const int le1 = le0 + nthr;
-                const bool has1 = le1 < nE;
-                const int lx = has1 ? le1 : le0;
-                double d0, d1, W0[3], W1[3];
-                geometry(gX, e_max, le0, d0, W0[0], W0[1], W0[2]);
-                geometry(gX, e_max, lx, d1, W1[0], W1[1], W1[2]);
-                double lm0[NQM], lc0[NQM], lm1[NQM], lc1[NQM];
-                form_lambda<NP, NQM>(sPhi, sW, nq, gU, e_max, le0, d0, DO_M ? prm.coef_m : prm.coef_c, lm0);
-                form_lambda<NP, NQM>(sPhi, sW, nq, gU, e_max, lx, d1, DO_M ? prm.coef_m : prm.coef_c, lm1);
-                if (two_lam) {
-                    form_lambda<NP, NQM>(sPhi, sW, nq, gU, e_max, le0, d0, prm.coef_c, lc0);
-                    form_lambda<NP, NQM>(sPhi, sW, nq, gU, e_max, lx, d1, prm.coef_c, lc1);
-                } else {
+    // ------------------------------------------------------------------ consumers
+    // This warp's row tile of Q_f as DMMA A-fragments, for the whole kernel (registers).
+    const int tt = warp % NTT, sub = warp / NTT;
+    const int g = lane >> 2, cq = lane & 3;
+    double afr[4][NK];
 #pragma unroll
-                    for (int q = 0; q < NQM; ++q) {
-                        lc0[q] = lm0[q];
-                        lc1[q] = lm1[q];
+    for (int f = 0; f < 4; ++f)
+#pragma unroll
+        for (int kk = 0; kk < NK; ++kk)
+            afr[f][kk] = (f == 0 ? DO_M : DO_C) ? __ldg(prm.qfrag + ((f * NTT + tt) * NK + kk) * 32 + lane) : 0.0;
+    constexpr bool INTERP_MMA = fea_interp_mma(P);
+    constexpr int MTN = INTERP_MMA ? (NQP + 7) / 8 : 1, KTN = INTERP_MMA ? fea_kt(P) : 1;
+    double pfr[MTN][KTN];  // Phi^T A-fragments (p >= 2)
+#pragma unroll
+    for (int mt = 0; mt < MTN; ++mt)
+#pragma unroll
+        for (int kt = 0; kt < KTN; ++kt)
+            pfr[mt][kt] = INTERP_MMA ? __ldg(prm.qfrag + 4 * NTT * NK * 32 + (mt * KTN + kt) * 32 + lane) : 0.0;
+    const double* cPhi = prm.ctab;
+    const double* cW = prm.ctab + ((NP * nq + 1) & ~1);
+
+    unsigned long long tacc[6] = {0, 0, 0, 0, 0, 0};
+    unsigned long long tcl = 0;
+    auto tick = [&](int slot) {  // optional phase timing (consumer thread 0)
+        if (prm.dbg && tid == 0) {
+            const unsigned long long now = clock64();
+            if (slot >= 0) tacc[slot] += now - tcl;
+            tcl = now;
+        }
+    };
+    tick(-1);
+    for (int j = 0; j < ncta_blocks; ++j) {
+        const FeaBlock blk = prm.blocks[blockIdx.x + j * gridDim.x];
+        const int rs = j % RS, gs = j & 1;
+        const uint8_t* rec = sRec(rs);
+        const int nE = blk.nE;
+        const int net = (nE + 7) >> 3;
+        const double* gU = gUb(gs);
+        const double2* gX = gXb(gs);
+        mbar_wait(&full_rec[rs], (uint32_t)((j / RS) & 1));
+        mbar_wait(&full_gat[gs], (uint32_t)((j >> 1) & 1));
+        tick(0);
+
+        // ---------------- A1: geometry (W_e, b_e), u_q = Phi^T u_e, k(u_q), Lambda
+        if constexpr (!INTERP_MMA) {
+            for (int le = tid; le < net * 8; le += NCT) {
+                if (le < nE) {
+                    double absdet, A00, A11, A01;
+                    geometry(gX, e_max, le, absdet, A00, A11, A01);
+                    sW[le] = A00;
+                    sW[e_max + le] = A11;
+                    sW[2 * e_max + le] = A01;
+                    double ue[NP];
+#pragma unroll
+                    for (int i = 0; i < NP; ++i) ue[i] = gU[i * e_max + le];
+#pragma unroll
+                    for (int q = 0; q < NQP; ++q) {
+                        double lm = 0.0, lc = 0.0;
+                        if (q < nq) {
+                            double uq = 0.0;
+#pragma unroll
+                            for (int i = 0; i < NP; ++i) uq = fma(cPhi[i * nq + q], ue[i], uq);
+                            const double wb = cW[q] * absdet;
+                            lm = wb * keval(DO_M ? prm.coef_m : prm.coef_c, uq);
+                            lc = two_lam ? wb * keval(prm.coef_c, uq) : lm;
+                        }
+                        sLm[q * e_max + le] = lm;
+                        if (two_lam) sLc[q * e_max + le] = lc;
+                    }
+                } else {  // padding columns of the last element tile
+#pragma unroll
+                    for (int q = 0; q < NQP; ++q) {
+                        sLm[q * e_max + le] = 0.0;
+                        if (two_lam) sLc[q * e_max + le] = 0.0;
+                    }
+                    sW[le] = sW[e_max + le] = sW[2 * e_max + le] = 0.0;
+                }
+            }
+            consumer_sync(NCT);
+        } else {
+            // A1a: geometry per element
+            for (int le = tid; le < net * 8; le += NCT) {
+                double absdet = 0.0, A00 = 0.0, A11 = 0.0, A01 = 0.0;
+                if (le < nE) geometry(gX, e_max, le, absdet, A00, A11, A01);
+                sW[le] = A00;
+                sW[e_max + le] = A11;
+                sW[2 * e_max + le] = A01;
+                sW[3 * e_max + le] = absdet;
+            }
+            consumer_sync(NCT);
+            // A1b: U = Phi^T U_e on DMMA; epilogue Lambda_qe = w_q b_e k(u_qe)
+            constexpr int MT = MTN, KT = KTN;
+            for (int un = warp; un < MT * net; un += NTT * S) {
+                const int mt = un % MT, et = un / MT;
+                double u0 = 0.0, u1 = 0.0;
+#pragma unroll
+                for (int kt = 0; kt < KT; ++kt) {
+                    const int i = kt * 4 + cq;
+                    const double b = i < NP ? gU[i * e_max + et * 8 + g] : 0.0;
+                    double a = pfr[0][kt];  // select the m-tile without dynamic register indexing
+#pragma unroll
+                    for (int m2 = 1; m2 < MT; ++m2) a = mt == m2 ? pfr[m2][kt] : a;
+                    dmma(u0, u1, a, b);
+                }
+                const int q = mt * 8 + g, le0 = et * 8 + 2 * cq;
+                if (q < NQP) {
+                    double lm0 = 0.0, lm1 = 0.0, lc0 = 0.0, lc1 = 0.0;
+                    if (q < nq) {
+                        const double w = cW[q];
+                        const double d0 = le0 < nE ? sW[3 * e_max + le0] : 0.0;
+                        const double d1 = le0 + 1 < nE ? sW[3 * e_max + le0 + 1] : 0.0;
+                        const FeaCoef& cf = DO_M ? prm.coef_m : prm.coef_c;
+                        if (le0 < nE) lm0 = w * d0 * keval(cf, u0);
+                        if (le0 + 1 < nE) lm1 = w * d1 * keval(cf, u1);
+                        if (two_lam) {
+                            if (le0 < nE) lc0 = w * d0 * keval(prm.coef_c, u0);
+                            if (le0 + 1 < nE) lc1 = w * d1 * keval(prm.coef_c, u1);
+                        }
+                    }
+                    *reinterpret_cast<double2*>(sLm + q * e_max + le0) = make_double2(lm0, lm1);
+                    if (two_lam) *reinterpret_cast<double2*>(sLc + q * e_max + le0) = make_double2(lc0, lc1);
+                }
+            }
+            consumer_sync(NCT);
+        }
+        // gather stage consumed: the producer may refill it
+        if (tid == 0) mbar_arrive(&gdone[gs]);
+        tick(1);
+
+        // ---------------- A2: V = Q Lambda on the FP64 tensor cores (DMMA m8n8k4)
+        {
+            const double* Lc = two_lam ? sLc : sLm;
+            const int t = tt * 8 + g;
+            for (int et = sub; et < net; et += S) {
+                const int col = et * 8 + g;       // B fragment column (element) of this lane
+                const int le0 = et * 8 + 2 * cq;  // the two accumulator columns of this lane
+                double bm[NK], bc[NK];
+#pragma unroll
+                for (int kk = 0; kk < NK; ++kk) {
+                    bm[kk] = sLm[(kk * 4 + cq) * e_max + col];
+                    bc[kk] = Lc[(kk * 4 + cq) * e_max + col];
+                }
+                double m0 = 0.0, m1 = 0.0, a0 = 0.0, a1 = 0.0, b0 = 0.0, b1 = 0.0, c0 = 0.0, c1 = 0.0;
+#pragma unroll
+                for (int kk = 0; kk < NK; ++kk) {
+                    if (DO_M) dmma(m0, m1, afr[0][kk], bm[kk]);
+                    if (DO_C) {
+                        dmma(a0, a1, afr[1][kk], bc[kk]);
+                        dmma(b0, b1, afr[2][kk], bc[kk]);
+                        dmma(c0, c1, afr[3][kk], bc[kk]);
                     }
                 }
-                contract2<NQM, DO_M, DO_C>(sQ, nq, 0, T, lm0, lc0, lm1, lc1, W0, W1, sVm, sVc, e_max, le0, le1, has1);
-            }
-        } else {
-            // A1: Lambda (one or two) and W per element into shared memory
-            const int nlam = two_lam ? 2 : 1;
-            for (int le = tid; le < nE; le += nthr) {
-                double d, W[3], lam[NQM];
-                geometry(gX, e_max, le, d, W[0], W[1], W[2]);
-                form_lambda<NP, NQM>(sPhi, sW, nq, gU, e_max, le, d, DO_M ? prm.coef_m : prm.coef_c, lam);
-#pragma unroll
-                for (int q = 0; q < NQM; ++q)
-                    if (q < nq) sLam[q * e_max + le] = lam[q];
-                if (two_lam) {
-                    form_lambda<NP, NQM>(sPhi, sW, nq, gU, e_max, le, d, prm.coef_c, lam);
-#pragma unroll
-                    for (int q = 0; q < NQM; ++q)
-                        if (q < nq) sLam[(nq + q) * e_max + le] = lam[q];
+                if (t < T) {
+                    if (DO_M) *reinterpret_cast<double2*>(sVm + t * e_max + le0) = make_double2(m0, m1);
+                    if (DO_C) {
+                        const double2 w0 = *reinterpret_cast<const double2*>(sW + le0);
+                        const double2 w1 = *reinterpret_cast<const double2*>(sW + e_max + le0);
+                        const double2 w2 = *reinterpret_cast<const double2*>(sW + 2 * e_max + le0);
+                        *reinterpret_cast<double2*>(sVc + t * e_max + le0) =
+                            make_double2(fma(w0.x, a0, fma(w1.x, b0, w2.x * c0)), fma(w0.y, a1, fma(w1.y, b1, w2.y * c1)));
+                    }
                 }
-                sLam[(nlam * nq + 0) * e_max + le] = W[0];
-                sLam[(nlam * nq + 1) * e_max + le] = W[1];
-                sLam[(nlam * nq + 2) * e_max + le] = W[2];
-            }
-            __syncthreads();
-            // A2: items (t-chunk, element pair); a warp shares one t-chunk
-            const int npair = (nE + 1) >> 1;
-            const int np32 = (npair + 31) & ~31;
-            const int ntc = prm.ntc;
-            const int tper = (T + ntc - 1) / ntc;
-            for (int it = tid; it < ntc * np32; it += nthr) {
-                const int tc = it / np32, pr = it - tc * np32;
-                if (pr >= npair) continue;
-                const int le0 = pr, le1 = pr + npair;  // second half of the block
-                const bool has1 = le1 < nE;
-                const int lx = has1 ? le1 : le0;
-                double lm0[NQM], lc0[NQM], lm1[NQM], lc1[NQM], W0[3], W1[3];
-#pragma unroll
-                for (int q = 0; q < NQM; ++q) {
-                    lm0[q] = q < nq ? sLam[q * e_max + le0] : 0.0;
-                    lm1[q] = q < nq ? sLam[q * e_max + lx] : 0.0;
-                    lc0[q] = two_lam ? (q < nq ? sLam[(nq + q) * e_max + le0] : 0.0) : lm0[q];
-                    lc1[q] = two_lam ? (q < nq ? sLam[(nq + q) * e_max + lx] : 0.0) : lm1[q];
-                }
-#pragma unroll
-                for (int f = 0; f < 3; ++f) {
-                    W0[f] = sLam[(nlam * nq + f) * e_max + le0];
-                    W1[f] = sLam[(nlam * nq + f) * e_max + lx];
-                }
-                const int t0 = tc * tper, t1 = min(T, t0 + tper);
-                contract2<NQM, DO_M, DO_C>(sQ, nq, t0, t1, lm0, lc0, lm1, lc1, W0, W1, sVm, sVc, e_max, le0, le1, has1);
             }
         }
-        // with prefetch, the next block's gathers fly during phase B
-        const int bn = bi + gridDim.x;
-        if (pf && bn < prm.nblocks) {
-            mbar_wait(&bars[buf ^ 1], (uint32_t)(((j + 1) >> 1) & 1));
-            gather(prm.blocks[bn], buf ? sRec0 : sRec1, buf ^ 1);
-        }
-        __syncthreads();
+        tick(2);
+        consumer_sync(NCT);
+        tick(5);
 
         // ---------------- Phase B: fixed-order segmented reduction into the CSR slots.
-        // Items (slots) come grouped by contributor count c, so every lane of a warp runs the
-        // same trip count and the contributor base is arithmetic (no scan).
         const int32_t* cls = reinterpret_cast<const int32_t*>(rec);
         const uint16_t* items = reinterpret_cast<const uint16_t*>(rec + fea_rec_off_items(blk));
         const uint16_t* con = reinterpret_cast<const uint16_t*>(rec + fea_rec_off_contrib(blk));
@@ -452,80 +460,68 @@ __global__ void __launch_bounds__(256, STAGED ? 1 : 2) k_reassemble(const __grid
             const int c = cls[3 * k], i0 = cls[3 * k + 1], cb = cls[3 * k + 2];
             const int i1 = k + 1 < blk.ncls ? cls[3 * k + 4] : blk.nslots;
             switch (c) {
-                case 1: class_items<1, DO_M, DO_C>(i0, i1, cb, items, con, sVm, sVc, om, oc, tid, nthr); break;
-                case 2: class_items<2, DO_M, DO_C>(i0, i1, cb, items, con, sVm, sVc, om, oc, tid, nthr); break;
-                case 3: class_items<3, DO_M, DO_C>(i0, i1, cb, items, con, sVm, sVc, om, oc, tid, nthr); break;
-                case 4: class_items<4, DO_M, DO_C>(i0, i1, cb, items, con, sVm, sVc, om, oc, tid, nthr); break;
-                case 6: class_items<6, DO_M, DO_C>(i0, i1, cb, items, con, sVm, sVc, om, oc, tid, nthr); break;
-                default: class_items_generic<DO_M, DO_C>(c, i0, i1, cb, items, con, sVm, sVc, om, oc, tid, nthr);
+                case 1: class_items<1, DO_M, DO_C>(i0, i1, cb, items, con, sVm, sVc, om, oc, tid, NCT); break;
+                case 2: class_items<2, DO_M, DO_C>(i0, i1, cb, items, con, sVm, sVc, om, oc, tid, NCT); break;
+                case 3: class_items<3, DO_M, DO_C>(i0, i1, cb, items, con, sVm, sVc, om, oc, tid, NCT); break;
+                case 4: class_items<4, DO_M, DO_C>(i0, i1, cb, items, con, sVm, sVc, om, oc, tid, NCT); break;
+                case 6: class_items<6, DO_M, DO_C>(i0, i1, cb, items, con, sVm, sVc, om, oc, tid, NCT); break;
+                default: class_items_generic<DO_M, DO_C>(c, i0, i1, cb, items, con, sVm, sVc, om, oc, tid, NCT);
             }
         }
-        __syncthreads();
-        // this block's record buffer is free: request the record two blocks ahead
-        if (tid == 0 && bi + 2 * (int)gridDim.x < prm.nblocks) issue(bi + 2 * gridDim.x, buf);
+        tick(3);
+        consumer_sync(NCT);  // V and the record stage are free
+        tick(5);
+        if (tid == 0) mbar_arrive(&rdone[rs]);
     }
+    if (prm.dbg && tid == 0)
+        for (int i = 0; i < 6; ++i) atomicAdd(prm.dbg + i, tacc[i]);
 }
 
-template <int P, int NQ_T>
 using kfun_t = void (*)(const FeaKParams);
 
 template <int P, int NQ_T>
-kfun_t<P, NQ_T> pick(int dm, int dc) {
-    constexpr bool S = P >= 3;  // Lambda staged in shared memory, rows split over threads
-    if (dm && dc) return k_reassemble<P, NQ_T, true, true, S>;
-    if (dm) return k_reassemble<P, NQ_T, true, false, S>;
-    return k_reassemble<P, NQ_T, false, true, S>;
+kfun_t pick(int dm, int dc) {
+    if (dm && dc) return k_reassemble<P, NQ_T, true, true>;
+    if (dm) return k_reassemble<P, NQ_T, true, false>;
+    return k_reassemble<P, NQ_T, false, true>;
 }
 
-template <int P, int NQ_T>
-cudaError_t launch_p(const FeaKParams& prm, int threads, int smem, int grid, cudaStream_t st) {
-    auto kern = pick<P, NQ_T>(prm.out_m != nullptr, prm.out_c != nullptr);
-    cudaError_t err = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
-    if (err != cudaSuccess) return err;
-    kern<<<grid, threads, smem, st>>>(prm);
-    return cudaGetLastError();
+kfun_t select(int order, int nq, int dm, int dc) {
+    const bool nat = nq == fea_nq_native(order);
+    switch (order) {
+        case 1: return nat ? pick<1, 3>(dm, dc) : pick<1, 0>(dm, dc);
+        case 2: return nat ? pick<2, 6>(dm, dc) : pick<2, 0>(dm, dc);
+        case 3: return nat ? pick<3, 12>(dm, dc) : pick<3, 0>(dm, dc);
+        case 4: return nat ? pick<4, 16>(dm, dc) : pick<4, 0>(dm, dc);
+        default: return nullptr;
+    }
 }
 
-template <int P, int NQ_T>
-cudaError_t occ_p(int dm, int dc, int threads, int smem, int* n) {
-    auto kern = pick<P, NQ_T>(dm, dc);
-    cudaError_t err = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
-    if (err != cudaSuccess) return err;
-    return cudaOccupancyMaxActiveBlocksPerMultiprocessor(n, kern, threads, smem);
+int threads_of(int order) {
+    switch (order) {
+        case 1: return fea_threads(1);
+        case 2: return fea_threads(2);
+        case 3: return fea_threads(3);
+        default: return fea_threads(4);
+    }
 }
 
 }  // namespace
 
-// Rule sizes with a specialised kernel: the minimal Dunavant rules of the configs
-// (3, 6, 12, 16 points for p = 1..4); any other n_q <= 16 runs the generic variant.
-static int nq_native(int order) { return order == 1 ? 3 : order == 2 ? 6 : order == 3 ? 12 : 16; }
-
-int fea_launch_reassemble(const FeaKParams& prm, int order, int threads, int smem_bytes, int grid, int staged,
-                          void* stream) {
-    cudaStream_t st = (cudaStream_t)stream;
-    if (staged != (order >= 3 ? 1 : 0)) return (int)cudaErrorInvalidValue;
-    const bool nat = prm.nq == nq_native(order);
-    cudaError_t e;
-    switch (order) {
-        case 1: e = nat ? launch_p<1, 3>(prm, threads, smem_bytes, grid, st) : launch_p<1, 0>(prm, threads, smem_bytes, grid, st); break;
-        case 2: e = nat ? launch_p<2, 6>(prm, threads, smem_bytes, grid, st) : launch_p<2, 0>(prm, threads, smem_bytes, grid, st); break;
-        case 3: e = nat ? launch_p<3, 12>(prm, threads, smem_bytes, grid, st) : launch_p<3, 0>(prm, threads, smem_bytes, grid, st); break;
-        case 4: e = nat ? launch_p<4, 16>(prm, threads, smem_bytes, grid, st) : launch_p<4, 0>(prm, threads, smem_bytes, grid, st); break;
-        default: e = cudaErrorInvalidValue;
-    }
-    return (int)e;
+int fea_launch_reassemble(const FeaKParams& prm, int order, int smem_bytes, int grid, void* stream) {
+    kfun_t kern = select(order, prm.nq, prm.out_m != nullptr, prm.out_c != nullptr);
+    if (!kern) return (int)cudaErrorInvalidValue;
+    cudaError_t err = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, smem_bytes);
+    if (err != cudaSuccess) return (int)err;
+    kern<<<grid, threads_of(order), smem_bytes, (cudaStream_t)stream>>>(prm);
+    return (int)cudaGetLastError();
 }
 
-int fea_kernel_occupancy(int order, int nq, int dm, int dc, int staged, int threads, int smem, int* n) {
-    if (staged != (order >= 3 ? 1 : 0)) return (int)cudaErrorInvalidValue;
-    const bool nat = nq == nq_native(order);
-    cudaError_t e;
-    switch (order) {
-        case 1: e = nat ? occ_p<1, 3>(dm, dc, threads, smem, n) : occ_p<1, 0>(dm, dc, threads, smem, n); break;
-        case 2: e = nat ? occ_p<2, 6>(dm, dc, threads, smem, n) : occ_p<2, 0>(dm, dc, threads, smem, n); break;
-        case 3: e = nat ? occ_p<3, 12>(dm, dc, threads, smem, n) : occ_p<3, 0>(dm, dc, threads, smem, n); break;
-        case 4: e = nat ? occ_p<4, 16>(dm, dc, threads, smem, n) : occ_p<4, 0>(dm, dc, threads, smem, n); break;
-        default: e = cudaErrorInvalidValue;
-    }
-    return (int)e;
+int fea_kernel_occupancy(int order, int nq, int dm, int dc, int smem_bytes, int* n, int* threads) {
+    kfun_t kern = select(order, nq, dm, dc);
+    if (!kern) return (int)cudaErrorInvalidValue;
+    *threads = threads_of(order);
+    cudaError_t err = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, smem_bytes);
+    if (err != cudaSuccess) return (int)err;
+    return (int)cudaOccupancyMaxActiveBlocksPerMultiprocessor(n, kern, *threads, smem_bytes);
 }

@@ -86,13 +86,11 @@ def test_deterministic_across_runs_and_tilings(p):
     base = library_assemble(m, xy, w, u, p, coef, coef)
     again = library_assemble(m, xy, w, u, p, coef, coef)
     assert np.array_equal(base["M"], again["M"]) and np.array_equal(base["K"], again["K"])
-    budgets = {1: [8192, 16384], 2: [16384, 40000], 3: [40000, 100000], 4: [100000, 130000]}[p]
+    budgets = {1: [24000, 40000], 2: [40000, 70000], 3: [100000, 150000], 4: [150000, 190000]}[p]
     for b in budgets:
         r = library_assemble(m, xy, w, u, p, coef, coef, tuning={1: b})
         assert r["ctx"].stat(1) > max(1, base["ctx"].stat(1) // 2)  # a different, finer tiling
         assert np.array_equal(base["M"], r["M"]) and np.array_equal(base["K"], r["K"])
-    r = library_assemble(m, xy, w, u, p, coef, coef, tuning={2: 128})
-    assert np.array_equal(base["M"], r["M"]) and np.array_equal(base["K"], r["K"])
 
 
 @pytest.mark.parametrize("p,world", [(1, 2), (2, 3), (3, 4), (4, 2)])
