@@ -224,7 +224,11 @@ def run_ours(args):
     for u in wl.u_sequence(R):
         ul = asm.to_library(u)
         us.append(torch.tensor(asm.owned_slice(ul) if world > 1 else ul, dtype=torch.float64, device=dev))
-    flush = torch.empty(256 * 1024 * 1024 // 4, dtype=torch.float32, device=dev)
+    flush_mb = int(os.environ.get("FEA_FLUSH_MB", "256"))  # diagnostics only; the bench default flushes
+    flush = torch.empty(max(1, flush_mb * 1024 * 1024 // 4), dtype=torch.float32, device=dev)
+    # diagnostics: FEA_FLUSH_CLEAN=1 follows the write with a read of another buffer larger than
+    # L2, so the kernel starts with a cold but CLEAN L2 (no dirty write-back of the flush data)
+    clean = torch.empty_like(flush) if os.environ.get("FEA_FLUSH_CLEAN") else None
     stream = torch.cuda.current_stream(dev)
 
     def barrier():
@@ -240,7 +244,10 @@ def run_ours(args):
     torch.cuda.synchronize()
     with sampler:
         for i in range(args.steps):
-            flush.fill_(float(i))  # evict L2 (126 MB) before every timed step, outside the events
+            if flush_mb:
+                flush.fill_(float(i))  # evict L2 (126 MB) before every timed step, outside the events
+                if clean is not None:
+                    clean.sum()
             ev[i][0].record(stream)
             asm.reassemble(us[i % R])
             ev[i][1].record(stream)
@@ -300,15 +307,19 @@ def run_ours(args):
                                            lib_to_user=asm.lib_to_user)
             cpu = {"value": rate, "unit": UNIT, "cores": cores, "kind": "oracle", "sample": desc}
         desc = workload_desc(cfg, wl)
-        desc.update({"l2": "flushed (256 MiB write) before every timed step", "parallelism": f"rows{world}",
+        desc.update({"l2": f"flushed ({flush_mb} MiB write) before every timed step" if flush_mb >= 256 else
+                     f"NOT flushed ({flush_mb} MiB write): diagnostic run, not a bench value", "parallelism": f"rows{world}",
                      "nnz": int(nnz_local) if world == 1 else None, "setup_s": round(t_setup, 3),
                      "blocks": asm.ctx.stat(1), "elem_visits_over_owned": round(asm.ctx.stat(2) / max(1, asm.ctx.stat(3)), 4),
                      "smem_per_cta": asm.ctx.stat(6), "grid": asm.ctx.stat(8), "tuning": tuning})
         if os.environ.get("FEA_DEBUG_TIMING"):
-            ph = [asm.ctx.stat(20 + i) for i in range(6)]
+            if asm.ctx.stat(11) == 5:  # per-warp timeline of k_reassemble5 (lane 0 of every warp)
+                names = ["compute", "move_refill", "full_wait", "rec_wait", "phaseB", "free_wait", "prologue"]
+            else:
+                names = ["rec_wait", "gather", "phaseA", "phaseB", "issue", "barriers"]
+            ph = [asm.ctx.stat(20 + i) for i in range(len(names))]
             tot = sum(ph) or 1
-            desc["phase_cycles_pct"] = dict(zip(["rec_wait", "gather", "phaseA", "phaseB", "issue", "barriers"],
-                                                [round(100.0 * x / tot, 1) for x in ph]))
+            desc["phase_cycles_pct"] = dict(zip(names, [round(100.0 * x / tot, 1) for x in ph]))
         line = {
             "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
             "warmup": args.warmup, "ms_per_step": ms_per_step, "higher_is_better": True,
@@ -316,7 +327,8 @@ def run_ours(args):
             "config": desc,
             "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
                          "frac": achieved / peak, "traffic": traffic, "algorithmic_bytes": B,
-                         "kernel": "k_reassemble", "peak_source": peak_src,
+                         "kernel": "k_reassemble5" if asm.ctx.stat(11) == 5 else "k_reassemble",
+                         "peak_source": peak_src,
                          "kernel_ms_median": kern_ms},
             "cpu_baseline": cpu,
             "e2e": {"value": entries_step / e2e_s, "unit": UNIT, "h2d_bytes_per_step": 8 * nu,

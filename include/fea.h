@@ -65,6 +65,9 @@ enum {
     FEA_TUNE_SMEM_BUDGET = 1,   /* bytes of shared memory per CTA (0 = default: 113 KiB for p <= 2,
                                    two CTAs per SM; 226 KiB for p >= 3).  Smaller budgets give
                                    smaller row blocks (more, finer CTA tiles)                        */
+    FEA_TUNE_KERNEL = 2,        /* kernel generation: 0 = automatic (v5 for p <= 2 with the native
+                                   3/6-point rules, v4 otherwise), 4 = force v4                      */
+    FEA_TUNE_EMAX = 3,          /* v5: cap on elements per row block (0 = from the smem budget)      */
     FEA_TUNE_PLAN_WHICH = 4     /* FEA_MASS | FEA_STIFF: matrices the plan's shared memory is sized
                                    for (default both); assembling more than planned runs one pass
                                    per matrix                                                        */

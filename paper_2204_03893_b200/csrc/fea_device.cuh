@@ -1,0 +1,345 @@
+// fea_device.cuh -- device helpers shared by the sm_100a reassembly kernels (fea_kernels.cu: v4,
+// p >= 3 and generic rules; fea_kernels5.cu: v5, p <= 2): PTX wrappers (mbarrier, TMA bulk copy,
+// cp.async, DMMA), the coefficient k(u), element geometry, and phase B (fixed-order segmented
+// sums of the contributor stream into the CSR slots).
+#pragma once
+#include <cuda_runtime.h>
+#include <cstdint>
+
+#include "fea_internal.h"
+
+namespace fea_dev {
+
+// ------------------------------------------------------------------ PTX helpers
+__device__ __forceinline__ uint32_t smem_u32(const void* p) { return (uint32_t)__cvta_generic_to_shared(p); }
+
+__device__ __forceinline__ void mbar_init(uint64_t* bar, uint32_t count) {
+    asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_u32(bar)), "r"(count) : "memory");
+}
+__device__ __forceinline__ void fence_mbar_init() { asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory"); }
+__device__ __forceinline__ void fence_proxy_async() { asm volatile("fence.proxy.async.shared::cta;" ::: "memory"); }
+__device__ __forceinline__ void mbar_expect_tx(uint64_t* bar, uint32_t bytes) {
+    asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(bar)), "r"(bytes) : "memory");
+}
+__device__ __forceinline__ void mbar_arrive(uint64_t* bar) {
+    asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(smem_u32(bar)) : "memory");
+}
+__device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity) {
+    asm volatile(
+        "{\n\t.reg .pred p;\n"
+        "WAIT_%=:\n\t"
+        "mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n\t"
+        "@!p bra WAIT_%=;\n}" ::"r"(smem_u32(bar)),
+        "r"(parity)
+        : "memory");
+}
+// 1D TMA bulk copy global -> shared, completion counted on an mbarrier
+__device__ __forceinline__ void tma_load_1d(void* dst, const void* src, uint32_t bytes, uint64_t* bar) {
+    asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
+                     smem_u32(dst)),
+                 "l"(src), "r"(bytes), "r"(smem_u32(bar))
+                 : "memory");
+}
+__device__ __forceinline__ void cp_async8(void* dst, const void* src) {
+    asm volatile("cp.async.ca.shared.global [%0], [%1], 8;" ::"r"(smem_u32(dst)), "l"(src) : "memory");
+}
+__device__ __forceinline__ void cp_async16(void* dst, const void* src) {
+    asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(smem_u32(dst)), "l"(src) : "memory");
+}
+// arrive on `bar` once all prior cp.async of this thread have completed
+__device__ __forceinline__ void cp_async_mbar_arrive(uint64_t* bar) {
+    asm volatile("cp.async.mbarrier.arrive.noinc.shared::cta.b64 [%0];" ::"r"(smem_u32(bar)) : "memory");
+}
+__device__ __forceinline__ void consumer_sync(int nct) {  // named barrier 1: consumer warps only
+    asm volatile("bar.sync 1, %0;" ::"r"(nct) : "memory");
+}
+// D = A (8x4, row) * B (4x8, col) + D on the FP64 tensor core; fragment ownership per lane
+// (g = lane / 4, c = lane % 4): a = A[g][c], b = B[c][g], d = D[g][2c .. 2c+1].
+__device__ __forceinline__ void dmma(double& d0, double& d1, double a, double b) {
+    asm volatile("mma.sync.aligned.m8n8k4.row.col.f64.f64.f64.f64 {%0,%1}, {%2}, {%3}, {%0,%1};"
+                 : "+d"(d0), "+d"(d1)
+                 : "d"(a), "d"(b));
+}
+
+// ------------------------------------------------------------------ math
+template <int N>
+__device__ __forceinline__ double horner(const double* par, double u) {  // sum_{i<N} par[i] u^i
+    double r = par[N - 1];
+#pragma unroll
+    for (int i = N - 2; i >= 0; --i) r = fma(r, u, par[i]);
+    return r;
+}
+
+// k(u); the branch is warp-uniform (one coefficient per launch), each case straight-line.
+__device__ __forceinline__ double keval(const FeaCoef& c, double u) {
+    if (c.kind == 0) {
+        switch (c.npar) {
+            case 1: return c.par[0];
+            case 2: return horner<2>(c.par, u);
+            case 3: return horner<3>(c.par, u);
+            case 4: return horner<4>(c.par, u);
+            case 5: return horner<5>(c.par, u);
+            case 6: return horner<6>(c.par, u);
+            case 7: return horner<7>(c.par, u);
+            case 8: return horner<8>(c.par, u);
+            default: return horner<9>(c.par, u);
+        }
+    }
+    if (c.kind == 1) return c.par[0] * exp(c.par[1] * u);
+    // piecewise linear, segment s covers (T_s, T_{s+1}]
+    const int m = c.npar / 2;
+    int s = 0;
+    while (s < m - 2 && u > c.par[2 * (s + 1)]) ++s;
+    const double T0 = c.par[2 * s], k0 = c.par[2 * s + 1], T1 = c.par[2 * s + 2], k1 = c.par[2 * s + 3];
+    return k0 + (k1 - k0) / (T1 - T0) * (u - T0);
+}
+
+// exp and the piecewise-linear k out of line (one copy of the code each)
+static __device__ __noinline__ double k_exp(double c0, double c1, double u) { return c0 * exp(c1 * u); }
+static __device__ __noinline__ double k_pwl(const FeaCoef& c, double u) {
+    const int m = c.npar / 2;
+    int s = 0;
+    while (s < m - 2 && u > c.par[2 * (s + 1)]) ++s;
+    const double T0 = c.par[2 * s], k0 = c.par[2 * s + 1], T1 = c.par[2 * s + 2], k1 = c.par[2 * s + 3];
+    return k0 + (k1 - k0) / (T1 - T0) * (u - T0);
+}
+
+// k(u_q) for all N quadrature points at once: one Horner loop over the coefficients with the N
+// points as independent FMA chains (compact code, the same per-point arithmetic as keval).
+template <int N>
+__device__ __forceinline__ void keval_all(const FeaCoef& c, const double (&u)[N], double (&k)[N]) {
+    if (c.kind == 0) {
+        const int n = c.npar;
+        const double top = c.par[n - 1];
+#pragma unroll
+        for (int q = 0; q < N; ++q) k[q] = top;
+#pragma unroll 1
+        for (int i = n - 2; i >= 0; --i) {
+            const double a = c.par[i];
+#pragma unroll
+            for (int q = 0; q < N; ++q) k[q] = fma(k[q], u[q], a);
+        }
+    } else if (c.kind == 1) {
+#pragma unroll
+        for (int q = 0; q < N; ++q) k[q] = k_exp(c.par[0], c.par[1], u[q]);
+    } else {
+#pragma unroll
+        for (int q = 0; q < N; ++q) k[q] = k_pwl(c, u[q]);
+    }
+}
+
+// Element geometry from the staged vertex coordinates: b_e = |det B_e|, A_e = (B^T B)^{-1}
+__device__ __forceinline__ void geometry(const double2* __restrict__ gX, int e_max, int le, double& absdet,
+                                         double& A00, double& A11, double& A01) {
+    const double2 a = gX[le], b = gX[e_max + le], c = gX[2 * e_max + le];
+    const double B00 = b.x - a.x, B10 = b.y - a.y, B01 = c.x - a.x, B11 = c.y - a.y;
+    const double det = B00 * B11 - B01 * B10;
+    absdet = fabs(det);
+    const double inv = 1.0 / (det * det);  // det(B^T B) = det(B)^2
+    A00 = (B01 * B01 + B11 * B11) * inv;
+    A11 = (B00 * B00 + B10 * B10) * inv;
+    A01 = -(B00 * B01 + B10 * B11) * inv;
+}
+
+// ------------------------------------------------------------------ phase B helpers
+// Sum of the C contributors of one slot in the fixed (stored) order, all loads issued first.
+template <int C, bool DO_M, bool DO_C>
+__device__ __forceinline__ void slot_sum(const uint16_t* __restrict__ cp, const double* __restrict__ sVm,
+                                         const double* __restrict__ sVc, double& am, double& ac) {
+    int off[C];
+#pragma unroll
+    for (int q = 0; q < C; ++q) off[q] = cp[q];
+    double vm[C], vc[C];
+#pragma unroll
+    for (int q = 0; q < C; ++q) {
+        if (DO_M) vm[q] = sVm[off[q]];
+        if (DO_C) vc[q] = sVc[off[q]];
+    }
+    am = 0.0;
+    ac = 0.0;
+#pragma unroll
+    for (int q = 0; q < C; ++q) {
+        if (DO_M) am += vm[q];
+        if (DO_C) ac += vc[q];
+    }
+}
+
+template <int C, bool DO_M, bool DO_C>
+__device__ __forceinline__ void class_items(int i0, int i1, int cb, const uint16_t* __restrict__ items,
+                                            const uint16_t* __restrict__ con, const double* __restrict__ sVm,
+                                            const double* __restrict__ sVc, double* om, double* oc, int tid,
+                                            int nthr) {
+    int it = i0 + tid;
+    for (; it + nthr < i1; it += 2 * nthr) {  // two items per thread in flight
+        const int s0 = items[it], s1 = items[it + nthr];
+        double am0, ac0, am1, ac1;
+        slot_sum<C, DO_M, DO_C>(con + cb + (it - i0) * C, sVm, sVc, am0, ac0);
+        slot_sum<C, DO_M, DO_C>(con + cb + (it + nthr - i0) * C, sVm, sVc, am1, ac1);
+        if (DO_M) {
+            om[s0] = am0;
+            om[s1] = am1;
+        }
+        if (DO_C) {
+            oc[s0] = ac0;
+            oc[s1] = ac1;
+        }
+    }
+    if (it < i1) {
+        const int s0 = items[it];
+        double am0, ac0;
+        slot_sum<C, DO_M, DO_C>(con + cb + (it - i0) * C, sVm, sVc, am0, ac0);
+        if (DO_M) om[s0] = am0;
+        if (DO_C) oc[s0] = ac0;
+    }
+}
+
+template <bool DO_M, bool DO_C>
+__device__ __forceinline__ void class_items_generic(int c, int i0, int i1, int cb, const uint16_t* __restrict__ items,
+                                                    const uint16_t* __restrict__ con, const double* __restrict__ sVm,
+                                                    const double* __restrict__ sVc, double* om, double* oc, int tid,
+                                                    int nthr) {
+    for (int it = i0 + tid; it < i1; it += nthr) {
+        const uint16_t* cp = con + cb + (it - i0) * c;
+        double am = 0.0, ac = 0.0;
+        for (int q = 0; q < c; ++q) {
+            const int off = cp[q];
+            if (DO_M) am += sVm[off];
+            if (DO_C) ac += sVc[off];
+        }
+        const int s = items[it];
+        if (DO_M) om[s] = am;
+        if (DO_C) oc[s] = ac;
+    }
+}
+
+// Phase B of one row block: every CSR slot of the block = the sum of its contributors in the
+// stored (ascending library element) order, class by class (uniform trip counts per class).
+template <bool DO_M, bool DO_C>
+__device__ __forceinline__ void phase_b(const uint8_t* __restrict__ rec, const FeaBlock& blk,
+                                        const double* __restrict__ sVm, const double* __restrict__ sVc, double* om,
+                                        double* oc, int tid, int nthr) {
+    const int32_t* cls = reinterpret_cast<const int32_t*>(rec);
+    const uint16_t* items = reinterpret_cast<const uint16_t*>(rec + fea_rec_off_items(blk));
+    const uint16_t* con = reinterpret_cast<const uint16_t*>(rec + fea_rec_off_contrib(blk));
+    for (int k = 0; k < blk.ncls; ++k) {
+        const int c = cls[3 * k], i0 = cls[3 * k + 1], cb = cls[3 * k + 2];
+        const int i1 = k + 1 < blk.ncls ? cls[3 * k + 4] : blk.nslots;
+        switch (c) {
+            case 1: class_items<1, DO_M, DO_C>(i0, i1, cb, items, con, sVm, sVc, om, oc, tid, nthr); break;
+            case 2: class_items<2, DO_M, DO_C>(i0, i1, cb, items, con, sVm, sVc, om, oc, tid, nthr); break;
+            case 3: class_items<3, DO_M, DO_C>(i0, i1, cb, items, con, sVm, sVc, om, oc, tid, nthr); break;
+            case 4: class_items<4, DO_M, DO_C>(i0, i1, cb, items, con, sVm, sVc, om, oc, tid, nthr); break;
+            case 6: class_items<6, DO_M, DO_C>(i0, i1, cb, items, con, sVm, sVc, om, oc, tid, nthr); break;
+            default: class_items_generic<DO_M, DO_C>(c, i0, i1, cb, items, con, sVm, sVc, om, oc, tid, nthr);
+        }
+    }
+}
+
+// ---- phase B of kernel v5 (record format: fea_internal.h fea5_item_bytes): one vector load per
+// item gives its slot and its C contributor offsets; ILP items per thread are in flight.  Each
+// slot sums its contributors in the stored (ascending library element) order.
+template <int R> struct ItemWord;
+template <> struct ItemWord<4> { using T = uint32_t; };
+template <> struct ItemWord<8> { using T = uint2; };
+template <> struct ItemWord<16> { using T = uint4; };
+// 16-bit field k of an item word (k compile-time after unrolling; shifts, no address taken)
+__device__ __forceinline__ uint32_t word_of(uint32_t w, int) { return w; }
+__device__ __forceinline__ uint32_t word_of(const uint2& w, int i) { return i == 0 ? w.x : w.y; }
+__device__ __forceinline__ uint32_t word_of(const uint4& w, int i) {
+    return i == 0 ? w.x : i == 1 ? w.y : i == 2 ? w.z : w.w;
+}
+template <typename W>
+__device__ __forceinline__ int u16_of(const W& w, int k) { return (word_of(w, k >> 1) >> (16 * (k & 1))) & 0xffff; }
+
+template <int C, bool DO_M, bool DO_C, int ILP>
+__device__ __forceinline__ void items5(const uint8_t* __restrict__ base, int n, const double* __restrict__ sVm,
+                                       const double* __restrict__ sVc, double* om, double* oc, int tid, int nthr) {
+    using W = typename ItemWord<fea5_item_bytes(C)>::T;
+    const W* it = reinterpret_cast<const W*>(base);
+    for (int i0 = tid; i0 < n; i0 += ILP * nthr) {
+        W w[ILP];
+#pragma unroll
+        for (int u = 0; u < ILP; ++u) w[u] = it[min(i0 + u * nthr, n - 1)];  // clamped: always valid
+        double vm[ILP][C], vc[ILP][C];
+#pragma unroll
+        for (int u = 0; u < ILP; ++u)
+#pragma unroll
+            for (int q = 0; q < C; ++q) {
+                const int off = u16_of(w[u], 1 + q);
+                if (DO_M) vm[u][q] = sVm[off];
+                if (DO_C) vc[u][q] = sVc[off];
+            }
+#pragma unroll
+        for (int u = 0; u < ILP; ++u)
+            if (i0 + u * nthr < n) {
+                double am = 0.0, ac = 0.0;
+#pragma unroll
+                for (int q = 0; q < C; ++q) {
+                    if (DO_M) am += vm[u][q];
+                    if (DO_C) ac += vc[u][q];
+                }
+                const int slot = u16_of(w[u], 0);
+                if (DO_M) om[slot] = am;
+                if (DO_C) oc[slot] = ac;
+            }
+    }
+}
+
+template <bool DO_M, bool DO_C>
+__device__ __forceinline__ void items5_generic(const uint8_t* __restrict__ base, int C, int n, int R,
+                                               const double* __restrict__ sVm, const double* __restrict__ sVc,
+                                               double* om, double* oc, int tid, int nthr) {
+    for (int i = tid; i < n; i += nthr) {
+        const uint16_t* w = reinterpret_cast<const uint16_t*>(base + (size_t)i * R);
+        double am = 0.0, ac = 0.0;
+        for (int q = 0; q < C; ++q) {
+            const int off = w[1 + q];
+            if (DO_M) am += sVm[off];
+            if (DO_C) ac += sVc[off];
+        }
+        if (DO_M) om[w[0]] = am;
+        if (DO_C) oc[w[0]] = ac;
+    }
+}
+
+// the classes of one block, threads tid of nthr (a block's B is split across all warps)
+template <bool DO_M, bool DO_C>
+__device__ __forceinline__ void phase_b5(const uint8_t* __restrict__ rec, int ncls, const double* __restrict__ sVm,
+                                         const double* __restrict__ sVc, double* om, double* oc, int tid, int nthr) {
+    const int4* cls = reinterpret_cast<const int4*>(rec);
+    for (int k = 0; k < ncls; ++k) {
+        const int4 c = cls[k];  // {C, n_items, byte offset, item bytes}
+        const uint8_t* base = rec + c.z;
+        switch (c.x) {
+            case 1: items5<1, DO_M, DO_C, 4>(base, c.y, sVm, sVc, om, oc, tid, nthr); break;
+            case 2: items5<2, DO_M, DO_C, 4>(base, c.y, sVm, sVc, om, oc, tid, nthr); break;
+            case 3: items5<3, DO_M, DO_C, 2>(base, c.y, sVm, sVc, om, oc, tid, nthr); break;
+            case 4: items5<4, DO_M, DO_C, 2>(base, c.y, sVm, sVc, om, oc, tid, nthr); break;
+            case 6: items5<6, DO_M, DO_C, 2>(base, c.y, sVm, sVc, om, oc, tid, nthr); break;
+            default: items5_generic<DO_M, DO_C>(base, c.x, c.y, c.w, sVm, sVc, om, oc, tid, nthr);
+        }
+    }
+}
+
+// L2 prefetch of a byte range (bulk, no completion tracking); bytes a multiple of 16
+__device__ __forceinline__ void prefetch_l2(const void* p, uint32_t bytes) {
+    asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;" ::"l"(p), "r"(bytes) : "memory");
+}
+// read-only global loads, issued where written (asm volatile keeps them ahead of their use)
+__device__ __forceinline__ double ldg_f64(const double* p) {
+    double v;
+    asm volatile("ld.global.nc.f64 %0, [%1];" : "=d"(v) : "l"(p));
+    return v;
+}
+__device__ __forceinline__ double2 ldg_f64x2(const double2* p) {
+    double2 v;
+    asm volatile("ld.global.nc.v2.f64 {%0, %1}, [%2];" : "=d"(v.x), "=d"(v.y) : "l"(p));
+    return v;
+}
+__device__ __forceinline__ int32_t ldg_s32(const int32_t* p) {
+    int32_t v;
+    asm volatile("ld.global.nc.s32 %0, [%1];" : "=r"(v) : "l"(p));
+    return v;
+}
+
+}  // namespace fea_dev

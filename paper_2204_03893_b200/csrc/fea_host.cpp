@@ -77,7 +77,7 @@ struct fea_ctx_s {
 
     // reference element
     int order = 0, np = 0, nq = 0, T = 0;
-    std::vector<double> qxy, qw, tables, qfrag;  // tables = Phi, w (kernel parameters)
+    std::vector<double> qxy, qw, tables, qfrag, jplain;  // tables = Phi, w; jplain = J (kernel parameters)
 
     // mesh, library numbering
     bool have_mesh = false;
@@ -97,6 +97,8 @@ struct fea_ctx_s {
     std::vector<int32_t> col_idx;
     FeaBlock* d_blocks = nullptr;
     uint8_t* d_records = nullptr;
+    int32_t* d_dofs = nullptr;  // v5: per-block element DOFs
+    int kver = 5;               // kernel generation of the plan (5: p <= 2 native rules, else 4)
     int nblocks = 0, e_max = 0, rec_max = 0, smem_bytes = 0, threads = 0, grid = 0;
     int32_t lay[FEA_L_N] = {0};
     int64_t record_bytes = 0;
@@ -108,6 +110,8 @@ struct fea_ctx_s {
 
     // tuning
     int64_t tune_smem = 0;
+    int tune_kver = 0;     // 0 = automatic, 4 = force kernel v4
+    int64_t tune_emax = 0; // v5 element cap per block (0 = from the budget)
 
     // reassemble buffers
     double* d_ufull = nullptr;
@@ -129,6 +133,7 @@ struct fea_ctx_s {
     void free_plan() {
         dfree(d_blocks);
         dfree(d_records);
+        dfree(d_dofs);
         dfree(d_vm);
         dfree(d_vc);
         row_ptr.clear();
@@ -204,7 +209,7 @@ bool invert(std::vector<long double>& A, int n) {
 // Tables (Algorithm 2 lines 1-3), symmetric rows only:
 //   Phi[i][q] = phi_i(x_q), w[q], and the rows t = (i <= j) of Q_m and Q_c (below).
 bool build_tables(int p, int nq, const double* qxy, const double* qw, std::vector<double>& ctab,
-                  std::vector<double>& qfrag) {
+                  std::vector<double>& qfrag, std::vector<double>& jplain) {
     int kk[FEA_MAX_NP][3];
     const int np = lib_nodes(p, kk);
     std::vector<std::pair<int, int>> mono;
@@ -250,6 +255,12 @@ bool build_tables(int p, int nq, const double* qxy, const double* qw, std::vecto
             ti[tri_index(np, i, j)] = i;
             tj[tri_index(np, i, j)] = j;
         }
+    // (2a) jplain: J [2][np][nq] reference gradients (kernel v5 parameters, constant-bank operands)
+    jplain.assign((size_t)2 * np * nq, 0.0);
+    for (int i = 0; i < np * nq; ++i) {
+        jplain[i] = (double)gx[i];
+        jplain[(size_t)np * nq + i] = (double)gy[i];
+    }
     for (int f = 0; f < 4; ++f)
         for (int tt = 0; tt < NTT; ++tt)
             for (int kk = 0; kk < NK; ++kk)
@@ -368,8 +379,8 @@ fea_status fea_set_element(fea_ctx c, int order, int n_q, const double* q_xy, co
     }
     if (fabsl(s - 0.5L) > 1e-14L)
         return c->fail(FEA_E_ARG, "quadrature weights sum to %.17g, expected 1/2 (reference-triangle measure)", (double)s);
-    std::vector<double> ctab, qfrag;
-    if (!build_tables(order, n_q, q_xy, q_w, ctab, qfrag)) return c->fail(FEA_E_UNSUPPORTED, "singular Vandermonde");
+    std::vector<double> ctab, qfrag, jplain;
+    if (!build_tables(order, n_q, q_xy, q_w, ctab, qfrag, jplain)) return c->fail(FEA_E_UNSUPPORTED, "singular Vandermonde");
     if (ctab.size() > FEA_CTAB_MAX) return c->fail(FEA_E_UNSUPPORTED, "tables exceed the parameter bank");
     if (!c->host_only) cudaSetDevice(c->device);
     c->free_mesh();
@@ -382,6 +393,7 @@ fea_status fea_set_element(fea_ctx c, int order, int n_q, const double* q_xy, co
     c->qw.assign(q_w, q_w + n_q);
     c->tables = ctab;
     c->qfrag = qfrag;
+    c->jplain = jplain;
     if (c->host_only) return FEA_OK;
     FEA_CUDA(c, cudaMalloc(&c->d_tables, qfrag.size() * sizeof(double)));
     FEA_CUDA(c, cudaMemcpy(c->d_tables, qfrag.data(), qfrag.size() * sizeof(double), cudaMemcpyHostToDevice));
@@ -506,6 +518,14 @@ fea_status fea_set_tuning(fea_ctx c, int key, int64_t value) {
             if (value != 0 && (value < 4096 || value > 232448)) return c->fail(FEA_E_ARG, "smem budget out of range");
             c->tune_smem = value;
             break;
+        case 2:  // kernel generation (0 = automatic, 4 = force v4)
+            if (value != 0 && value != 4 && value != 5) return c->fail(FEA_E_ARG, "kernel must be 0, 4 or 5");
+            c->tune_kver = (int)value;
+            break;
+        case 3:  // v5 elements per block cap
+            if (value < 0 || value > 65535) return c->fail(FEA_E_ARG, "element cap out of range");
+            c->tune_emax = value;
+            break;
         case 4:  // plan matrices bitmask (FEA_MASS | FEA_STIFF)
             if (value < 1 || value > 3) return c->fail(FEA_E_ARG, "plan matrices must be a nonzero MASS|STIFF mask");
             c->plan_which = (int)value;
@@ -534,16 +554,29 @@ fea_status fea_build_pattern(fea_ctx c, int64_t* row_begin, int64_t* n_rows_loca
     // ---- shared-memory budget -> elements per block (e_max) and record budget
     const int dm = (c->plan_which & FEA_MASS) ? 1 : 0, dcm = (c->plan_which & FEA_STIFF) ? 1 : 0;
     const int nmat = dm + dcm;
-    const int rstages = c->order <= 2 ? 3 : 2;  // fea_rstages
-    const int ctas = c->order <= 2 ? 2 : 1;     // fea_ctas
-    const int64_t budget = c->tune_smem ? c->tune_smem : (ctas == 2 ? 113 * 1024 : 226 * 1024);
-    const int nqp = 4 * fea_nk_kernel(c->order, nq);
-    const int64_t per_el_smem = 8LL * T * nmat + 2 * (8LL * np + 48) + 2 * 8LL * nqp + 32;
-    const double rec_el = 1.3 * (3.0 * np * np + 4.0 * np) + 8;  // record bytes per element (estimate)
-    int64_t e_max = (int64_t)((budget - 256 - 3 * 128) / (per_el_smem + rstages * rec_el));
-    e_max = std::min<int64_t>(e_max, 65535 / T);
-    e_max = e_max >= 8 ? ((e_max - 8) / 16) * 16 + 8 : 0;  // multiple of 8, == 8 mod 16
-    const int64_t rec_budget = ((int64_t)(rec_el * e_max) + 15) & ~int64_t(15);
+    const bool v5 = fea5_supported(c->order, nq) && c->tune_kver != 4;
+    c->kver = v5 ? 5 : 4;
+    const int rstages = c->order <= 2 ? 3 : 2;  // fea_rstages (v4)
+    int64_t e_max, rec_budget;
+    if (v5) {
+        // two V_m, V_c [T][e_max | 1] buffers + two record stages in 227 KiB (one CTA per SM)
+        const int64_t budget = c->tune_smem ? c->tune_smem : 227 * 1024;
+        const double rec_el = 1.1 * 2.0 * np * np + 8;  // record bytes per element (estimate)
+        e_max = (int64_t)((budget - 1024) / (2 * (8.0 * T * nmat + rec_el)));
+        if (c->tune_emax) e_max = std::min(e_max, c->tune_emax);
+        e_max = std::min<int64_t>(e_max, 65535 / T - 1) / 8 * 8;
+        rec_budget = ((budget - 1024 - 2 * 8LL * T * nmat * (e_max | 1)) / 2 - 128) & ~int64_t(15);
+    } else {
+        const int ctas = c->order <= 2 ? 2 : 1;  // fea_ctas
+        const int64_t budget = c->tune_smem ? c->tune_smem : (ctas == 2 ? 113 * 1024 : 226 * 1024);
+        const int nqp = 4 * fea_nk_kernel(c->order, nq);
+        const int64_t per_el_smem = 8LL * T * nmat + 2 * (8LL * np + 48) + 2 * 8LL * nqp + 32;
+        const double rec_el = 1.3 * (3.0 * np * np + 4.0 * np) + 8;  // record bytes per element (estimate)
+        e_max = (int64_t)((budget - 256 - 3 * 128) / (per_el_smem + rstages * rec_el));
+        e_max = std::min<int64_t>(e_max, 65535 / T);
+        e_max = e_max >= 8 ? ((e_max - 8) / 16) * 16 + 8 : 0;  // multiple of 8, == 8 mod 16
+        rec_budget = ((int64_t)(rec_el * e_max) + 15) & ~int64_t(15);
+    }
 
     // ---- incidence of this rank's rows (ascending library element per row)
     std::vector<int64_t> iptr(nr + 1, 0);
@@ -581,7 +614,8 @@ fea_status fea_build_pattern(fea_ctx c, int64_t* row_begin, int64_t* n_rows_loca
             int64_t add = 0;
             for (int64_t k = iptr[r]; k < iptr[r + 1]; ++k) add += mark[inc[k]] != cur;
             const int64_t rent = (iptr[r + 1] - iptr[r]) * np;
-            const int64_t ub = 4 * (ent + rent) + 4 * np * (nE + add + 3) + 12 * FEA_MAX_CLASSES + 64;
+            const int64_t ub = v5 ? 4 * (ent + rent) + 32 * FEA_MAX_CLASSES + 64
+                                  : 4 * (ent + rent) + 4 * np * (nE + add + 3) + 12 * FEA_MAX_CLASSES + 64;
             if (cur < 0 || nE + add > e_max || ub > rec_budget) {
                 ++cur;
                 brow.push_back(r);
@@ -599,14 +633,14 @@ fea_status fea_build_pattern(fea_ctx c, int64_t* row_begin, int64_t* n_rows_loca
 
     // ---- per block: element set, (row, col) records sorted -> slots, contributors, record
     struct BOut {
-        std::vector<int32_t> rownnz, cols;
+        std::vector<int32_t> rownnz, cols, dofs;
         std::vector<uint8_t> rec;
         FeaBlock fb{};
         int64_t nghost = 0, nown = 0;
         std::string err;
     };
     std::vector<BOut> bo(nb);
-    const int64_t EM = e_max;
+    const int64_t EM = v5 ? (e_max | 1) : e_max;  // V row stride (v5: odd, fea_kernels5.cu)
     parallel_for(nb, [&](int64_t b) {
         BOut& o = bo[b];
         const int64_t ra = brow[b], rb = brow[b + 1];
@@ -675,17 +709,51 @@ fea_status fea_build_pattern(fea_ctx c, int64_t* row_begin, int64_t* n_rows_loca
             o.err = "too many contributor-count classes";
             return;
         }
-        F.rec_bytes = fea_rec_bytes(F, np);
-        if (F.rec_bytes > rec_budget) {
-            o.err = "record exceeds the shared-memory budget";
-            return;
+        if (v5) {  // class table + fixed-size item records (fea_internal.h)
+            const int ncl = F.ncls;
+            std::vector<int32_t> coff(ncl);
+            int32_t off = 16 * ncl;
+            for (int k2 = 0; k2 < ncl; ++k2) {
+                const int C = cls[3 * k2], n = (k2 + 1 < ncl ? cls[3 * k2 + 4] : nslot) - cls[3 * k2 + 1];
+                coff[k2] = off;
+                off += fea_pad16(n * fea5_item_bytes(C));
+            }
+            F.rec_bytes = off;
+            if (F.rec_bytes > rec_budget) {
+                o.err = "record exceeds the shared-memory budget";
+                return;
+            }
+            o.rec.assign(F.rec_bytes, 0);
+            int32_t* tab = reinterpret_cast<int32_t*>(o.rec.data());
+            for (int k2 = 0; k2 < ncl; ++k2) {
+                const int C = cls[3 * k2], i0 = cls[3 * k2 + 1], n = (k2 + 1 < ncl ? cls[3 * k2 + 4] : nslot) - i0;
+                const int R = fea5_item_bytes(C);
+                tab[4 * k2] = C;
+                tab[4 * k2 + 1] = n;
+                tab[4 * k2 + 2] = coff[k2];
+                tab[4 * k2 + 3] = R;
+                for (int it = 0; it < n; ++it) {
+                    uint16_t* w = reinterpret_cast<uint16_t*>(o.rec.data() + coff[k2] + (size_t)it * R);
+                    w[0] = items[i0 + it];
+                    for (int q = 0; q < C; ++q) w[1 + q] = contrib[cls[3 * k2 + 2] + (size_t)it * C + q];
+                }
+            }
+        } else {
+            F.rec_bytes = fea_rec_bytes(F, np);
+            if (F.rec_bytes > rec_budget) {
+                o.err = "record exceeds the shared-memory budget";
+                return;
+            }
+            o.rec.assign(F.rec_bytes, 0);
+            std::memcpy(o.rec.data(), cls.data(), 4 * cls.size());
+            std::memcpy(o.rec.data() + fea_rec_off_items(F), items.data(), 2 * items.size());
+            std::memcpy(o.rec.data() + fea_rec_off_contrib(F), contrib.data(), 2 * contrib.size());
         }
-        o.rec.assign(F.rec_bytes, 0);
-        std::memcpy(o.rec.data(), cls.data(), 4 * cls.size());
-        std::memcpy(o.rec.data() + fea_rec_off_items(F), items.data(), 2 * items.size());
-        std::memcpy(o.rec.data() + fea_rec_off_contrib(F), contrib.data(), 2 * contrib.size());
-        int32_t* dofs = reinterpret_cast<int32_t*>(o.rec.data() + fea_rec_off_dofs(F));
         const int32_t nEp = fea_pad4(F.nE);
+        if (v5) o.dofs.assign((size_t)np * nEp, 0);
+        F.r0 = (int32_t)ga;
+        F.nr = (int32_t)(gb - ga);
+        int32_t* dofs = v5 ? o.dofs.data() : reinterpret_cast<int32_t*>(o.rec.data() + fea_rec_off_dofs(F));
         for (int64_t le = 0; le < (int64_t)E.size(); ++le)
             for (int i = 0; i < np; ++i) dofs[i * nEp + le] = c->ed[(size_t)E[le] * np + i];
         for (int64_t le = E.size(); le < nEp; ++le)  // padding lanes point at a valid DOF
@@ -696,12 +764,14 @@ fea_status fea_build_pattern(fea_ctx c, int64_t* row_begin, int64_t* n_rows_loca
 
     // ---- concatenate
     std::vector<FeaBlock> blocks(nb);
-    int64_t nnz = 0, rbytes = 0, ncon = 0, visits = 0, owned = 0, rec_max = 16;
+    int64_t nnz = 0, rbytes = 0, ncon = 0, visits = 0, owned = 0, rec_max = 16, ndofs = 0;
     for (int64_t b = 0; b < nb; ++b) {
         FeaBlock& B = blocks[b];
         B = bo[b].fb;
         B.slot0 = nnz;
         B.rec_off = rbytes;
+        B.dof_off = ndofs;
+        ndofs += (int64_t)bo[b].dofs.size();
         nnz += B.nslots;
         rbytes += B.rec_bytes;
         ncon += B.ncontrib;
@@ -713,8 +783,11 @@ fea_status fea_build_pattern(fea_ctx c, int64_t* row_begin, int64_t* n_rows_loca
     c->row_ptr.assign(nr + 1, 0);
     c->col_idx.resize(nnz);
     std::vector<uint8_t> records(std::max<int64_t>(rbytes, 16));
+    std::vector<int32_t> alldofs(std::max<int64_t>(ndofs, 4));
     parallel_for(nb, [&](int64_t b) {
         const FeaBlock& B = blocks[b];
+        std::copy(bo[b].dofs.begin(), bo[b].dofs.end(), alldofs.begin() + B.dof_off);
+        std::vector<int32_t>().swap(bo[b].dofs);
         std::copy(bo[b].cols.begin(), bo[b].cols.end(), c->col_idx.begin() + B.slot0);
         std::memcpy(records.data() + B.rec_off, bo[b].rec.data(), B.rec_bytes);
         for (int64_t r = brow[b]; r < brow[b + 1]; ++r) c->row_ptr[r + 1] = bo[b].rownnz[r - brow[b]];
@@ -724,7 +797,8 @@ fea_status fea_build_pattern(fea_ctx c, int64_t* row_begin, int64_t* n_rows_loca
     bo.clear();
 
     int32_t L[FEA_L_N];
-    fea_smem_layout(L, rstages, (int)rec_max, (int)e_max, c->order, nq, dm, dcm);
+    if (v5) fea5_smem_layout(L, (int)rec_max, (int)e_max, c->order, dm, dcm);
+    else fea_smem_layout(L, rstages, (int)rec_max, (int)e_max, c->order, nq, dm, dcm);
     c->nblocks = (int)nb;
     c->e_max = (int)e_max;
     c->rec_max = (int)rec_max;
@@ -747,10 +821,15 @@ fea_status fea_build_pattern(fea_ctx c, int64_t* row_begin, int64_t* n_rows_loca
     if (nb) FEA_CUDA(c, cudaMemcpy(c->d_blocks, blocks.data(), nb * sizeof(FeaBlock), cudaMemcpyHostToDevice));
     FEA_CUDA(c, cudaMalloc((void**)&c->d_records, records.size()));
     FEA_CUDA(c, cudaMemcpy(c->d_records, records.data(), records.size(), cudaMemcpyHostToDevice));
+    if (v5) {
+        FEA_CUDA(c, cudaMalloc((void**)&c->d_dofs, alldofs.size() * sizeof(int32_t)));
+        FEA_CUDA(c, cudaMemcpy(c->d_dofs, alldofs.data(), alldofs.size() * sizeof(int32_t), cudaMemcpyHostToDevice));
+    }
     if (!c->d_ufull) FEA_CUDA(c, cudaMalloc(&c->d_ufull, (size_t)rpr * c->world * sizeof(double)));
     if (!c->d_usend) FEA_CUDA(c, cudaMalloc(&c->d_usend, (size_t)rpr * sizeof(double)));
     int occ = 0;
-    int rc = fea_kernel_occupancy(c->order, c->nq, dm, dcm, c->smem_bytes, &occ, &c->threads);
+    int rc = v5 ? fea_kernel_occupancy5(c->order, dm, dcm, c->smem_bytes, &occ, &c->threads)
+                : fea_kernel_occupancy(c->order, c->nq, dm, dcm, c->smem_bytes, &occ, &c->threads);
     if (rc != 0) return c->fail(FEA_E_CUDA, "occupancy query: %s", cudaGetErrorString((cudaError_t)rc));
     if (occ < 1) return c->fail(FEA_E_UNSUPPORTED, "kernel does not fit: %d B shared memory", c->smem_bytes);
     c->grid = (int)std::min<int64_t>(std::max<int64_t>(nb, 1), (int64_t)occ * c->sm_count);
@@ -816,6 +895,7 @@ static fea_status launch(fea_ctx c, const double* u, double* vm, double* vc) {
     prm.blocks = c->d_blocks;
     prm.records = c->d_records;
     prm.xy = c->d_xy;
+    prm.dofs = c->d_dofs;
     prm.u = u;
     prm.qfrag = c->d_tables;
     prm.out_m = vm;
@@ -828,15 +908,18 @@ static fea_status launch(fea_ctx c, const double* u, double* vm, double* vc) {
     prm.coef_m = c->coef_m;
     prm.coef_c = c->coef_c;
     std::memcpy(prm.ctab, c->tables.data(), c->tables.size() * sizeof(double));
+    if (c->kver == 5) std::memcpy(prm.jtab, c->jplain.data(), c->jplain.size() * sizeof(double));
+    if (const char* dm = getenv("FEA_DEBUG_MODE")) prm.dbg_mode = atoi(dm);
     if (getenv("FEA_DEBUG_TIMING")) {
         if (!c->d_dbg) {
-            FEA_CUDA(c, cudaMalloc(&c->d_dbg, 8 * sizeof(unsigned long long)));
-            FEA_CUDA(c, cudaMemset(c->d_dbg, 0, 8 * sizeof(unsigned long long)));
+            FEA_CUDA(c, cudaMalloc(&c->d_dbg, 1536 * sizeof(unsigned long long)));
+            FEA_CUDA(c, cudaMemset(c->d_dbg, 0, 1536 * sizeof(unsigned long long)));
         }
         prm.dbg = c->d_dbg;
     }
     if (c->nblocks == 0) return FEA_OK;
-    const int rc = fea_launch_reassemble(prm, c->order, c->smem_bytes, c->grid, c->stream);
+    const int rc = c->kver == 5 ? fea_launch_reassemble5(prm, c->order, c->smem_bytes, c->grid, c->stream)
+                                : fea_launch_reassemble(prm, c->order, c->smem_bytes, c->grid, c->stream);
     if (rc != 0) return c->fail(FEA_E_CUDA, "k_reassemble launch: %s", cudaGetErrorString((cudaError_t)rc));
     return FEA_OK;
 }
@@ -959,14 +1042,23 @@ fea_status fea_get_stat(fea_ctx c, int key, int64_t* value) {
         case 7: *value = c->e_max; break;
         case 8: *value = c->grid; break;
         case 9: *value = c->record_bytes; break;
-        case 20: case 21: case 22: case 23: case 24: case 25: {  // FEA_DEBUG_TIMING cycle sums
+        case 20: case 21: case 22: case 23: case 24: case 25: case 26: case 27:
+        case 28: case 29: case 30: case 31: case 32: case 33: case 34: case 35: {  // FEA_DEBUG_TIMING cycle sums
             unsigned long long v = 0;
             if (c->d_dbg) FEA_CUDA(c, cudaMemcpy(&v, c->d_dbg + (key - 20), sizeof(v), cudaMemcpyDeviceToHost));
             *value = (int64_t)v;
             break;
         }
         case 10: *value = c->rec_max; break;
-        default: return c->fail(FEA_E_ARG, "unknown stat key %d", key);
+        default:
+            if (key >= 40 && key < 1536 + 24) {  // FEA_DEBUG_MODE & 8 / 32 trace words
+                unsigned long long v = 0;
+                if (c->d_dbg) FEA_CUDA(c, cudaMemcpy(&v, c->d_dbg + 16 + (key - 40), sizeof(v), cudaMemcpyDeviceToHost));
+                *value = (int64_t)v;
+                break;
+            }
+            return c->fail(FEA_E_ARG, "unknown stat key %d", key);
+        case 11: *value = c->kver; break;
     }
     return FEA_OK;
 }

@@ -49,13 +49,19 @@ __host__ __device__ constexpr int fea_kt(int p) { return (fea_np(p) + 3) / 4; }
 struct FeaBlock {
     int64_t slot0;
     int64_t rec_off;   // byte offset of the record
+    int64_t dof_off;   // v5: offset (int32 units) of the block's element DOFs [n_p][pad4(nE)] in
+                       // FeaKParams::dofs (v4 keeps them at the end of the record instead)
     int32_t nslots;
     int32_t ncontrib;
     int32_t nE;
     int32_t rec_bytes; // multiple of 16
     int32_t ncls;
     int32_t pad_;
+    int32_t r0, nr;    // v5: the block's own rows [r0, r0 + nr) (library DOFs): the bulk of the u and
+                       // xy entries its gathers touch (L2-prefetched blocks ahead)
+    int32_t spare_[2]; // 64 bytes: the v5 kernel copies descriptors with 16-byte cp.async
 };
+static_assert(sizeof(FeaBlock) == 64, "FeaBlock must stay 64 bytes");
 
 __host__ __device__ inline int32_t fea_pad16(int32_t b) { return (b + 15) & ~15; }
 __host__ __device__ inline int32_t fea_pad4(int32_t n) { return (n + 3) & ~3; }
@@ -69,6 +75,23 @@ __host__ __device__ inline int32_t fea_rec_off_dofs(const FeaBlock& b) {
 __host__ __device__ inline int32_t fea_rec_bytes(const FeaBlock& b, int np) {
     return fea_rec_off_dofs(b) + 4 * np * fea_pad4(b.nE);
 }
+// v5 record: int4 class table {C, n_items, byte offset, item bytes} [ncls], then per class n_items
+// fixed-size item records {u16 block-local slot, u16 V offset [C]} of fea5_item_bytes(C) bytes
+// (one vector shared-memory load per item), each class array 16-byte aligned.  Classes group
+// the slots by contributor count C so a warp's lanes run uniform trip counts.
+__host__ __device__ constexpr int fea5_item_bytes(int C) {
+    return C == 1 ? 4 : C <= 3 ? 8 : C <= 7 ? 16 : (2 * (C + 1) + 15) / 16 * 16;
+}
+
+// ---- kernel v5 (p <= 2 with the configs' native rules): lane-per-element, constant-bank tables.
+// NW warps per CTA (no producer warp), one CTA per SM, and the units per 32-element tile.
+__host__ __device__ constexpr int fea5_nw(int p) { return p == 1 ? 16 : 16; }
+__host__ __device__ constexpr int fea5_ctas(int p) { return 1; }
+__host__ __device__ constexpr int fea5_nsplit(int p) { return p == 2 ? 2 : 1; }  // units per tile
+__host__ __device__ constexpr int fea5_threads(int p) { return fea5_nw(p) * 32; }
+__host__ __device__ constexpr bool fea5_supported(int p, int nq) { return p <= 2 && nq == fea_nq_native(p); }
+// reference gradients in the kernel parameters: jtab[a][k][q] = d phi_k / d xhat_a at x_q
+#define FEA_JTAB_MAX (2 * 6 * 6)
 
 // Coefficient k(u) (fea.h FEA_K_*).
 struct FeaCoef {
@@ -103,11 +126,28 @@ __host__ __device__ inline void fea_smem_layout(int32_t* L, int rstages, int rec
     L[FEA_L_TOTAL] = o;
 }
 
+// Shared-memory layout of k_reassemble5: V_m, V_c [2][T][e_max | 1], two record stages of
+// stride L[FEA_L_GU], mbarriers (6), descriptor ring (8 x 64 B at L[FEA_L_W]).
+__host__ __device__ inline void fea5_smem_layout(int32_t* L, int rec_max, int e_max, int p, int do_m, int do_c) {
+    const int T = fea_T(p);
+    for (int i = 0; i < FEA_L_N; ++i) L[i] = 0;
+    int32_t o = 0;
+    L[FEA_L_VM] = o; o += do_m ? 2 * 8 * T * (e_max | 1) : 0;
+    L[FEA_L_VC] = o; o += do_c ? 2 * 8 * T * (e_max | 1) : 0;
+    o = (o + 127) / 128 * 128;
+    L[FEA_L_GU] = (rec_max + 127) / 128 * 128;  // record stage stride
+    L[FEA_L_REC] = o; o += 2 * L[FEA_L_GU];
+    L[FEA_L_BARS] = o; o += 64;
+    L[FEA_L_W] = o; o += 64 * 8;
+    L[FEA_L_TOTAL] = o;
+}
+
 // Kernel parameters (passed by value as __grid_constant__).
 struct FeaKParams {
     const FeaBlock* blocks;
     const uint8_t* records;   // all block records
     const double2* xy;        // [n_dof] DOF coordinates (vertex DOFs give B_e)
+    const int32_t* dofs;      // v5: all blocks' element DOFs (see FeaBlock::dof_off)
     const double* u;          // [n_dof] u_full, library numbering
     const double* qfrag;      // Q_f A-fragments [4][NTT][NK][32] (lane order), zero padded
     double* out_m;            // [nslots_total] (rank-local slot index) or nullptr
@@ -117,13 +157,18 @@ struct FeaKParams {
     int32_t e_max;            // V / Lambda row stride (elements per block, max)
     int32_t nq;
     int32_t same_coef;        // mass and stiffness share k -> one Lambda
+    int32_t dbg_mode;         // diagnostics only (FEA_DEBUG_MODE): 1 skip B stores, 2 skip B, 4 skip A2
     int32_t lay[FEA_L_N];     // shared-memory layout (byte offsets)
     FeaCoef coef_m;
     FeaCoef coef_c;
     double ctab[FEA_CTAB_MAX];  // Phi [np][nq] at 0, w [nq] at pad2(np nq)
+    double jtab[FEA_JTAB_MAX];  // v5: J [2][np][nq] (constant-bank DFMA operands)
 };
 
 // Launch the fused reassembly kernel (defined in fea_kernels.cu).  Returns a cudaError_t.
 int fea_launch_reassemble(const FeaKParams& prm, int order, int smem_bytes, int grid, void* stream);
 // Per-SM CTA occupancy of the kernel variant and its block size (threads).
 int fea_kernel_occupancy(int order, int nq, int do_m, int do_c, int smem_bytes, int* ctas_per_sm, int* threads);
+// The same for kernel v5 (fea_kernels5.cu).
+int fea_launch_reassemble5(const FeaKParams& prm, int order, int smem_bytes, int grid, void* stream);
+int fea_kernel_occupancy5(int order, int do_m, int do_c, int smem_bytes, int* ctas_per_sm, int* threads);

@@ -25,177 +25,10 @@
 #include <cuda_runtime.h>
 #include <cstdint>
 
-#include "fea_internal.h"
+#include "fea_device.cuh"
 
 namespace {
-
-// ------------------------------------------------------------------ PTX helpers
-__device__ __forceinline__ uint32_t smem_u32(const void* p) { return (uint32_t)__cvta_generic_to_shared(p); }
-
-__device__ __forceinline__ void mbar_init(uint64_t* bar, uint32_t count) {
-    asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_u32(bar)), "r"(count) : "memory");
-}
-__device__ __forceinline__ void fence_mbar_init() { asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory"); }
-__device__ __forceinline__ void fence_proxy_async() { asm volatile("fence.proxy.async.shared::cta;" ::: "memory"); }
-__device__ __forceinline__ void mbar_expect_tx(uint64_t* bar, uint32_t bytes) {
-    asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(bar)), "r"(bytes) : "memory");
-}
-__device__ __forceinline__ void mbar_arrive(uint64_t* bar) {
-    asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(smem_u32(bar)) : "memory");
-}
-__device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity) {
-    asm volatile(
-        "{\n\t.reg .pred p;\n"
-        "WAIT_%=:\n\t"
-        "mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n\t"
-        "@!p bra WAIT_%=;\n}" ::"r"(smem_u32(bar)),
-        "r"(parity)
-        : "memory");
-}
-// 1D TMA bulk copy global -> shared, completion counted on an mbarrier
-__device__ __forceinline__ void tma_load_1d(void* dst, const void* src, uint32_t bytes, uint64_t* bar) {
-    asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
-                     smem_u32(dst)),
-                 "l"(src), "r"(bytes), "r"(smem_u32(bar))
-                 : "memory");
-}
-__device__ __forceinline__ void cp_async8(void* dst, const void* src) {
-    asm volatile("cp.async.ca.shared.global [%0], [%1], 8;" ::"r"(smem_u32(dst)), "l"(src) : "memory");
-}
-__device__ __forceinline__ void cp_async16(void* dst, const void* src) {
-    asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(smem_u32(dst)), "l"(src) : "memory");
-}
-// arrive on `bar` once all prior cp.async of this thread have completed
-__device__ __forceinline__ void cp_async_mbar_arrive(uint64_t* bar) {
-    asm volatile("cp.async.mbarrier.arrive.noinc.shared::cta.b64 [%0];" ::"r"(smem_u32(bar)) : "memory");
-}
-__device__ __forceinline__ void consumer_sync(int nct) {  // named barrier 1: consumer warps only
-    asm volatile("bar.sync 1, %0;" ::"r"(nct) : "memory");
-}
-// D = A (8x4, row) * B (4x8, col) + D on the FP64 tensor core; fragment ownership per lane
-// (g = lane / 4, c = lane % 4): a = A[g][c], b = B[c][g], d = D[g][2c .. 2c+1].
-__device__ __forceinline__ void dmma(double& d0, double& d1, double a, double b) {
-    asm volatile("mma.sync.aligned.m8n8k4.row.col.f64.f64.f64.f64 {%0,%1}, {%2}, {%3}, {%0,%1};"
-                 : "+d"(d0), "+d"(d1)
-                 : "d"(a), "d"(b));
-}
-
-// ------------------------------------------------------------------ math
-template <int N>
-__device__ __forceinline__ double horner(const double* par, double u) {  // sum_{i<N} par[i] u^i
-    double r = par[N - 1];
-#pragma unroll
-    for (int i = N - 2; i >= 0; --i) r = fma(r, u, par[i]);
-    return r;
-}
-
-// k(u); the branch is warp-uniform (one coefficient per launch), each case straight-line.
-__device__ __forceinline__ double keval(const FeaCoef& c, double u) {
-    if (c.kind == 0) {
-        switch (c.npar) {
-            case 1: return c.par[0];
-            case 2: return horner<2>(c.par, u);
-            case 3: return horner<3>(c.par, u);
-            case 4: return horner<4>(c.par, u);
-            case 5: return horner<5>(c.par, u);
-            case 6: return horner<6>(c.par, u);
-            case 7: return horner<7>(c.par, u);
-            case 8: return horner<8>(c.par, u);
-            default: return horner<9>(c.par, u);
-        }
-    }
-    if (c.kind == 1) return c.par[0] * exp(c.par[1] * u);
-    // piecewise linear, segment s covers (T_s, T_{s+1}]
-    const int m = c.npar / 2;
-    int s = 0;
-    while (s < m - 2 && u > c.par[2 * (s + 1)]) ++s;
-    const double T0 = c.par[2 * s], k0 = c.par[2 * s + 1], T1 = c.par[2 * s + 2], k1 = c.par[2 * s + 3];
-    return k0 + (k1 - k0) / (T1 - T0) * (u - T0);
-}
-
-// Element geometry from the staged vertex coordinates: b_e = |det B_e|, A_e = (B^T B)^{-1}
-__device__ __forceinline__ void geometry(const double2* __restrict__ gX, int e_max, int le, double& absdet,
-                                         double& A00, double& A11, double& A01) {
-    const double2 a = gX[le], b = gX[e_max + le], c = gX[2 * e_max + le];
-    const double B00 = b.x - a.x, B10 = b.y - a.y, B01 = c.x - a.x, B11 = c.y - a.y;
-    const double det = B00 * B11 - B01 * B10;
-    absdet = fabs(det);
-    const double inv = 1.0 / (det * det);  // det(B^T B) = det(B)^2
-    A00 = (B01 * B01 + B11 * B11) * inv;
-    A11 = (B00 * B00 + B10 * B10) * inv;
-    A01 = -(B00 * B01 + B10 * B11) * inv;
-}
-
-// ------------------------------------------------------------------ phase B helpers
-// Sum of the C contributors of one slot in the fixed (stored) order, all loads issued first.
-template <int C, bool DO_M, bool DO_C>
-__device__ __forceinline__ void slot_sum(const uint16_t* __restrict__ cp, const double* __restrict__ sVm,
-                                         const double* __restrict__ sVc, double& am, double& ac) {
-    int off[C];
-#pragma unroll
-    for (int q = 0; q < C; ++q) off[q] = cp[q];
-    double vm[C], vc[C];
-#pragma unroll
-    for (int q = 0; q < C; ++q) {
-        if (DO_M) vm[q] = sVm[off[q]];
-        if (DO_C) vc[q] = sVc[off[q]];
-    }
-    am = 0.0;
-    ac = 0.0;
-#pragma unroll
-    for (int q = 0; q < C; ++q) {
-        if (DO_M) am += vm[q];
-        if (DO_C) ac += vc[q];
-    }
-}
-
-template <int C, bool DO_M, bool DO_C>
-__device__ __forceinline__ void class_items(int i0, int i1, int cb, const uint16_t* __restrict__ items,
-                                            const uint16_t* __restrict__ con, const double* __restrict__ sVm,
-                                            const double* __restrict__ sVc, double* om, double* oc, int tid,
-                                            int nthr) {
-    int it = i0 + tid;
-    for (; it + nthr < i1; it += 2 * nthr) {  // two items per thread in flight
-        const int s0 = items[it], s1 = items[it + nthr];
-        double am0, ac0, am1, ac1;
-        slot_sum<C, DO_M, DO_C>(con + cb + (it - i0) * C, sVm, sVc, am0, ac0);
-        slot_sum<C, DO_M, DO_C>(con + cb + (it + nthr - i0) * C, sVm, sVc, am1, ac1);
-        if (DO_M) {
-            om[s0] = am0;
-            om[s1] = am1;
-        }
-        if (DO_C) {
-            oc[s0] = ac0;
-            oc[s1] = ac1;
-        }
-    }
-    if (it < i1) {
-        const int s0 = items[it];
-        double am0, ac0;
-        slot_sum<C, DO_M, DO_C>(con + cb + (it - i0) * C, sVm, sVc, am0, ac0);
-        if (DO_M) om[s0] = am0;
-        if (DO_C) oc[s0] = ac0;
-    }
-}
-
-template <bool DO_M, bool DO_C>
-__device__ __forceinline__ void class_items_generic(int c, int i0, int i1, int cb, const uint16_t* __restrict__ items,
-                                                    const uint16_t* __restrict__ con, const double* __restrict__ sVm,
-                                                    const double* __restrict__ sVc, double* om, double* oc, int tid,
-                                                    int nthr) {
-    for (int it = i0 + tid; it < i1; it += nthr) {
-        const uint16_t* cp = con + cb + (it - i0) * c;
-        double am = 0.0, ac = 0.0;
-        for (int q = 0; q < c; ++q) {
-            const int off = cp[q];
-            if (DO_M) am += sVm[off];
-            if (DO_C) ac += sVc[off];
-        }
-        const int s = items[it];
-        if (DO_M) om[s] = am;
-        if (DO_C) oc[s] = ac;
-    }
-}
+using namespace fea_dev;
 
 // ------------------------------------------------------------------ the kernel
 template <int P, int NQ_T, bool DO_M, bool DO_C>
@@ -451,23 +284,8 @@ __global__ void __launch_bounds__(fea_threads(P), fea_ctas(P)) k_reassemble(cons
         tick(5);
 
         // ---------------- Phase B: fixed-order segmented reduction into the CSR slots.
-        const int32_t* cls = reinterpret_cast<const int32_t*>(rec);
-        const uint16_t* items = reinterpret_cast<const uint16_t*>(rec + fea_rec_off_items(blk));
-        const uint16_t* con = reinterpret_cast<const uint16_t*>(rec + fea_rec_off_contrib(blk));
-        double* om = DO_M ? prm.out_m + blk.slot0 : nullptr;
-        double* oc = DO_C ? prm.out_c + blk.slot0 : nullptr;
-        for (int k = 0; k < blk.ncls; ++k) {
-            const int c = cls[3 * k], i0 = cls[3 * k + 1], cb = cls[3 * k + 2];
-            const int i1 = k + 1 < blk.ncls ? cls[3 * k + 4] : blk.nslots;
-            switch (c) {
-                case 1: class_items<1, DO_M, DO_C>(i0, i1, cb, items, con, sVm, sVc, om, oc, tid, NCT); break;
-                case 2: class_items<2, DO_M, DO_C>(i0, i1, cb, items, con, sVm, sVc, om, oc, tid, NCT); break;
-                case 3: class_items<3, DO_M, DO_C>(i0, i1, cb, items, con, sVm, sVc, om, oc, tid, NCT); break;
-                case 4: class_items<4, DO_M, DO_C>(i0, i1, cb, items, con, sVm, sVc, om, oc, tid, NCT); break;
-                case 6: class_items<6, DO_M, DO_C>(i0, i1, cb, items, con, sVm, sVc, om, oc, tid, NCT); break;
-                default: class_items_generic<DO_M, DO_C>(c, i0, i1, cb, items, con, sVm, sVc, om, oc, tid, NCT);
-            }
-        }
+        phase_b<DO_M, DO_C>(rec, blk, sVm, sVc, DO_M ? prm.out_m + blk.slot0 : nullptr,
+                            DO_C ? prm.out_c + blk.slot0 : nullptr, tid, NCT);
         tick(3);
         consumer_sync(NCT);  // V and the record stage are free
         tick(5);

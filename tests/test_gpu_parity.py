@@ -32,12 +32,16 @@ SMALL = [("C1", 32), ("C2", 48), ("C3", 24), ("C4", 96), ("C5", 12)]
 
 
 @pytest.mark.parametrize("name,N", SMALL)
-def test_config_parity_small(name, N):
+@pytest.mark.parametrize("kernel", [0, 4])
+def test_config_parity_small(name, N, kernel):
+    """kernel 0: automatic (v5 for p <= 2 with the native rule), 4: v4 forced (FEA_TUNE_KERNEL)."""
     cfg = scaled(CONFIGS[name], N)
     w = make_workload(cfg)
     coef = coef_of(cfg)
     for u in w.u_sequence(min(cfg.reassemblies, 2)):
-        res = library_assemble(w.mesh, w.q_xy, w.q_w, u, cfg.p, coef, coef, which=cfg.which)
+        res = library_assemble(w.mesh, w.q_xy, w.q_w, u, cfg.p, coef, coef, which=cfg.which,
+                               tuning={2: kernel} if kernel else None)
+        assert res["ctx"].stat(11) == (5 if cfg.p <= 2 and kernel == 0 else 4)
         assert res["ctx"].stat(1) >= 2  # several blocks
         ref = oracle_for(w.mesh, w.q_xy, w.q_w, u, res["perm"], coef, coef, cfg.which)
         _check(res, ref, cfg.which)
@@ -86,9 +90,11 @@ def test_deterministic_across_runs_and_tilings(p):
     base = library_assemble(m, xy, w, u, p, coef, coef)
     again = library_assemble(m, xy, w, u, p, coef, coef)
     assert np.array_equal(base["M"], again["M"]) and np.array_equal(base["K"], again["K"])
-    budgets = {1: [24000, 40000], 2: [40000, 70000], 3: [100000, 150000], 4: [150000, 190000]}[p]
-    for b in budgets:
-        r = library_assemble(m, xy, w, u, p, coef, coef, tuning={1: b})
+    # smem budgets (v4 and v5) and element caps per block (v5, FEA_TUNE_EMAX = 3)
+    tunings = {1: [{1: 24000}, {3: 64}, {3: 120}], 2: [{1: 40000}, {3: 48}, {3: 120}],
+               3: [{1: 100000}, {1: 150000}], 4: [{1: 150000}, {1: 190000}]}[p]
+    for tu in tunings:
+        r = library_assemble(m, xy, w, u, p, coef, coef, tuning=tu)
         assert r["ctx"].stat(1) > max(1, base["ctx"].stat(1) // 2)  # a different, finer tiling
         assert np.array_equal(base["M"], r["M"]) and np.array_equal(base["K"], r["K"])
 
