@@ -37,7 +37,8 @@ def build(force: bool = False, verbose: bool = False) -> str:
     def compile_one(src):
         obj = os.path.join(OBJ, src + ".o")
         if src.endswith(".cu"):
-            cmd = [NVCC, "-O3", "-std=c++17", *ARCH, "-lineinfo", "-Xcompiler", "-fPIC", *inc, "-c",
+            diag = ["-DFEA5_DIAG"] if os.environ.get("FEA_BUILD_DIAG") else []
+            cmd = [NVCC, "-O3", "-std=c++17", *ARCH, "-lineinfo", "-Xcompiler", "-fPIC", *diag, *inc, "-c",
                    os.path.join(CSRC, src), "-o", obj]
         else:
             cmd = ["g++", "-O3", "-std=c++17", "-fPIC", "-Wall", "-Wno-unused-function", "-pthread",

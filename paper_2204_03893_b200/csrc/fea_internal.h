@@ -4,6 +4,9 @@
 #include <cstdint>
 
 #define FEA_MAX_ORDER 4
+#ifndef FEA5_NS2
+#define FEA5_NS2 2  // units per P2 tile in kernel v5 (column halves)
+#endif
 #define FEA_MAX_NP 15
 #define FEA_MAX_NQ 16
 #define FEA_MAX_PAR 16
@@ -87,7 +90,7 @@ __host__ __device__ constexpr int fea5_item_bytes(int C) {
 // NW warps per CTA (no producer warp), one CTA per SM, and the units per 32-element tile.
 __host__ __device__ constexpr int fea5_nw(int p) { return p == 1 ? 16 : 16; }
 __host__ __device__ constexpr int fea5_ctas(int p) { return 1; }
-__host__ __device__ constexpr int fea5_nsplit(int p) { return p == 2 ? 2 : 1; }  // units per tile
+__host__ __device__ constexpr int fea5_nsplit(int p) { return p == 2 ? FEA5_NS2 : 1; }  // units per tile
 __host__ __device__ constexpr int fea5_threads(int p) { return fea5_nw(p) * 32; }
 __host__ __device__ constexpr bool fea5_supported(int p, int nq) { return p <= 2 && nq == fea_nq_native(p); }
 // reference gradients in the kernel parameters: jtab[a][k][q] = d phi_k / d xhat_a at x_q

@@ -65,6 +65,9 @@ __global__ void __launch_bounds__(fea5_threads(P), 1) k_reassemble5(const __grid
     constexpr int DR = 8;                        // descriptor ring
     static_assert(2 * NP * NQ <= FEA_JTAB_MAX, "J tables exceed the parameter bank");
     static_assert(NS == 1 || NP == 6, "column halves are defined for P2");
+#ifdef FEA5_DIAG
+    if (prm.dbg_mode & 64) return;  // diagnostics: empty launch (fixed launch overhead)
+#endif
     const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
     const int vs = prm.e_max | 1;
     const int G = gridDim.x, b0 = blockIdx.x;
@@ -186,7 +189,9 @@ __global__ void __launch_bounds__(fea5_threads(P), 1) k_reassemble5(const __grid
             if constexpr (two_lam) return lc[q];
             else return lm[q];
         };
+#ifdef FEA5_DIAG
         if (prm.dbg_mode & 4) return;  // diagnostics: skip the contraction
+#endif
         // Contraction, column j of the symmetric element matrices at a time (rows i <= j):
         //   V_m[ij] = sum_q phi_i(x_q) y_jq,               y_jq = phi_j(x_q) Lambda_q
         //   V_c[ij] = sum_q sum_a J_ia(x_q) z_jqa,          z_jq = Lambda_q A_e J_j(x_q)^T
@@ -196,6 +201,13 @@ __global__ void __launch_bounds__(fea5_threads(P), 1) k_reassemble5(const __grid
         // operands stay compile-time constant-bank offsets.
         auto J = [&](int a, int k, int q) { return prm.jtab[(a * NP + k) * NQ + q]; };
         const uint32_t jset = fea5_jset(h);
+        double g00[NQ], g01[NQ], g11[NQ];  // Lambda_q A_e (the symmetric 2 x 2 per point)
+#pragma unroll
+        for (int q = 0; q < NQ; ++q) {
+            g00[q] = LC(q) * A00;
+            g01[q] = LC(q) * A01;
+            g11[q] = LC(q) * A11;
+        }
 #pragma unroll 1
         for (int jj = 0; jj < NJ; ++jj) {
             const int j = NS == 1 ? jj : (int)((jset >> (4 * jj)) & 15u);
@@ -205,8 +217,8 @@ __global__ void __launch_bounds__(fea5_threads(P), 1) k_reassemble5(const __grid
                 if (DO_M) y[q] = prm.ctab[j * NQ + q] * lm[q];
                 if (DO_C) {
                     const double j0 = J(0, j, q), j1 = J(1, j, q);
-                    z0[q] = LC(q) * fma(A00, j0, A01 * j1);
-                    z1[q] = LC(q) * fma(A01, j0, A11 * j1);
+                    z0[q] = fma(g00[q], j0, g01[q] * j1);
+                    z1[q] = fma(g01[q], j0, g11[q] * j1);
                 }
             }
 #pragma unroll
@@ -220,16 +232,21 @@ __global__ void __launch_bounds__(fea5_threads(P), 1) k_reassemble5(const __grid
                     sVm[t * vs + le] = m;
                 }
                 if (DO_C) {
-                    double c = 0.0;
+                    double c0 = 0.0, c1 = 0.0;  // two chains (ILP)
 #pragma unroll
-                    for (int q = 0; q < NQ; ++q) c = fma(J(0, i, q), z0[q], fma(J(1, i, q), z1[q], c));
-                    sVc[t * vs + le] = c;
+                    for (int q = 0; q < NQ; ++q) {
+                        c0 = fma(J(0, i, q), z0[q], c0);
+                        c1 = fma(J(1, i, q), z1[q], c1);
+                    }
+                    sVc[t * vs + le] = c0 + c1;
                 }
             }
         }
     };
 
-    // ---- diagnostics (FEA_DEBUG_TIMING / FEA_DEBUG_MODE): per-warp cycle split, CTA 0 trace
+    // ---- diagnostics, compiled in only with -DFEA5_DIAG (FEA_DEBUG_TIMING: per-warp cycle split;
+    // FEA_DEBUG_MODE & 8: CTA 0 event trace, & 32: per-CTA start/end)
+#ifdef FEA5_DIAG
     unsigned long long tacc[7] = {0, 0, 0, 0, 0, 0, 0};
     unsigned long long tcl = clock64();
     int nev = 0;
@@ -253,6 +270,9 @@ __global__ void __launch_bounds__(fea5_threads(P), 1) k_reassemble5(const __grid
             tcl = now;
         }
     };
+#else
+    auto tick = [](int) {};
+#endif
 
     // ---- prologue: DOFs of the first unit, then two units of gathers in flight
     Gath<NP> ga, gb;  // ga: the compute cursor's unit, gb: the one after it
@@ -304,13 +324,9 @@ __global__ void __launch_bounds__(fea5_threads(P), 1) k_reassemble5(const __grid
             mbar_wait(&recb[b], (uint32_t)((s1 >> 1) & 1));
             tick(3);
             const FeaBlock& bk = blk_of(s1);
-            if (!(prm.dbg_mode & 2)) {
+            {
                 double* om = DO_M ? prm.out_m + bk.slot0 : nullptr;
                 double* oc = DO_C ? prm.out_c + bk.slot0 : nullptr;
-                if (prm.dbg_mode & 1) {  // diagnostics: stores into this V buffer instead of the CSR
-                    om = DO_M ? sVm0 + b * vbuf : nullptr;
-                    oc = DO_C ? sVc0 + b * vbuf : nullptr;
-                }
                 phase_b5<DO_M, DO_C>(sRec0 + b * rec_stride, bk.ncls, sVm0 + b * vbuf, sVc0 + b * vbuf, om, oc, tid,
                                      NW * 32);
             }
@@ -320,6 +336,7 @@ __global__ void __launch_bounds__(fea5_threads(P), 1) k_reassemble5(const __grid
         }
     }
 
+#ifdef FEA5_DIAG
     if (prm.dbg && lane == 0)
         for (int i = 0; i < 7; ++i) atomicAdd(prm.dbg + i, tacc[i]);
     if ((prm.dbg_mode & 32) && prm.dbg && tid == 0 && blockIdx.x < 400) {  // per-CTA start / end
@@ -331,6 +348,7 @@ __global__ void __launch_bounds__(fea5_threads(P), 1) k_reassemble5(const __grid
         prm.dbg[201 + 3 * blockIdx.x] = t_end;
         prm.dbg[202 + 3 * blockIdx.x] = smid;
     }
+#endif
 }
 
 using kfun_t = void (*)(const FeaKParams);
