@@ -147,6 +147,22 @@ fea_status fea_reassemble(fea_ctx ctx, const double* u_owned, double* mass_vals,
  * (nnz_local each, may be NULL).  Synchronous. */
 fea_status fea_reassemble_host(fea_ctx ctx, const double* u_host, double* mass_host, double* stiff_host);
 
+/* Tensor contractions of the Newton Jacobian:
+ *   mt_vals <- (M o2 v)_{ik} = sum_e sum_q w_q m'(u_h(x_q)) phi_i phi_k v_h(x_q) |det B_e|
+ *              (mass tensor M_ijk = int m' phi_i phi_j phi_k contracted with v, PAPER.md:311;
+ *               symmetric)
+ *   ct_vals <- (C o2 v)_{ik} = sum_e sum_q w_q c'(u_h(x_q)) (J_q[i,:] A_e J_q^T v_e) phi_k |det B_e|
+ *              (conductivity tensor C_ijk = int c' grad phi_i . grad phi_j phi_k contracted in its
+ *               second mode; NONSYMMETRIC)
+ * m' and c' are the derivatives of the FEA_MASS / FEA_STIFF coefficients (fea_set_coefficient;
+ * PWL: the slope of the segment).  u_full, v_full: device, n_dof float64, library numbering.
+ * mt_vals / ct_vals: device, nnz_local float64 each, 16-byte aligned, either may be NULL; same
+ * pattern (fea_get_pattern) as the matrices.  The first call builds the tensor plan (host,
+ * synchronous); the assembly itself is asynchronous on the ctx stream.
+ * Errors: FEA_E_STATE (no pattern), FEA_E_ARG (NULL u/v, misalignment), FEA_E_UNSUPPORTED. */
+fea_status fea_assemble_tensor(fea_ctx ctx, const double* u_full, const double* v_full, double* mt_vals,
+                               double* ct_vals);
+
 /* Multi-GPU: the 128-byte ncclUniqueId.  Rank 0 calls fea_nccl_unique_id and broadcasts the
  * bytes (e.g. over a torch.distributed process group); every rank then calls fea_set_nccl. */
 fea_status fea_nccl_unique_id(void* id_out_128_bytes);

@@ -251,9 +251,12 @@ __device__ __forceinline__ uint32_t word_of(const uint4& w, int i) {
 template <typename W>
 __device__ __forceinline__ int u16_of(const W& w, int k) { return (word_of(w, k >> 1) >> (16 * (k & 1))) & 0xffff; }
 
-template <int C, bool DO_M, bool DO_C, int ILP>
+// ORIENT (tensor contractions): bit 15 of an offset selects sVd (entry (i, k) with local i > k)
+// over sVc for the nonsymmetric channel; the symmetric channel ignores it.
+template <int C, bool DO_M, bool DO_C, int ILP, bool ORIENT = false>
 __device__ __forceinline__ void items5(const uint8_t* __restrict__ base, int n, const double* __restrict__ sVm,
-                                       const double* __restrict__ sVc, double* om, double* oc, int tid, int nthr) {
+                                       const double* __restrict__ sVc, double* om, double* oc, int tid, int nthr,
+                                       const double* __restrict__ sVd = nullptr) {
     using W = typename ItemWord<fea5_item_bytes(C)>::T;
     const W* it = reinterpret_cast<const W*>(base);
     for (int i0 = tid; i0 < n; i0 += ILP * nthr) {
@@ -265,9 +268,10 @@ __device__ __forceinline__ void items5(const uint8_t* __restrict__ base, int n, 
         for (int u = 0; u < ILP; ++u)
 #pragma unroll
             for (int q = 0; q < C; ++q) {
-                const int off = u16_of(w[u], 1 + q);
+                const int raw = u16_of(w[u], 1 + q);
+                const int off = ORIENT ? (raw & 0x7fff) : raw;
                 if (DO_M) vm[u][q] = sVm[off];
-                if (DO_C) vc[u][q] = sVc[off];
+                if (DO_C) vc[u][q] = (ORIENT && (raw & 0x8000)) ? sVd[off] : sVc[off];
             }
 #pragma unroll
         for (int u = 0; u < ILP; ++u)
@@ -285,17 +289,19 @@ __device__ __forceinline__ void items5(const uint8_t* __restrict__ base, int n, 
     }
 }
 
-template <bool DO_M, bool DO_C>
+template <bool DO_M, bool DO_C, bool ORIENT = false>
 __device__ __forceinline__ void items5_generic(const uint8_t* __restrict__ base, int C, int n, int R,
                                                const double* __restrict__ sVm, const double* __restrict__ sVc,
-                                               double* om, double* oc, int tid, int nthr) {
+                                               double* om, double* oc, int tid, int nthr,
+                                               const double* __restrict__ sVd = nullptr) {
     for (int i = tid; i < n; i += nthr) {
         const uint16_t* w = reinterpret_cast<const uint16_t*>(base + (size_t)i * R);
         double am = 0.0, ac = 0.0;
         for (int q = 0; q < C; ++q) {
-            const int off = w[1 + q];
+            const int raw = w[1 + q];
+            const int off = ORIENT ? (raw & 0x7fff) : raw;
             if (DO_M) am += sVm[off];
-            if (DO_C) ac += sVc[off];
+            if (DO_C) ac += (ORIENT && (raw & 0x8000)) ? sVd[off] : sVc[off];
         }
         if (DO_M) om[w[0]] = am;
         if (DO_C) oc[w[0]] = ac;
@@ -303,22 +309,37 @@ __device__ __forceinline__ void items5_generic(const uint8_t* __restrict__ base,
 }
 
 // the classes of one block, threads tid of nthr (a block's B is split across all warps)
-template <bool DO_M, bool DO_C>
+template <bool DO_M, bool DO_C, bool ORIENT = false>
 __device__ __forceinline__ void phase_b5(const uint8_t* __restrict__ rec, int ncls, const double* __restrict__ sVm,
-                                         const double* __restrict__ sVc, double* om, double* oc, int tid, int nthr) {
+                                         const double* __restrict__ sVc, double* om, double* oc, int tid, int nthr,
+                                         const double* __restrict__ sVd = nullptr) {
     const int4* cls = reinterpret_cast<const int4*>(rec);
     for (int k = 0; k < ncls; ++k) {
         const int4 c = cls[k];  // {C, n_items, byte offset, item bytes}
         const uint8_t* base = rec + c.z;
         switch (c.x) {
-            case 1: items5<1, DO_M, DO_C, 4>(base, c.y, sVm, sVc, om, oc, tid, nthr); break;
-            case 2: items5<2, DO_M, DO_C, 4>(base, c.y, sVm, sVc, om, oc, tid, nthr); break;
-            case 3: items5<3, DO_M, DO_C, 2>(base, c.y, sVm, sVc, om, oc, tid, nthr); break;
-            case 4: items5<4, DO_M, DO_C, 2>(base, c.y, sVm, sVc, om, oc, tid, nthr); break;
-            case 6: items5<6, DO_M, DO_C, 2>(base, c.y, sVm, sVc, om, oc, tid, nthr); break;
-            default: items5_generic<DO_M, DO_C>(base, c.x, c.y, c.w, sVm, sVc, om, oc, tid, nthr);
+            case 1: items5<1, DO_M, DO_C, 4, ORIENT>(base, c.y, sVm, sVc, om, oc, tid, nthr, sVd); break;
+            case 2: items5<2, DO_M, DO_C, 4, ORIENT>(base, c.y, sVm, sVc, om, oc, tid, nthr, sVd); break;
+            case 3: items5<3, DO_M, DO_C, 2, ORIENT>(base, c.y, sVm, sVc, om, oc, tid, nthr, sVd); break;
+            case 4: items5<4, DO_M, DO_C, 2, ORIENT>(base, c.y, sVm, sVc, om, oc, tid, nthr, sVd); break;
+            case 6: items5<6, DO_M, DO_C, 2, ORIENT>(base, c.y, sVm, sVc, om, oc, tid, nthr, sVd); break;
+            default: items5_generic<DO_M, DO_C, ORIENT>(base, c.x, c.y, c.w, sVm, sVc, om, oc, tid, nthr, sVd);
         }
     }
+}
+
+// derivative k'(u) of the coefficient (fea.h FEA_K_*); PWL: slope of the segment of u
+__device__ __forceinline__ double dkeval(const FeaCoef& c, double u) {
+    if (c.kind == 0) {
+        double r = 0.0;
+        for (int i = c.npar - 1; i >= 1; --i) r = fma(r, u, (double)i * c.par[i]);
+        return r;
+    }
+    if (c.kind == 1) return c.par[0] * c.par[1] * exp(c.par[1] * u);
+    const int m = c.npar / 2;
+    int s = 0;
+    while (s < m - 2 && u > c.par[2 * (s + 1)]) ++s;
+    return (c.par[2 * s + 3] - c.par[2 * s + 1]) / (c.par[2 * s + 2] - c.par[2 * s]);
 }
 
 // L2 prefetch of a byte range (bulk, no completion tracking); bytes a multiple of 16

@@ -78,6 +78,7 @@ struct fea_ctx_s {
     // reference element
     int order = 0, np = 0, nq = 0, T = 0;
     std::vector<double> qxy, qw, tables, qfrag, jplain;  // tables = Phi, w; jplain = J (kernel parameters)
+    double* d_ttab = nullptr;                             // tensor kernel: Phi, J0, J1 [np][16], w [16]
 
     // mesh, library numbering
     bool have_mesh = false;
@@ -104,6 +105,14 @@ struct fea_ctx_s {
     int64_t record_bytes = 0;
     int64_t stat_visits = 0, stat_owned = 0, stat_entries = 0;
     int launches_per_call = 1;
+
+    // tensor-contraction plan (built on the first fea_assemble_tensor)
+    bool have_tplan = false;
+    FeaBlock* dt_blocks = nullptr;
+    uint8_t* dt_records = nullptr;
+    int32_t* dt_dofs = nullptr;
+    int t_nblocks = 0, t_emax = 0, t_smem = 0, t_grid = 0;
+    int32_t t_lay[FEA_LT_N] = {0};
 
     // coefficients
     FeaCoef coef_m{}, coef_c{};
@@ -134,6 +143,10 @@ struct fea_ctx_s {
         dfree(d_blocks);
         dfree(d_records);
         dfree(d_dofs);
+        dfree(dt_blocks);
+        dfree(dt_records);
+        dfree(dt_dofs);
+        have_tplan = false;
         dfree(d_vm);
         dfree(d_vc);
         row_ptr.clear();
@@ -359,6 +372,7 @@ void fea_destroy(fea_ctx c) {
     if (!c->host_only) cudaSetDevice(c->device);
     c->free_mesh();
     dfree(c->d_tables);
+    dfree(c->d_ttab);
     dfree(c->d_dbg);
     if (c->comm && nccl().ok) nccl().commDestroy((ncclComm_t)c->comm);
     delete c;
@@ -397,6 +411,21 @@ fea_status fea_set_element(fea_ctx c, int order, int n_q, const double* q_xy, co
     if (c->host_only) return FEA_OK;
     FEA_CUDA(c, cudaMalloc(&c->d_tables, qfrag.size() * sizeof(double)));
     FEA_CUDA(c, cudaMemcpy(c->d_tables, qfrag.data(), qfrag.size() * sizeof(double), cudaMemcpyHostToDevice));
+    {  // tensor kernel tables: Phi, J0, J1 [np][16], w [16], zero padded
+        const int np = c->np;
+        std::vector<double> tt((size_t)3 * np * 16 + 16, 0.0);
+        for (int i = 0; i < np; ++i)
+            for (int q = 0; q < n_q; ++q) {
+                tt[(size_t)i * 16 + q] = ctab[(size_t)i * n_q + q];
+                tt[(size_t)(np + i) * 16 + q] = jplain[(size_t)i * n_q + q];
+                tt[(size_t)(2 * np + i) * 16 + q] = jplain[(size_t)(np + i) * n_q + q];
+            }
+        const size_t oW = ((size_t)np * n_q + 1) & ~size_t(1);
+        for (int q = 0; q < n_q; ++q) tt[(size_t)3 * np * 16 + q] = ctab[oW + q];
+        dfree(c->d_ttab);
+        FEA_CUDA(c, cudaMalloc(&c->d_ttab, tt.size() * sizeof(double)));
+        FEA_CUDA(c, cudaMemcpy(c->d_ttab, tt.data(), tt.size() * sizeof(double), cudaMemcpyHostToDevice));
+    }
     return FEA_OK;
 }
 
@@ -537,47 +566,26 @@ fea_status fea_set_tuning(fea_ctx c, int key, int64_t value) {
     return FEA_OK;
 }
 
-fea_status fea_build_pattern(fea_ctx c, int64_t* row_begin, int64_t* n_rows_local, int64_t* nnz_local) {
-    if (!c) return FEA_E_ARG;
-    if (!c->have_mesh) return c->fail(FEA_E_STATE, "build_pattern before mesh_upload");
-    if (!c->host_only) cudaSetDevice(c->device);
-    c->free_plan();
-    const int np = c->np, T = c->T, nq = c->nq;
-    const int64_t n_e = c->n_e, n_dof = c->n_dof;
-    const int64_t rpr = (n_dof + c->world - 1) / c->world;
-    const int64_t R0 = std::min<int64_t>(n_dof, rpr * c->rank), R1 = std::min<int64_t>(n_dof, R0 + rpr);
-    const int64_t nr = R1 - R0;
-    c->rows_per_rank = rpr;
-    c->row_begin = R0;
-    c->n_rows = nr;
+// Host plan of one kernel family: row blocks of this rank's rows, each with its element set
+// (ghosts first), its CSR slots and the per-slot contributor lists (ascending library element),
+// encoded as the kernel's block record.  v5 = class/item record + separate DOF array; else the
+// v4 record (DOFs inside).  orient: bit 15 of each contributor offset = (local i > local j), for
+// nonsymmetric element matrices (the tensor contraction C o2 v).
+struct PlanData {
+    std::vector<FeaBlock> blocks;
+    std::vector<uint8_t> records;
+    std::vector<int32_t> dofs;
+    std::vector<int64_t> row_ptr;
+    std::vector<int32_t> col_idx;
+    int64_t nnz = 0, rec_max = 16, visits = 0, owned = 0, ncon = 0, rbytes = 0;
+};
 
-    // ---- shared-memory budget -> elements per block (e_max) and record budget
-    const int dm = (c->plan_which & FEA_MASS) ? 1 : 0, dcm = (c->plan_which & FEA_STIFF) ? 1 : 0;
-    const int nmat = dm + dcm;
-    const bool v5 = fea5_supported(c->order, nq) && c->tune_kver != 4;
-    c->kver = v5 ? 5 : 4;
-    const int rstages = c->order <= 2 ? 3 : 2;  // fea_rstages (v4)
-    int64_t e_max, rec_budget;
-    if (v5) {
-        // two V_m, V_c [T][e_max | 1] buffers + two record stages in 227 KiB (one CTA per SM)
-        const int64_t budget = c->tune_smem ? c->tune_smem : 227 * 1024;
-        const double rec_el = 1.1 * 2.0 * np * np + 8;  // record bytes per element (estimate)
-        e_max = (int64_t)((budget - 1024) / (2 * (8.0 * T * nmat + rec_el)));
-        if (c->tune_emax) e_max = std::min(e_max, c->tune_emax);
-        e_max = std::min<int64_t>(e_max, 65535 / T - 1) / 8 * 8;
-        rec_budget = ((budget - 1024 - 2 * 8LL * T * nmat * (e_max | 1)) / 2 - 128) & ~int64_t(15);
-    } else {
-        const int ctas = c->order <= 2 ? 2 : 1;  // fea_ctas
-        const int64_t budget = c->tune_smem ? c->tune_smem : (ctas == 2 ? 113 * 1024 : 226 * 1024);
-        const int nqp = 4 * fea_nk_kernel(c->order, nq);
-        const int64_t per_el_smem = 8LL * T * nmat + 2 * (8LL * np + 48) + 2 * 8LL * nqp + 32;
-        const double rec_el = 1.3 * (3.0 * np * np + 4.0 * np) + 8;  // record bytes per element (estimate)
-        e_max = (int64_t)((budget - 256 - 3 * 128) / (per_el_smem + rstages * rec_el));
-        e_max = std::min<int64_t>(e_max, 65535 / T);
-        e_max = e_max >= 8 ? ((e_max - 8) / 16) * 16 + 8 : 0;  // multiple of 8, == 8 mod 16
-        rec_budget = ((int64_t)(rec_el * e_max) + 15) & ~int64_t(15);
-    }
-
+static fea_status build_blocks(fea_ctx c, bool v5, bool orient, int64_t e_max, int64_t rec_budget, int64_t EM,
+                               PlanData& P) {
+    const int np = c->np, T = c->T;
+    const int64_t n_e = c->n_e;
+    const int64_t R0 = c->row_begin, nr = c->n_rows;
+    const int64_t R1 = R0 + nr;
     // ---- incidence of this rank's rows (ascending library element per row)
     std::vector<int64_t> iptr(nr + 1, 0);
     for (int64_t e = 0; e < n_e; ++e)
@@ -602,6 +610,8 @@ fea_status fea_build_pattern(fea_ctx c, int64_t* row_begin, int64_t* n_rows_loca
     const int64_t row_ub_max = max_inc * np * 4 + 4 * np * (max_inc + 3) + 12 * FEA_MAX_CLASSES + 64;
     if (e_max < std::max<int64_t>(max_inc, 1) || rec_budget < row_ub_max)
         return c->fail(FEA_E_UNSUPPORTED, "shared-memory budget too small: %lld elements per block", (long long)e_max);
+    if (orient && (int64_t)T * EM >= 32768)
+        return c->fail(FEA_E_UNSUPPORTED, "tensor plan: V offsets need 15 bits");
 
     // ---- greedy row blocks: elements <= e_max and record upper bound <= rec_budget
     // record upper bound: slots <= entries, so counts + contrib + chunks <= 3 entries + entries/8
@@ -640,7 +650,6 @@ fea_status fea_build_pattern(fea_ctx c, int64_t* row_begin, int64_t* n_rows_loca
         std::string err;
     };
     std::vector<BOut> bo(nb);
-    const int64_t EM = v5 ? (e_max | 1) : e_max;  // V row stride (v5: odd, fea_kernels5.cu)
     parallel_for(nb, [&](int64_t b) {
         BOut& o = bo[b];
         const int64_t ra = brow[b], rb = brow[b + 1];
@@ -650,14 +659,15 @@ fea_status fea_build_pattern(fea_ctx c, int64_t* row_begin, int64_t* n_rows_loca
         std::sort(E.begin(), E.end());
         E.erase(std::unique(E.begin(), E.end()), E.end());
         for (int32_t e : E) (c->elem_min[e] < ga ? o.nghost : o.nown)++;
-        struct Rec { int32_t row, col, le, t; };
+        struct Rec { int32_t row, col, le, t; };  // t: symmetric row (| 0x8000 if orient and i > j)
         std::vector<Rec> recs;
         for (int64_t le = 0; le < (int64_t)E.size(); ++le) {
             const int32_t* d = &c->ed[(size_t)E[le] * np];
             for (int i = 0; i < np; ++i) {
                 if (d[i] < ga || d[i] >= gb) continue;
                 for (int j = 0; j < np; ++j)
-                    recs.push_back({d[i], d[j], (int32_t)le, tri_index(np, std::min(i, j), std::max(i, j))});
+                    recs.push_back({d[i], d[j], (int32_t)le, tri_index(np, std::min(i, j), std::max(i, j)) |
+                                                                 (orient && i > j ? 0x10000 : 0)});
             }
         }
         // stable: within a (row, col) slot the contributors stay in ascending le (= library element)
@@ -698,7 +708,7 @@ fea_status fea_build_pattern(fea_ctx c, int64_t* row_begin, int64_t* n_rows_loca
             }
             items[it] = (uint16_t)sl;
             for (int32_t m = sstart[sl]; m < sstart[sl] + scount[sl]; ++m)
-                contrib.push_back((uint16_t)(recs[m].t * EM + recs[m].le));
+                contrib.push_back((uint16_t)(((recs[m].t & 0xffff) * EM + recs[m].le) | ((recs[m].t >> 16) << 15)));
         }
         FeaBlock& F = o.fb;
         F.nslots = nslot;
@@ -780,22 +790,91 @@ fea_status fea_build_pattern(fea_ctx c, int64_t* row_begin, int64_t* n_rows_loca
         rec_max = std::max<int64_t>(rec_max, B.rec_bytes);
     }
     if (nnz >= (1ll << 31)) return c->fail(FEA_E_UNSUPPORTED, "nnz %lld >= 2^31 on one rank", (long long)nnz);
-    c->row_ptr.assign(nr + 1, 0);
-    c->col_idx.resize(nnz);
+    std::vector<int64_t>& row_ptr = P.row_ptr;
+    std::vector<int32_t>& col_idx = P.col_idx;
+    row_ptr.assign(nr + 1, 0);
+    col_idx.resize(nnz);
     std::vector<uint8_t> records(std::max<int64_t>(rbytes, 16));
     std::vector<int32_t> alldofs(std::max<int64_t>(ndofs, 4));
     parallel_for(nb, [&](int64_t b) {
         const FeaBlock& B = blocks[b];
         std::copy(bo[b].dofs.begin(), bo[b].dofs.end(), alldofs.begin() + B.dof_off);
         std::vector<int32_t>().swap(bo[b].dofs);
-        std::copy(bo[b].cols.begin(), bo[b].cols.end(), c->col_idx.begin() + B.slot0);
+        std::copy(bo[b].cols.begin(), bo[b].cols.end(), col_idx.begin() + B.slot0);
         std::memcpy(records.data() + B.rec_off, bo[b].rec.data(), B.rec_bytes);
-        for (int64_t r = brow[b]; r < brow[b + 1]; ++r) c->row_ptr[r + 1] = bo[b].rownnz[r - brow[b]];
+        for (int64_t r = brow[b]; r < brow[b + 1]; ++r) row_ptr[r + 1] = bo[b].rownnz[r - brow[b]];
         std::vector<uint8_t>().swap(bo[b].rec);
     });
-    for (int64_t r = 0; r < nr; ++r) c->row_ptr[r + 1] += c->row_ptr[r];
+    for (int64_t r = 0; r < nr; ++r) row_ptr[r + 1] += row_ptr[r];
     bo.clear();
+    P.blocks.swap(blocks);
+    P.records.swap(records);
+    P.dofs.swap(alldofs);
+    P.nnz = nnz;
+    P.rec_max = rec_max;
+    P.visits = visits;
+    P.owned = owned;
+    P.ncon = ncon;
+    P.rbytes = rbytes;
+    return FEA_OK;
+}
 
+
+fea_status fea_build_pattern(fea_ctx c, int64_t* row_begin, int64_t* n_rows_local, int64_t* nnz_local) {
+    if (!c) return FEA_E_ARG;
+    if (!c->have_mesh) return c->fail(FEA_E_STATE, "build_pattern before mesh_upload");
+    if (!c->host_only) cudaSetDevice(c->device);
+    c->free_plan();
+    const int np = c->np, T = c->T, nq = c->nq;
+    const int64_t n_dof = c->n_dof;
+    const int64_t rpr = (n_dof + c->world - 1) / c->world;
+    const int64_t R0 = std::min<int64_t>(n_dof, rpr * c->rank), R1 = std::min<int64_t>(n_dof, R0 + rpr);
+    const int64_t nr = R1 - R0;
+    c->rows_per_rank = rpr;
+    c->row_begin = R0;
+    c->n_rows = nr;
+
+    // ---- shared-memory budget -> elements per block (e_max) and record budget
+    const int dm = (c->plan_which & FEA_MASS) ? 1 : 0, dcm = (c->plan_which & FEA_STIFF) ? 1 : 0;
+    const int nmat = dm + dcm;
+    const bool v5 = fea5_supported(c->order, nq) && c->tune_kver != 4;
+    c->kver = v5 ? 5 : 4;
+    const int rstages = c->order <= 2 ? 3 : 2;  // fea_rstages (v4)
+    int64_t e_max, rec_budget;
+    if (v5) {
+        // two V_m, V_c [T][e_max | 1] buffers + two record stages in 227 KiB (one CTA per SM)
+        const int64_t budget = c->tune_smem ? c->tune_smem : 227 * 1024;
+        const double rec_el = 1.1 * 2.0 * np * np + 8;  // record bytes per element (estimate)
+        e_max = (int64_t)((budget - 1024) / (2 * (8.0 * T * nmat + rec_el)));
+        if (c->tune_emax) e_max = std::min(e_max, c->tune_emax);
+        e_max = std::min<int64_t>(e_max, 65535 / T - 1) / 8 * 8;
+        rec_budget = ((budget - 1024 - 2 * 8LL * T * nmat * (e_max | 1)) / 2 - 128) & ~int64_t(15);
+    } else {
+        const int ctas = c->order <= 2 ? 2 : 1;  // fea_ctas
+        const int64_t budget = c->tune_smem ? c->tune_smem : (ctas == 2 ? 113 * 1024 : 226 * 1024);
+        const int nqp = 4 * fea_nk_kernel(c->order, nq);
+        const int64_t per_el_smem = 8LL * T * nmat + 2 * (8LL * np + 48) + 2 * 8LL * nqp + 32;
+        const double rec_el = 1.3 * (3.0 * np * np + 4.0 * np) + 8;  // record bytes per element (estimate)
+        e_max = (int64_t)((budget - 256 - 3 * 128) / (per_el_smem + rstages * rec_el));
+        e_max = std::min<int64_t>(e_max, 65535 / T);
+        e_max = e_max >= 8 ? ((e_max - 8) / 16) * 16 + 8 : 0;  // multiple of 8, == 8 mod 16
+        rec_budget = ((int64_t)(rec_el * e_max) + 15) & ~int64_t(15);
+    }
+
+    const int64_t EM = v5 ? (e_max | 1) : e_max;  // V row stride (v5: odd, fea_kernels5.cu)
+    PlanData P;
+    {
+        const fea_status st = build_blocks(c, v5, false, e_max, rec_budget, EM, P);
+        if (st != FEA_OK) return st;
+    }
+    const int64_t nb = (int64_t)P.blocks.size();
+    const int64_t nnz = P.nnz, rec_max = P.rec_max;
+    c->row_ptr.swap(P.row_ptr);
+    c->col_idx.swap(P.col_idx);
+    std::vector<FeaBlock>& blocks = P.blocks;
+    std::vector<uint8_t>& records = P.records;
+    std::vector<int32_t>& alldofs = P.dofs;
+    const int64_t visits = P.visits, owned = P.owned, ncon = P.ncon, rbytes = P.rbytes;
     int32_t L[FEA_L_N];
     if (v5) fea5_smem_layout(L, (int)rec_max, (int)e_max, c->order, dm, dcm);
     else fea_smem_layout(L, rstages, (int)rec_max, (int)e_max, c->order, nq, dm, dcm);
@@ -993,6 +1072,75 @@ fea_status fea_reassemble_host(fea_ctx c, const double* u_host, double* mass_hos
     if (mass_host) FEA_CUDA(c, cudaMemcpyAsync(mass_host, c->d_vm, c->nnz * sizeof(double), cudaMemcpyDeviceToHost, c->stream));
     if (stiff_host) FEA_CUDA(c, cudaMemcpyAsync(stiff_host, c->d_vc, c->nnz * sizeof(double), cudaMemcpyDeviceToHost, c->stream));
     FEA_CUDA(c, cudaStreamSynchronize(c->stream));
+    return FEA_OK;
+}
+
+// Tensor plan: same rows as the matrix plan, v5 record format with orientation bits, blocks sized
+// for V1 + Vup + Vdn (3 T doubles per element) in one CTA per SM.
+static fea_status build_tensor_plan(fea_ctx c) {
+    const int np = c->np, T = c->T;
+    const int64_t budget = 227 * 1024;
+    const int64_t tabs = 8LL * (3 * np * 16 + 16) + 256;
+    const double rec_el = 1.1 * 2.0 * np * np + 8;
+    int64_t e_max = (int64_t)((budget - tabs - 1024) / (3 * 8.0 * T + rec_el));
+    e_max = std::min<int64_t>(e_max, 32767 / T - 1) / 8 * 8;
+    const int64_t rec_budget = (budget - tabs - 1024 - 3 * 8LL * T * (e_max | 1)) & ~int64_t(15);
+    PlanData P;
+    const fea_status st = build_blocks(c, true, true, e_max, rec_budget, e_max | 1, P);
+    if (st != FEA_OK) return st;
+    if (P.nnz != c->nnz || P.row_ptr != c->row_ptr) return c->fail(FEA_E_STATE, "tensor plan: pattern mismatch");
+    const int64_t nb = (int64_t)P.blocks.size();
+    fea_t_smem_layout(c->t_lay, (int)P.rec_max, (int)e_max, c->order);
+    c->t_nblocks = (int)nb;
+    c->t_emax = (int)e_max;
+    c->t_smem = c->t_lay[FEA_LT_TOTAL];
+    FEA_CUDA(c, cudaMalloc((void**)&c->dt_blocks, std::max<int64_t>(nb, 1) * sizeof(FeaBlock)));
+    if (nb) FEA_CUDA(c, cudaMemcpy(c->dt_blocks, P.blocks.data(), nb * sizeof(FeaBlock), cudaMemcpyHostToDevice));
+    FEA_CUDA(c, cudaMalloc((void**)&c->dt_records, P.records.size()));
+    FEA_CUDA(c, cudaMemcpy(c->dt_records, P.records.data(), P.records.size(), cudaMemcpyHostToDevice));
+    FEA_CUDA(c, cudaMalloc((void**)&c->dt_dofs, P.dofs.size() * sizeof(int32_t)));
+    FEA_CUDA(c, cudaMemcpy(c->dt_dofs, P.dofs.data(), P.dofs.size() * sizeof(int32_t), cudaMemcpyHostToDevice));
+    int occ = 0, thr = 0;
+    const int rc = fea_tensor_occupancy(c->order, c->t_smem, &occ, &thr);
+    if (rc != 0) return c->fail(FEA_E_CUDA, "tensor occupancy: %s", cudaGetErrorString((cudaError_t)rc));
+    if (occ < 1) return c->fail(FEA_E_UNSUPPORTED, "tensor kernel does not fit: %d B shared memory", c->t_smem);
+    c->t_grid = (int)std::min<int64_t>(std::max<int64_t>(nb, 1), (int64_t)occ * c->sm_count);
+    c->have_tplan = true;
+    return FEA_OK;
+}
+
+fea_status fea_assemble_tensor(fea_ctx c, const double* u_full, const double* v_full, double* mt_vals, double* ct_vals) {
+    if (!c) return FEA_E_ARG;
+    if (c->host_only) return c->fail(FEA_E_STATE, "host-only (planning) context has no device");
+    if (!c->have_plan) return c->fail(FEA_E_STATE, "assemble_tensor before build_pattern");
+    if (!u_full || !v_full) return c->fail(FEA_E_ARG, "u_full / v_full is NULL");
+    if ((mt_vals && ((uintptr_t)mt_vals & 15)) || (ct_vals && ((uintptr_t)ct_vals & 15)))
+        return c->fail(FEA_E_ARG, "vals must be 16-byte aligned");
+    if (!mt_vals && !ct_vals) return FEA_OK;
+    cudaSetDevice(c->device);
+    if (!c->have_tplan) {
+        const fea_status st = build_tensor_plan(c);
+        if (st != FEA_OK) return st;
+    }
+    if (c->t_nblocks == 0) return FEA_OK;
+    FeaTParams prm{};
+    prm.blocks = c->dt_blocks;
+    prm.records = c->dt_records;
+    prm.dofs = c->dt_dofs;
+    prm.xy = c->d_xy;
+    prm.u = u_full;
+    prm.v = v_full;
+    prm.tab = c->d_ttab;
+    prm.out_m = mt_vals;
+    prm.out_c = ct_vals;
+    prm.nblocks = c->t_nblocks;
+    prm.e_max = c->t_emax;
+    prm.nq = c->nq;
+    std::memcpy(prm.lay, c->t_lay, sizeof(prm.lay));
+    prm.coef_m = c->coef_m;
+    prm.coef_c = c->coef_c;
+    const int rc = fea_launch_tensor(prm, c->order, c->t_smem, c->t_grid, c->stream);
+    if (rc != 0) return c->fail(FEA_E_CUDA, "k_tensor launch: %s", cudaGetErrorString((cudaError_t)rc));
     return FEA_OK;
 }
 

@@ -168,6 +168,44 @@ struct FeaKParams {
     double jtab[FEA_JTAB_MAX];  // v5: J [2][np][nq] (constant-bank DFMA operands)
 };
 
+// ---- tensor contractions (NEXT-1 / NEXT-2; kernel fea_kernels_t.cu)
+// Plan: v5 record format with orientation bits (bit 15 of a contributor offset = local i > j).
+// Shared memory: V1 [T][vs] (M o2 v, symmetric), Vup / Vdn [T][vs] (C o2 v: entries (i, k) with
+// i <= k / i > k, indexed by the symmetric row of (min, max)), one record stage, reference tables
+// (Phi [np][16], J [2][np][16], w [16]), mbarrier.
+enum { FEA_LT_V1 = 0, FEA_LT_VUP = 1, FEA_LT_VDN = 2, FEA_LT_REC = 3, FEA_LT_TAB = 4, FEA_LT_BAR = 5,
+       FEA_LT_TOTAL = 6, FEA_LT_N = 8 };
+#define FEA_T_WARPS 8
+__host__ __device__ inline void fea_t_smem_layout(int32_t* L, int rec_max, int e_max, int p) {
+    const int T = fea_T(p), np = fea_np(p), vs = e_max | 1;
+    int32_t o = 0;
+    L[FEA_LT_V1] = o; o += 8 * T * vs;
+    L[FEA_LT_VUP] = o; o += 8 * T * vs;
+    L[FEA_LT_VDN] = o; o += 8 * T * vs;
+    o = (o + 127) / 128 * 128;
+    L[FEA_LT_REC] = o; o += (rec_max + 127) / 128 * 128;
+    L[FEA_LT_TAB] = o; o += 8 * (3 * np * 16 + 16);
+    L[FEA_LT_BAR] = o; o += 16;
+    L[FEA_LT_TOTAL] = o;
+    L[7] = 0;
+}
+struct FeaTParams {
+    const FeaBlock* blocks;
+    const uint8_t* records;
+    const int32_t* dofs;
+    const double2* xy;
+    const double* u;      // u_full (k'(u_h) at the quadrature points)
+    const double* v;      // the contracted vector v (library numbering)
+    const double* tab;    // Phi [np][16], J [2][np][16], w [16] (zero padded)
+    double* out_m;        // (M o2 v) values or nullptr
+    double* out_c;        // (C o2 v) values or nullptr
+    int32_t nblocks, e_max, nq, pad_;
+    int32_t lay[FEA_LT_N];
+    FeaCoef coef_m, coef_c;  // k' of these
+};
+int fea_launch_tensor(const FeaTParams& prm, int order, int smem_bytes, int grid, void* stream);
+int fea_tensor_occupancy(int order, int smem_bytes, int* ctas_per_sm, int* threads);
+
 // Launch the fused reassembly kernel (defined in fea_kernels.cu).  Returns a cudaError_t.
 int fea_launch_reassemble(const FeaKParams& prm, int order, int smem_bytes, int grid, void* stream);
 // Per-SM CTA occupancy of the kernel variant and its block size (threads).

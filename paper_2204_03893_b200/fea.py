@@ -26,7 +26,7 @@ FEA_TUNE_SMEM_BUDGET, FEA_TUNE_KERNEL, FEA_TUNE_EMAX, FEA_TUNE_PLAN_WHICH = 1, 2
 SYMBOLS = ["fea_create", "fea_set_element", "fea_mesh_upload", "fea_set_tuning", "fea_build_pattern",
            "fea_get_pattern", "fea_get_dof_perm", "fea_get_elem_perm", "fea_set_coefficient",
            "fea_assemble_mass", "fea_assemble_stiffness", "fea_assemble", "fea_reassemble",
-           "fea_reassemble_host", "fea_nccl_unique_id", "fea_set_nccl", "fea_sync", "fea_get_stat",
+           "fea_reassemble_host", "fea_assemble_tensor", "fea_nccl_unique_id", "fea_set_nccl", "fea_sync", "fea_get_stat",
            "fea_last_error", "fea_destroy"]
 
 
@@ -63,6 +63,7 @@ def load_library():
         "fea_assemble": [P, P, P, P],
         "fea_reassemble": [P, P, P, P],
         "fea_reassemble_host": [P, P, P, P],
+        "fea_assemble_tensor": [P, P, P, P, P],
         "fea_nccl_unique_id": [P],
         "fea_set_nccl": [P, P],
         "fea_sync": [P],
@@ -208,6 +209,13 @@ class Context:
         self._check(self._lib.fea_reassemble(self._h, _dev_ptr(u_owned, "u_owned", self.n_rows),
                                              _dev_ptr(mass_vals, "mass_vals", self.nnz),
                                              _dev_ptr(stiff_vals, "stiff_vals", self.nnz)))
+
+    def assemble_tensor(self, u_full, v_full, mt_vals=None, ct_vals=None):
+        """(M o2 v) into mt_vals and (C o2 v) into ct_vals (NEXT-1 / NEXT-2)."""
+        self._check(self._lib.fea_assemble_tensor(self._h, _dev_ptr(u_full, "u_full", self.n_dof),
+                                                  _dev_ptr(v_full, "v_full", self.n_dof),
+                                                  _dev_ptr(mt_vals, "mt_vals", self.nnz),
+                                                  _dev_ptr(ct_vals, "ct_vals", self.nnz)))
 
     def reassemble_host(self, u_host, mass_host=None, stiff_host=None):
         """Host buffers (numpy float64; pinned torch CPU tensors also accepted via .numpy())."""
