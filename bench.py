@@ -128,7 +128,7 @@ def workload_desc(cfg, wl):
             "reorder": "morton" if cfg.reorder else "none"}
 
 
-def cpu_oracle_run(wl, cfg, target_s: float, nthreads: int, lib_to_user=None):
+def cpu_oracle_run(wl, cfg, target_s: float, nthreads: int, lib_to_user=None, tensor: bool = False):
     """Time the oracle (Algorithm 1, as it stands) on a bounded sample: whole reassemblies of the
     workload if one takes < target_s, else a leading block of rows.  Returns (entries/s, desc)."""
     import oracle
@@ -143,6 +143,17 @@ def cpu_oracle_run(wl, cfg, target_s: float, nthreads: int, lib_to_user=None):
     else:
         u = wl.u0
     coef = (cfg.k_kind, tuple(cfg.k_par))
+    if tensor:  # the oracle's tensor contraction (single-threaded: it has no OpenMP path)
+        v = np.full_like(u, 0.01)
+        nthreads = 1
+
+        def run(r1, pat):
+            oracle.assemble_tensor_contraction(m, wl.q_xy, wl.q_w, u, v, m_coef=coef if cfg.which & MASS else None,
+                                               c_coef=coef if cfg.which & STIFF else None, r0=0, r1=r1, pat=pat)
+    else:
+        def run(r1, pat):
+            oracle.assemble(m, wl.q_xy, wl.q_w, u, m_coef=coef, c_coef=coef, which=cfg.which, r0=0, r1=r1,
+                            nthreads=nthreads, pat=pat)
     n_p = cfg.n_p
     nmat = cfg.n_matrices
     # sample rows [0, r1): grow until the estimated time reaches target_s
@@ -150,8 +161,7 @@ def cpu_oracle_run(wl, cfg, target_s: float, nthreads: int, lib_to_user=None):
     while True:
         pat = oracle.pattern(m.n_dof, m.elem_dof, 0, r1)
         t0 = time.perf_counter()
-        oracle.assemble(m, wl.q_xy, wl.q_w, u, m_coef=coef, c_coef=coef, which=cfg.which, r0=0, r1=r1,
-                        nthreads=nthreads, pat=pat)
+        run(r1, pat)
         dt = time.perf_counter() - t0
         if r1 >= m.n_dof or dt >= 0.25 * target_s:
             break
@@ -159,8 +169,7 @@ def cpu_oracle_run(wl, cfg, target_s: float, nthreads: int, lib_to_user=None):
     reps = max(1, int(target_s / max(dt, 1e-6)))
     t0 = time.perf_counter()
     for _ in range(reps):
-        oracle.assemble(m, wl.q_xy, wl.q_w, u, m_coef=coef, c_coef=coef, which=cfg.which, r0=0, r1=r1,
-                        nthreads=nthreads, pat=pat)
+        run(r1, pat)
     dt = (time.perf_counter() - t0) / reps
     # entries attributable to the sampled rows: local entries whose row lies in [0, r1)
     ed = m.elem_dof
@@ -235,8 +244,21 @@ def run_ours(args):
         if world > 1:
             torch.distributed.barrier()
 
+    tensor = args.op == "tensor"
+    if tensor:  # NEXT-1/2: (M o2 v), (C o2 v) at u = u_r, v = u_{r+1} - u_r (a Newton direction)
+        if world > 1:
+            raise SystemExit("--op tensor is single-GPU")
+        vs = [us[(i + 1) % R] - us[i % R] for i in range(R)]
+        mt = torch.empty(max(asm.nnz, 1), dtype=torch.float64, device=dev) if cfg.which & MASS else None
+        ct = torch.empty(max(asm.nnz, 1), dtype=torch.float64, device=dev) if cfg.which & STIFF else None
+
+        def step(i):
+            asm.ctx.assemble_tensor(us[i % R], vs[i % R], mt, ct)
+    else:
+        def step(i):
+            asm.reassemble(us[i % R])
     for i in range(args.warmup):
-        asm.reassemble(us[i % R])
+        step(i)
     torch.cuda.synchronize()
     ev = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)) for _ in range(args.steps)]
     sampler = ClockSampler(local)
@@ -249,7 +271,7 @@ def run_ours(args):
                 if clean is not None:
                     clean.sum()
             ev[i][0].record(stream)
-            asm.reassemble(us[i % R])
+            step(i)
             ev[i][1].record(stream)
         torch.cuda.synchronize()
     barrier()
@@ -267,19 +289,21 @@ def run_ours(args):
     rp, _ = asm.pattern()
     nnz_local = asm.nnz
     if world == 1:
-        B = canonical_bytes(m.n_v, m.n_e, cfg.n_p, m.n_dof, nnz_local, nmat)
+        B = canonical_bytes(m.n_v, m.n_e, cfg.n_p, m.n_dof, nnz_local, nmat) + (8 * m.n_dof if tensor else 0)
     else:  # per-rank share of the canonical bytes (rows owned)
         frac_rows = asm.n_rows / m.n_dof
         B = canonical_bytes(m.n_v, m.n_e, cfg.n_p, m.n_dof, 0, nmat) * frac_rows + 8 * nnz_local * nmat
     kern_ms = statistics.median(step_ms)
     achieved = B / (kern_ms * 1e-3) / 1e9
     traffic = None
-    prof = os.path.join(ROOT, "profiles", f"ncu_traffic_{cfg.name}.json")
-    if os.path.exists(prof):
+    kname = "k_tensor" if tensor else ("k_reassemble5" if asm.ctx.stat(11) == 5 else "k_reassemble")
+    prof = os.path.join(ROOT, "profiles", f"ncu_traffic_{cfg.name}_{kname}.json")
+    if os.path.exists(prof):  # an ncu --set full capture of this kernel on this config
         with open(prof) as f:
             traffic = json.load(f).get("dram_bytes_per_launch")
 
     # e2e: public API with host buffers (pinned), H2D of u and D2H of the values inside the timing
+    # (for --op tensor: H2D of u and v, the tensor call, D2H of the values, through the same API)
     nu = m.n_dof if world == 1 else asm.n_rows
     u_pin = torch.empty(nu, dtype=torch.float64, pin_memory=True)
     u_pin.copy_(us[0].cpu())
@@ -287,11 +311,27 @@ def run_ours(args):
             for b in (MASS, STIFF)]
     outs_np = [o.numpy() if o is not None else None for o in outs]
     e2e_steps = max(3, min(args.steps, 20))
-    asm.ctx.reassemble_host(u_pin.numpy(), *outs_np)
+    if tensor:
+        v_pin = torch.empty(nu, dtype=torch.float64, pin_memory=True)
+        v_pin.copy_(vs[0].cpu())
+        ud, vd = torch.empty_like(us[0]), torch.empty_like(vs[0])
+
+        def e2e_once():
+            ud.copy_(u_pin, non_blocking=True)
+            vd.copy_(v_pin, non_blocking=True)
+            asm.ctx.assemble_tensor(ud, vd, mt, ct)
+            for o, d in zip(outs, (mt, ct)):
+                if o is not None:
+                    o.copy_(d[: o.shape[0]], non_blocking=True)
+            torch.cuda.synchronize()
+    else:
+        def e2e_once():
+            asm.ctx.reassemble_host(u_pin.numpy(), *outs_np)
+    e2e_once()
     barrier()
     t0 = time.perf_counter()
     for _ in range(e2e_steps):
-        asm.ctx.reassemble_host(u_pin.numpy(), *outs_np)
+        e2e_once()
     e2e_s = (time.perf_counter() - t0) / e2e_steps
     tmax = torch.tensor([e2e_s], dtype=torch.float64, device=dev)
     if world > 1:
@@ -304,9 +344,12 @@ def run_ours(args):
         if world == 1 and not args.no_cpu_baseline:
             cores = len(os.sched_getaffinity(0))
             rate, desc, _ = cpu_oracle_run(wl, cfg, float(os.environ.get("FEA_CPU_BASELINE_S", "10")), cores,
-                                           lib_to_user=asm.lib_to_user)
+                                           lib_to_user=asm.lib_to_user, tensor=tensor)
+            cores = 1 if tensor else cores
             cpu = {"value": rate, "unit": UNIT, "cores": cores, "kind": "oracle", "sample": desc}
         desc = workload_desc(cfg, wl)
+        if tensor:
+            desc["op"] = "tensor contractions (M o2 v, C o2 v), NEXT-1/2: u = u_r, v = u_{r+1} - u_r"
         desc.update({"l2": f"flushed ({flush_mb} MiB write) before every timed step" if flush_mb >= 256 else
                      f"NOT flushed ({flush_mb} MiB write): diagnostic run, not a bench value", "parallelism": f"rows{world}",
                      "nnz": int(nnz_local) if world == 1 else None, "setup_s": round(t_setup, 3),
@@ -327,11 +370,11 @@ def run_ours(args):
             "config": desc,
             "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
                          "frac": achieved / peak, "traffic": traffic, "algorithmic_bytes": B,
-                         "kernel": "k_reassemble5" if asm.ctx.stat(11) == 5 else "k_reassemble",
+                         "kernel": kname,
                          "peak_source": peak_src,
                          "kernel_ms_median": kern_ms},
             "cpu_baseline": cpu,
-            "e2e": {"value": entries_step / e2e_s, "unit": UNIT, "h2d_bytes_per_step": 8 * nu,
+            "e2e": {"value": entries_step / e2e_s, "unit": UNIT, "h2d_bytes_per_step": 8 * nu * (2 if tensor else 1),
                     "d2h_bytes_per_step": 8 * nnz_local * nmat, "ms_per_step": e2e_s * 1e3},
             "gpu_launches": args.steps * asm.ctx.stat(5),
             "clocks": sampler.summary(),
@@ -350,6 +393,8 @@ def main():
     ap.add_argument("--warmup", type=int, default=5)
     ap.add_argument("--config", default=os.environ.get("FEA_BENCH_CONFIG", DEFAULT_CONFIG), choices=sorted(CONFIGS))
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--op", default="reassemble", choices=["reassemble", "tensor"],
+                    help="reassemble: the per-iteration M, K reassembly (default); tensor: NEXT-1/2")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--tune", action="append", default=[], help="libfea tuning key=value (fea.h FEA_TUNE_*)")
     args = ap.parse_args()

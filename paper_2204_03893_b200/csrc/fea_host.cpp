@@ -607,7 +607,7 @@ static fea_status build_blocks(fea_ctx c, bool v5, bool orient, int64_t e_max, i
     for (int64_t r = 0; r < nr; ++r) max_inc = std::max(max_inc, iptr[r + 1] - iptr[r]);
     if (max_inc > 255) return c->fail(FEA_E_UNSUPPORTED, "a DOF belongs to %lld elements (> 255)", (long long)max_inc);
     // one row must fit a block: its elements and its record upper bound
-    const int64_t row_ub_max = max_inc * np * 4 + 4 * np * (max_inc + 3) + 12 * FEA_MAX_CLASSES + 64;
+    const int64_t row_ub_max = max_inc * np * 4 + 4 * np * (max_inc + 3) + 32 * FEA_MAX_CLASSES + 96;
     if (e_max < std::max<int64_t>(max_inc, 1) || rec_budget < row_ub_max)
         return c->fail(FEA_E_UNSUPPORTED, "shared-memory budget too small: %lld elements per block", (long long)e_max);
     if (orient && (int64_t)T * EM >= 32768)
@@ -624,8 +624,7 @@ static fea_status build_blocks(fea_ctx c, bool v5, bool orient, int64_t e_max, i
             int64_t add = 0;
             for (int64_t k = iptr[r]; k < iptr[r + 1]; ++k) add += mark[inc[k]] != cur;
             const int64_t rent = (iptr[r + 1] - iptr[r]) * np;
-            const int64_t ub = v5 ? 4 * (ent + rent) + 32 * FEA_MAX_CLASSES + 64
-                                  : 4 * (ent + rent) + 4 * np * (nE + add + 3) + 12 * FEA_MAX_CLASSES + 64;
+            const int64_t ub = 4 * (ent + rent) + (v5 ? 0 : 4 * np * (nE + add + 3) + 32) + 32 * FEA_MAX_CLASSES + 64;
             if (cur < 0 || nE + add > e_max || ub > rec_budget) {
                 ++cur;
                 brow.push_back(r);
@@ -719,51 +718,52 @@ static fea_status build_blocks(fea_ctx c, bool v5, bool orient, int64_t e_max, i
             o.err = "too many contributor-count classes";
             return;
         }
-        if (v5) {  // class table + fixed-size item records (fea_internal.h)
-            const int ncl = F.ncls;
-            std::vector<int32_t> coff(ncl);
-            int32_t off = 16 * ncl;
-            for (int k2 = 0; k2 < ncl; ++k2) {
-                const int C = cls[3 * k2], n = (k2 + 1 < ncl ? cls[3 * k2 + 4] : nslot) - cls[3 * k2 + 1];
-                coff[k2] = off;
-                off += fea_pad16(n * fea5_item_bytes(C));
-            }
-            F.rec_bytes = off;
-            if (F.rec_bytes > rec_budget) {
-                o.err = "record exceeds the shared-memory budget";
-                return;
-            }
-            o.rec.assign(F.rec_bytes, 0);
-            int32_t* tab = reinterpret_cast<int32_t*>(o.rec.data());
-            for (int k2 = 0; k2 < ncl; ++k2) {
-                const int C = cls[3 * k2], i0 = cls[3 * k2 + 1], n = (k2 + 1 < ncl ? cls[3 * k2 + 4] : nslot) - i0;
-                const int R = fea5_item_bytes(C);
-                tab[4 * k2] = C;
-                tab[4 * k2 + 1] = n;
-                tab[4 * k2 + 2] = coff[k2];
-                tab[4 * k2 + 3] = R;
-                for (int it = 0; it < n; ++it) {
-                    uint16_t* w = reinterpret_cast<uint16_t*>(o.rec.data() + coff[k2] + (size_t)it * R);
-                    w[0] = items[i0 + it];
-                    for (int q = 0; q < C; ++q) w[1 + q] = contrib[cls[3 * k2 + 2] + (size_t)it * C + q];
-                }
-            }
-        } else {
-            F.rec_bytes = fea_rec_bytes(F, np);
-            if (F.rec_bytes > rec_budget) {
-                o.err = "record exceeds the shared-memory budget";
-                return;
-            }
-            o.rec.assign(F.rec_bytes, 0);
-            std::memcpy(o.rec.data(), cls.data(), 4 * cls.size());
-            std::memcpy(o.rec.data() + fea_rec_off_items(F), items.data(), 2 * items.size());
-            std::memcpy(o.rec.data() + fea_rec_off_contrib(F), contrib.data(), 2 * contrib.size());
+        // class table + fixed-size item records (fea_internal.h), at byte `base` of the record:
+        // v5 records are only this; v4 records put a FeaRecHdr4 before and the DOFs after it
+        const int32_t base = v5 ? 0 : 32;
+        const int ncl = F.ncls;
+        std::vector<int32_t> coff(ncl);
+        int32_t off = 16 * ncl;
+        for (int k2 = 0; k2 < ncl; ++k2) {
+            const int C = cls[3 * k2], n = (k2 + 1 < ncl ? cls[3 * k2 + 4] : nslot) - cls[3 * k2 + 1];
+            coff[k2] = off;
+            off += fea_pad16(n * fea5_item_bytes(C));
         }
-        const int32_t nEp = fea_pad4(F.nE);
+        const int32_t nEp4 = fea_pad4(F.nE);
+        const int32_t dofs_off = base + off;
+        F.rec_bytes = v5 ? off : dofs_off + 4 * np * nEp4;
+        if (F.rec_bytes > rec_budget) {
+            o.err = "record exceeds the shared-memory budget";
+            return;
+        }
+        o.rec.assign(F.rec_bytes, 0);
+        int32_t* tab = reinterpret_cast<int32_t*>(o.rec.data() + base);
+        for (int k2 = 0; k2 < ncl; ++k2) {
+            const int C = cls[3 * k2], i0 = cls[3 * k2 + 1], n = (k2 + 1 < ncl ? cls[3 * k2 + 4] : nslot) - i0;
+            const int R = fea5_item_bytes(C);
+            tab[4 * k2] = C;
+            tab[4 * k2 + 1] = n;
+            tab[4 * k2 + 2] = coff[k2];
+            tab[4 * k2 + 3] = R;
+            for (int it = 0; it < n; ++it) {
+                uint16_t* w = reinterpret_cast<uint16_t*>(o.rec.data() + base + coff[k2] + (size_t)it * R);
+                w[0] = items[i0 + it];
+                for (int q = 0; q < C; ++q) w[1 + q] = contrib[cls[3 * k2 + 2] + (size_t)it * C + q];
+            }
+        }
+        if (!v5) {
+            FeaRecHdr4* h = reinterpret_cast<FeaRecHdr4*>(o.rec.data());
+            h->nE = F.nE;
+            h->ncls = F.ncls;
+            h->nslots = nslot;
+            h->dofs_off = dofs_off;
+            h->slot0 = 0;  // filled at concatenation (fea_build_pattern)
+        }
+        const int32_t nEp = nEp4;
         if (v5) o.dofs.assign((size_t)np * nEp, 0);
         F.r0 = (int32_t)ga;
         F.nr = (int32_t)(gb - ga);
-        int32_t* dofs = v5 ? o.dofs.data() : reinterpret_cast<int32_t*>(o.rec.data() + fea_rec_off_dofs(F));
+        int32_t* dofs = v5 ? o.dofs.data() : reinterpret_cast<int32_t*>(o.rec.data() + dofs_off);
         for (int64_t le = 0; le < (int64_t)E.size(); ++le)
             for (int i = 0; i < np; ++i) dofs[i * nEp + le] = c->ed[(size_t)E[le] * np + i];
         for (int64_t le = E.size(); le < nEp; ++le)  // padding lanes point at a valid DOF
@@ -802,6 +802,7 @@ static fea_status build_blocks(fea_ctx c, bool v5, bool orient, int64_t e_max, i
         std::vector<int32_t>().swap(bo[b].dofs);
         std::copy(bo[b].cols.begin(), bo[b].cols.end(), col_idx.begin() + B.slot0);
         std::memcpy(records.data() + B.rec_off, bo[b].rec.data(), B.rec_bytes);
+        if (!v5) reinterpret_cast<FeaRecHdr4*>(records.data() + B.rec_off)->slot0 = B.slot0;
         for (int64_t r = brow[b]; r < brow[b + 1]; ++r) row_ptr[r + 1] = bo[b].rownnz[r - brow[b]];
         std::vector<uint8_t>().swap(bo[b].rec);
     });
@@ -855,13 +856,13 @@ fea_status fea_build_pattern(fea_ctx c, int64_t* row_begin, int64_t* n_rows_loca
         const int nqp = 4 * fea_nk_kernel(c->order, nq);
         const int64_t per_el_smem = 8LL * T * nmat + 2 * (8LL * np + 48) + 2 * 8LL * nqp + 32;
         const double rec_el = 1.3 * (3.0 * np * np + 4.0 * np) + 8;  // record bytes per element (estimate)
-        e_max = (int64_t)((budget - 256 - 3 * 128) / (per_el_smem + rstages * rec_el));
+        e_max = (int64_t)((budget - 256 - 3 * 128 - 16LL * T * nmat) / (per_el_smem + rstages * rec_el));
         e_max = std::min<int64_t>(e_max, 65535 / T);
         e_max = e_max >= 8 ? ((e_max - 8) / 16) * 16 + 8 : 0;  // multiple of 8, == 8 mod 16
         rec_budget = ((int64_t)(rec_el * e_max) + 15) & ~int64_t(15);
     }
 
-    const int64_t EM = v5 ? (e_max | 1) : e_max;  // V row stride (v5: odd, fea_kernels5.cu)
+    const int64_t EM = v5 ? (e_max | 1) : fea4_vstride((int32_t)e_max);  // V row strides (fea_internal.h)
     PlanData P;
     {
         const fea_status st = build_blocks(c, v5, false, e_max, rec_budget, EM, P);

@@ -78,6 +78,19 @@ __host__ __device__ inline int32_t fea_rec_off_dofs(const FeaBlock& b) {
 __host__ __device__ inline int32_t fea_rec_bytes(const FeaBlock& b, int np) {
     return fea_rec_off_dofs(b) + 4 * np * fea_pad4(b.nE);
 }
+// v4 record (p >= 3, generic rules): a 32-byte header (FeaRecHdr4), the v5 class/item part
+// below (offsets relative to byte 32), then the block's element DOFs int32 [n_p][pad4(nE)] at
+// dofs_off.  The header lets the consumer warps read the block descriptor from shared memory.
+struct FeaRecHdr4 {
+    int32_t nE, ncls, nslots, dofs_off;
+    int64_t slot0;
+    int32_t pad_[2];
+};
+static_assert(sizeof(FeaRecHdr4) == 32, "FeaRecHdr4 must be 32 bytes");
+// v4 V row stride: even (16-byte DMMA epilogue stores) and == 2 (mod 8), so phase B's gathers of
+// many rows t of one element column spread over the banks (e_max == 8 mod 16)
+__host__ __device__ inline int32_t fea4_vstride(int32_t e_max) { return e_max + 2; }
+
 // v5 record: int4 class table {C, n_items, byte offset, item bytes} [ncls], then per class n_items
 // fixed-size item records {u16 block-local slot, u16 V offset [C]} of fea5_item_bytes(C) bytes
 // (one vector shared-memory load per item), each class array 16-byte aligned.  Classes group
@@ -123,8 +136,8 @@ __host__ __device__ inline void fea_smem_layout(int32_t* L, int rstages, int rec
     L[FEA_L_LAMM] = o; o = fea_align(o + 8 * nqp * e_max, 16);
     L[FEA_L_LAMC] = o; o = fea_align(o + 8 * nqp * e_max, 16);
     L[FEA_L_W] = o;    o = fea_align(o + 8 * 4 * e_max, 16);  // A00, A11, A01, |det B_e|
-    L[FEA_L_VM] = o;   o = fea_align(o + (do_m ? 8 * T * e_max : 0), 16);
-    L[FEA_L_VC] = o;   o = fea_align(o + (do_c ? 8 * T * e_max : 0), 16);
+    L[FEA_L_VM] = o;   o = fea_align(o + (do_m ? 8 * T * fea4_vstride(e_max) : 0), 16);
+    L[FEA_L_VC] = o;   o = fea_align(o + (do_c ? 8 * T * fea4_vstride(e_max) : 0), 16);
     L[FEA_L_BARS] = o; o += 16 * 8;
     L[FEA_L_TOTAL] = o;
 }

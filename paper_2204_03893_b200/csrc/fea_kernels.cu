@@ -89,12 +89,12 @@ __global__ void __launch_bounds__(fea_threads(P), fea_ctas(P)) k_reassemble(cons
         if (lane == 0)
             for (int jj = 0; jj < RS - 1 && jj < ncta_blocks; ++jj) issue_rec(jj);
         for (int j = 0; j < ncta_blocks; ++j) {
-            const FeaBlock blk = prm.blocks[blockIdx.x + j * gridDim.x];
             const int rs = j % RS, gs = j & 1;
             if (j >= 2) mbar_wait(&gdone[gs], (uint32_t)(((j >> 1) - 1) & 1));  // stage free (block j-2)
             mbar_wait(&full_rec[rs], (uint32_t)((j / RS) & 1));                   // record j landed
+            const FeaRecHdr4 blk = *reinterpret_cast<const FeaRecHdr4*>(sRec(rs));
             const int nEp = fea_pad4(blk.nE);
-            const int32_t* gd = reinterpret_cast<const int32_t*>(sRec(rs) + fea_rec_off_dofs(blk));
+            const int32_t* gd = reinterpret_cast<const int32_t*>(sRec(rs) + blk.dofs_off);
             double* gu = gUb(gs);
             double2* gx = gXb(gs);
             for (int le = lane; le < blk.nE; le += 32) {
@@ -146,15 +146,16 @@ __global__ void __launch_bounds__(fea_threads(P), fea_ctas(P)) k_reassemble(cons
         }
     };
     tick(-1);
+    const int vs = fea4_vstride(e_max);  // V row stride (fea_internal.h)
     for (int j = 0; j < ncta_blocks; ++j) {
-        const FeaBlock blk = prm.blocks[blockIdx.x + j * gridDim.x];
         const int rs = j % RS, gs = j & 1;
         const uint8_t* rec = sRec(rs);
-        const int nE = blk.nE;
-        const int net = (nE + 7) >> 3;
         const double* gU = gUb(gs);
         const double2* gX = gXb(gs);
         mbar_wait(&full_rec[rs], (uint32_t)((j / RS) & 1));
+        const FeaRecHdr4 blk = *reinterpret_cast<const FeaRecHdr4*>(rec);  // descriptor from the record
+        const int nE = blk.nE;
+        const int net = (nE + 7) >> 3;
         mbar_wait(&full_gat[gs], (uint32_t)((j >> 1) & 1));
         tick(0);
 
@@ -268,12 +269,12 @@ __global__ void __launch_bounds__(fea_threads(P), fea_ctas(P)) k_reassemble(cons
                     }
                 }
                 if (t < T) {
-                    if (DO_M) *reinterpret_cast<double2*>(sVm + t * e_max + le0) = make_double2(m0, m1);
+                    if (DO_M) *reinterpret_cast<double2*>(sVm + t * vs + le0) = make_double2(m0, m1);
                     if (DO_C) {
                         const double2 w0 = *reinterpret_cast<const double2*>(sW + le0);
                         const double2 w1 = *reinterpret_cast<const double2*>(sW + e_max + le0);
                         const double2 w2 = *reinterpret_cast<const double2*>(sW + 2 * e_max + le0);
-                        *reinterpret_cast<double2*>(sVc + t * e_max + le0) =
+                        *reinterpret_cast<double2*>(sVc + t * vs + le0) =
                             make_double2(fma(w0.x, a0, fma(w1.x, b0, w2.x * c0)), fma(w0.y, a1, fma(w1.y, b1, w2.y * c1)));
                     }
                 }
@@ -284,8 +285,8 @@ __global__ void __launch_bounds__(fea_threads(P), fea_ctas(P)) k_reassemble(cons
         tick(5);
 
         // ---------------- Phase B: fixed-order segmented reduction into the CSR slots.
-        phase_b<DO_M, DO_C>(rec, blk, sVm, sVc, DO_M ? prm.out_m + blk.slot0 : nullptr,
-                            DO_C ? prm.out_c + blk.slot0 : nullptr, tid, NCT);
+        phase_b5<DO_M, DO_C>(rec + 32, blk.ncls, sVm, sVc, DO_M ? prm.out_m + blk.slot0 : nullptr,
+                             DO_C ? prm.out_c + blk.slot0 : nullptr, tid, NCT);
         tick(3);
         consumer_sync(NCT);  // V and the record stage are free
         tick(5);
