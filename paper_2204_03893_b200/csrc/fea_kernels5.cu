@@ -86,11 +86,13 @@ __global__ void __launch_bounds__(fea5_threads(P), 1) k_reassemble5(const __grid
     uint64_t* recb = bars + 4;  // [2] TMA transactions of the buffer's record
     FeaBlock* sBlk = reinterpret_cast<FeaBlock*>(smem + prm.lay[FEA_L_W]);
 
-    // Block descriptors: ring of DR entries (slot k % DR = block k).  Blocks 0..4 are written before
-    // the first barrier; thread 0 copies block s + 5 (cp.async) at step s, completes the copy at
-    // step s + 1 before arriving on full[(s + 1) & 1], and every warp acquires it with that
-    // barrier in step s + 2.  Reads beyond the published window go to global memory.
-    int win = 5;  // blocks < win are readable from the ring
+    // Block descriptors: ring of DR entries (slot k % DR = block k).  Blocks 0..5 are written before
+    // the first barrier; thread 0 copies block s + 6 (cp.async) at step s into the slot of block
+    // s - 2 (whose phase B is done: thread 0 waited on free[s & 1]), completes the copy at step
+    // s + 1 before arriving on full[(s + 1) & 1], and every warp acquires it with that barrier in
+    // step s + 2.  So during [A] of step t blocks < t + 4 are readable, after its full wait < t + 5
+    // (the load cursor reads up to t + 3).  Reads beyond the window go to global memory.
+    int win = 6;  // blocks < win are readable from the ring
     auto blk_of = [&](int k) -> const FeaBlock& { return k < win ? sBlk[k & (DR - 1)] : prm.blocks[b0 + k * G]; };
 
     auto prefetch_range = [&](const void* p, size_t bytes) {
@@ -116,7 +118,7 @@ __global__ void __launch_bounds__(fea5_threads(P), 1) k_reassemble5(const __grid
         }
         fence_mbar_init();
     }
-    if (tid < 5 && tid < nb) sBlk[tid] = prm.blocks[b0 + tid * G];
+    if (tid < 6 && tid < nb) sBlk[tid] = prm.blocks[b0 + tid * G];
     __syncthreads();
     if (tid == 0)
         for (int k = 0; k < PF && k < nb; ++k) prefetch_blk(k);
@@ -282,20 +284,20 @@ __global__ void __launch_bounds__(fea5_threads(P), 1) k_reassemble5(const __grid
     tick(6);
 
     for (int s = 0; s <= nb; ++s) {
-        win = max(s + 3, 5);  // ring entries published by the full barrier of step s - 1
+        win = max(s + 4, 6);  // ring entries published by the full barrier of step s - 1
         if (s < nb) {
             const int b = s & 1;
             if (s >= 2) mbar_wait(&freeb[b], (uint32_t)(((s - 2) >> 1) & 1));  // B of block s - 2 done
             tick(5);
             if (tid == 0) {
-                asm volatile("cp.async.wait_all;" ::: "memory");  // ring entry of block s + 4
+                asm volatile("cp.async.wait_all;" ::: "memory");  // ring entry of block s + 5
                 const FeaBlock& bk = sBlk[s & (DR - 1)];
                 fence_proxy_async();
                 mbar_expect_tx(&recb[b], (uint32_t)bk.rec_bytes);
                 tma_load_1d(sRec0 + b * rec_stride, prm.records + bk.rec_off, (uint32_t)bk.rec_bytes, &recb[b]);
-                if (s + 5 < nb) {  // slot of block s - 3, whose phase B is done (B(s - 2) is)
-                    const uint8_t* src = reinterpret_cast<const uint8_t*>(prm.blocks + b0 + (s + 5) * G);
-                    uint8_t* dst = reinterpret_cast<uint8_t*>(sBlk + ((s + 5) & (DR - 1)));
+                if (s + 6 < nb) {  // slot of block s - 2, whose phase B is done
+                    const uint8_t* src = reinterpret_cast<const uint8_t*>(prm.blocks + b0 + (s + 6) * G);
+                    uint8_t* dst = reinterpret_cast<uint8_t*>(sBlk + ((s + 6) & (DR - 1)));
 #pragma unroll
                     for (int w = 0; w < 4; ++w) cp_async16(dst + 16 * w, src + 16 * w);
                     asm volatile("cp.async.commit_group;" ::: "memory");
@@ -319,7 +321,7 @@ __global__ void __launch_bounds__(fea5_threads(P), 1) k_reassemble5(const __grid
         if (s >= 1) {
             const int s1 = s - 1, b = s1 & 1;
             mbar_wait(&full[b], (uint32_t)((s1 >> 1) & 1));
-            win = max(s + 4, 5);
+            win = max(s + 5, 6);
             tick(2);
             mbar_wait(&recb[b], (uint32_t)((s1 >> 1) & 1));
             tick(3);

@@ -47,6 +47,18 @@ if __name__ == "__main__":
                 print(f"  {k:70s} {v[0]} {v[1]}")
         top = sorted(stalls.items(), key=lambda kv: -kv[1][0])[:6]
         print("  top stalls (per issue):", ", ".join(f"{k.split('stalled_')[1].split('_per')[0]}={v[0]:.2f}" for k, v in top))
+    if "--traffic" in sys.argv:  # --traffic CFG OUT.json: per-launch DRAM bytes of the (first) kernel
+        cfg, out = sys.argv[sys.argv.index("--traffic") + 1], sys.argv[sys.argv.index("--traffic") + 2]
+        d = res[0]
+        rd = d["dram__bytes_read.sum"][0] * (1e6 if d["dram__bytes_read.sum"][1].startswith("M") else
+                                              1e9 if d["dram__bytes_read.sum"][1].startswith("G") else 1.0)
+        wr = d["dram__bytes_write.sum"][0] * (1e6 if d["dram__bytes_write.sum"][1].startswith("M") else
+                                               1e9 if d["dram__bytes_write.sum"][1].startswith("G") else 1.0)
+        t = d["gpu__time_duration.sum"]
+        with open(out, "w") as f:
+            json.dump({"config": cfg, "kernel": d["kernel"], "dram_bytes_read": rd, "dram_bytes_write": wr,
+                       "dram_bytes_per_launch": rd + wr, "duration_under_ncu": f"{t[0]} {t[1]}",
+                       "source": f"ncu --set full --clock-control none, one launch ({sys.argv[1]})"}, f, indent=1)
     if "--json" in sys.argv:
         with open(sys.argv[sys.argv.index("--json") + 1], "w") as f:
             json.dump(res, f, indent=1)
