@@ -68,6 +68,8 @@ enum {
     FEA_TUNE_KERNEL = 2,        /* kernel generation: 0 = automatic (v5 for p <= 2 with the native
                                    3/6-point rules, v4 otherwise), 4 = force v4                      */
     FEA_TUNE_EMAX = 3,          /* v5: cap on elements per row block (0 = from the smem budget)      */
+    FEA_TUNE_EXCHANGE = 5,      /* world > 1: 0 = interface-only exchange of u (default), 1 = full-
+                                   vector allgather                                                 */
     FEA_TUNE_PLAN_WHICH = 4     /* FEA_MASS | FEA_STIFF: matrices the plan's shared memory is sized
                                    for (default both); assembling more than planned runs one pass
                                    per matrix                                                        */
@@ -162,6 +164,20 @@ fea_status fea_reassemble_host(fea_ctx ctx, const double* u_host, double* mass_h
  * Errors: FEA_E_STATE (no pattern), FEA_E_ARG (NULL u/v, misalignment), FEA_E_UNSUPPORTED. */
 fea_status fea_assemble_tensor(fea_ctx ctx, const double* u_full, const double* v_full, double* mt_vals,
                                double* ct_vals);
+
+/* Interface-only exchange of u (world > 1).  I_t = the library DOFs owned by
+ * rank t that another rank's elements read (ascending; every rank derives all lists from the full
+ * mesh at fea_build_pattern).  fea_get_interface: offsets (host, world + 1 int64, I_t =
+ * dofs[offsets[t] .. offsets[t + 1])) and dofs (host, offsets[world] int32); either may be NULL.
+ * fea_reassemble (world > 1, FEA_TUNE_EXCHANGE 0) runs, on the ctx stream: pack (send[k] =
+ * u_owned[I_r[k] - row_begin], k < maxI = fea_get_stat key 14, zero padded), one ncclAllGather of
+ * maxI float64 per rank, unpack (u_full[I_t[k]] = recv[t * maxI + k] for t != rank; u_full rows
+ * of this rank = u_owned).  The pack / unpack steps are exported for callers with their own
+ * transport (MPI, ...): send is device maxI float64; recv is device world * maxI float64 (the
+ * concatenation of every rank's send); u_full is device n_dof float64.  Asynchronous. */
+fea_status fea_get_interface(fea_ctx ctx, int64_t* offsets, int32_t* dofs);
+fea_status fea_exchange_pack(fea_ctx ctx, const double* u_owned, double* send);
+fea_status fea_exchange_unpack(fea_ctx ctx, const double* u_owned, const double* recv, double* u_full);
 
 /* Multi-GPU: the 128-byte ncclUniqueId.  Rank 0 calls fea_nccl_unique_id and broadcasts the
  * bytes (e.g. over a torch.distributed process group); every rank then calls fea_set_nccl. */

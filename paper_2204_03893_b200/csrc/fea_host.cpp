@@ -125,6 +125,15 @@ struct fea_ctx_s {
     // reassemble buffers
     double* d_ufull = nullptr;
     double* d_usend = nullptr;
+    // interface-only exchange (world > 1; NEXT-3): I_t of every rank t, concatenated
+    int exchange = 0;  // 0 = interface-only (default), 1 = full-vector allgather
+    std::vector<int32_t> iface;
+    std::vector<int64_t> ioff;
+    int maxI = 0;
+    int32_t* d_iface = nullptr;
+    int64_t* d_ioff = nullptr;
+    double* d_isend = nullptr;
+    double* d_irecv = nullptr;
     double* d_vm = nullptr;
     double* d_vc = nullptr;
     void* comm = nullptr;
@@ -158,6 +167,10 @@ struct fea_ctx_s {
         dfree(d_xy);
         dfree(d_ufull);
         dfree(d_usend);
+        dfree(d_iface);
+        dfree(d_ioff);
+        dfree(d_isend);
+        dfree(d_irecv);
         have_mesh = false;
     }
 };
@@ -555,6 +568,10 @@ fea_status fea_set_tuning(fea_ctx c, int key, int64_t value) {
             if (value < 0 || value > 65535) return c->fail(FEA_E_ARG, "element cap out of range");
             c->tune_emax = value;
             break;
+        case 5:  // exchange of u between ranks: 0 = interface-only, 1 = full allgather
+            if (value != 0 && value != 1) return c->fail(FEA_E_ARG, "exchange must be 0 or 1");
+            c->exchange = (int)value;
+            break;
         case 4:  // plan matrices bitmask (FEA_MASS | FEA_STIFF)
             if (value < 1 || value > 3) return c->fail(FEA_E_ARG, "plan matrices must be a nonzero MASS|STIFF mask");
             c->plan_which = (int)value;
@@ -885,6 +902,34 @@ fea_status fea_build_pattern(fea_ctx c, int64_t* row_begin, int64_t* n_rows_loca
     c->nnz = nnz;
     c->smem_bytes = L[FEA_L_TOTAL];
     std::memcpy(c->lay, L, sizeof(c->lay));
+    // ---- interface sets I_t of every rank t (world > 1): owned DOFs that another rank's elements
+    // read.  Ranks own contiguous chunks of rows_per_rank library rows; every rank derives the
+    // same lists from the full mesh.
+    c->iface.clear();
+    c->ioff.assign(c->world + 1, 0);
+    c->maxI = 0;
+    if (c->world > 1) {
+        const int W = c->world;
+        std::vector<uint8_t> need((size_t)c->n_dof, 0);
+        for (int64_t e = 0; e < c->n_e; ++e) {
+            const int32_t* d = &c->ed[(size_t)e * np];
+            int o0 = (int)(d[0] / rpr);
+            bool multi = false;
+            for (int i = 1; i < np; ++i) multi |= (int)(d[i] / rpr) != o0;
+            if (multi)
+                for (int i = 0; i < np; ++i) need[d[i]] = 1;  // read by another rank (some owner of e differs)
+        }
+        std::vector<int64_t> cnt(W + 1, 0);
+        for (int64_t d = 0; d < c->n_dof; ++d)
+            if (need[d]) cnt[d / rpr + 1]++;
+        for (int t = 0; t < W; ++t) cnt[t + 1] += cnt[t];
+        c->ioff = cnt;
+        c->iface.resize(cnt[W]);
+        std::vector<int64_t> pos(cnt.begin(), cnt.end() - 1);
+        for (int64_t d = 0; d < c->n_dof; ++d)
+            if (need[d]) c->iface[pos[d / rpr]++] = (int32_t)d;
+        for (int t = 0; t < W; ++t) c->maxI = std::max<int>(c->maxI, (int)(cnt[t + 1] - cnt[t]));
+    }
     c->stat_visits = visits;
     c->stat_owned = owned;
     c->stat_entries = ncon;
@@ -907,6 +952,19 @@ fea_status fea_build_pattern(fea_ctx c, int64_t* row_begin, int64_t* n_rows_loca
     }
     if (!c->d_ufull) FEA_CUDA(c, cudaMalloc(&c->d_ufull, (size_t)rpr * c->world * sizeof(double)));
     if (!c->d_usend) FEA_CUDA(c, cudaMalloc(&c->d_usend, (size_t)rpr * sizeof(double)));
+    if (c->world > 1) {
+        dfree(c->d_iface);
+        dfree(c->d_ioff);
+        dfree(c->d_isend);
+        dfree(c->d_irecv);
+        FEA_CUDA(c, cudaMalloc(&c->d_iface, std::max<size_t>(1, c->iface.size()) * sizeof(int32_t)));
+        if (!c->iface.empty())
+            FEA_CUDA(c, cudaMemcpy(c->d_iface, c->iface.data(), c->iface.size() * sizeof(int32_t), cudaMemcpyHostToDevice));
+        FEA_CUDA(c, cudaMalloc(&c->d_ioff, c->ioff.size() * sizeof(int64_t)));
+        FEA_CUDA(c, cudaMemcpy(c->d_ioff, c->ioff.data(), c->ioff.size() * sizeof(int64_t), cudaMemcpyHostToDevice));
+        FEA_CUDA(c, cudaMalloc(&c->d_isend, std::max<size_t>(1, c->maxI) * sizeof(double)));
+        FEA_CUDA(c, cudaMalloc(&c->d_irecv, std::max<size_t>(1, (size_t)c->maxI * c->world) * sizeof(double)));
+    }
     int occ = 0;
     int rc = v5 ? fea_kernel_occupancy5(c->order, dm, dcm, c->smem_bytes, &occ, &c->threads)
                 : fea_kernel_occupancy(c->order, c->nq, dm, dcm, c->smem_bytes, &occ, &c->threads);
@@ -1032,6 +1090,63 @@ fea_status fea_assemble_stiffness(fea_ctx c, const double* u_full, double* vals)
     return fea_assemble(c, u_full, nullptr, vals);
 }
 
+// u_owned (this rank's rows) -> c->d_ufull holding every value this rank's kernel reads:
+// interface-only (pack, one ncclAllGather of maxI values per rank, unpack) or the full-vector
+// allgather of rows_per_rank values per rank.  Stream-ordered on the ctx stream.
+static fea_status exchange_u(fea_ctx c, const double* u_owned) {
+    if (c->exchange == 0) {
+        int rc = fea_launch_pack(u_owned, c->d_iface + c->ioff[c->rank], (int)(c->ioff[c->rank + 1] - c->ioff[c->rank]),
+                                 c->row_begin, c->maxI, c->d_isend, c->stream);
+        if (rc) return c->fail(FEA_E_CUDA, "pack: %s", cudaGetErrorString((cudaError_t)rc));
+        if (c->maxI > 0) {
+            ncclResult_t r = nccl().allGather(c->d_isend, c->d_irecv, (size_t)c->maxI, ncclDouble, (ncclComm_t)c->comm,
+                                              c->stream);
+            if (r != ncclSuccess) return c->fail(FEA_E_NCCL, "ncclAllGather: %s", nccl().getErrorString(r));
+        }
+        rc = fea_launch_unpack(c->d_irecv, c->d_iface, c->d_ioff, c->world, c->rank, c->maxI, c->ioff[c->world],
+                               u_owned, c->row_begin, c->n_rows, c->d_ufull, c->stream);
+        if (rc) return c->fail(FEA_E_CUDA, "unpack: %s", cudaGetErrorString((cudaError_t)rc));
+        return FEA_OK;
+    }
+    // full vector: pad the owned slice to rows_per_rank, then allgather
+    if (c->n_rows && u_owned != c->d_usend)
+        FEA_CUDA(c, cudaMemcpyAsync(c->d_usend, u_owned, c->n_rows * sizeof(double), cudaMemcpyDeviceToDevice, c->stream));
+    ncclResult_t r = nccl().allGather(c->d_usend, c->d_ufull, (size_t)c->rows_per_rank, ncclDouble,
+                                      (ncclComm_t)c->comm, c->stream);
+    if (r != ncclSuccess) return c->fail(FEA_E_NCCL, "ncclAllGather: %s", nccl().getErrorString(r));
+    return FEA_OK;
+}
+
+fea_status fea_get_interface(fea_ctx c, int64_t* offsets, int32_t* dofs) {
+    if (!c) return FEA_E_ARG;
+    if (!c->have_plan) return c->fail(FEA_E_STATE, "get_interface before build_pattern");
+    if (offsets) std::memcpy(offsets, c->ioff.data(), c->ioff.size() * sizeof(int64_t));
+    if (dofs && !c->iface.empty()) std::memcpy(dofs, c->iface.data(), c->iface.size() * sizeof(int32_t));
+    return FEA_OK;
+}
+
+fea_status fea_exchange_pack(fea_ctx c, const double* u_owned, double* send) {
+    if (!c) return FEA_E_ARG;
+    if (c->host_only) return c->fail(FEA_E_STATE, "host-only (planning) context has no device");
+    if (!c->have_plan || c->world < 2) return c->fail(FEA_E_STATE, "exchange_pack needs a world > 1 plan");
+    if (!u_owned || !send) return c->fail(FEA_E_ARG, "NULL buffer");
+    cudaSetDevice(c->device);
+    const int rc = fea_launch_pack(u_owned, c->d_iface + c->ioff[c->rank], (int)(c->ioff[c->rank + 1] - c->ioff[c->rank]),
+                                   c->row_begin, c->maxI, send, c->stream);
+    return rc ? c->fail(FEA_E_CUDA, "pack: %s", cudaGetErrorString((cudaError_t)rc)) : FEA_OK;
+}
+
+fea_status fea_exchange_unpack(fea_ctx c, const double* u_owned, const double* recv, double* u_full) {
+    if (!c) return FEA_E_ARG;
+    if (c->host_only) return c->fail(FEA_E_STATE, "host-only (planning) context has no device");
+    if (!c->have_plan || c->world < 2) return c->fail(FEA_E_STATE, "exchange_unpack needs a world > 1 plan");
+    if (!u_owned || !recv || !u_full) return c->fail(FEA_E_ARG, "NULL buffer");
+    cudaSetDevice(c->device);
+    const int rc = fea_launch_unpack(recv, c->d_iface, c->d_ioff, c->world, c->rank, c->maxI, c->ioff[c->world],
+                                     u_owned, c->row_begin, c->n_rows, u_full, c->stream);
+    return rc ? c->fail(FEA_E_CUDA, "unpack: %s", cudaGetErrorString((cudaError_t)rc)) : FEA_OK;
+}
+
 fea_status fea_reassemble(fea_ctx c, const double* u_owned, double* mass_vals, double* stiff_vals) {
     if (!c) return FEA_E_ARG;
     if (c->host_only) return c->fail(FEA_E_STATE, "host-only (planning) context has no device");
@@ -1040,12 +1155,8 @@ fea_status fea_reassemble(fea_ctx c, const double* u_owned, double* mass_vals, d
     cudaSetDevice(c->device);
     if (c->world == 1) return fea_assemble(c, u_owned, mass_vals, stiff_vals);
     if (!c->comm) return c->fail(FEA_E_STATE, "world > 1 requires fea_set_nccl");
-    // pad the owned slice to rows_per_rank, then allgather (the only cross-GPU traffic)
-    if (c->n_rows)
-        FEA_CUDA(c, cudaMemcpyAsync(c->d_usend, u_owned, c->n_rows * sizeof(double), cudaMemcpyDeviceToDevice, c->stream));
-    ncclResult_t r = nccl().allGather(c->d_usend, c->d_ufull, (size_t)c->rows_per_rank, ncclDouble,
-                                      (ncclComm_t)c->comm, c->stream);
-    if (r != ncclSuccess) return c->fail(FEA_E_NCCL, "ncclAllGather: %s", nccl().getErrorString(r));
+    const fea_status st = exchange_u(c, u_owned);
+    if (st != FEA_OK) return st;
     return fea_assemble(c, c->d_ufull, mass_vals, stiff_vals);
 }
 
@@ -1064,9 +1175,8 @@ fea_status fea_reassemble_host(fea_ctx c, const double* u_host, double* mass_hos
     if (c->world == 1) s = fea_assemble(c, c->d_ufull, mass_host ? c->d_vm : nullptr, stiff_host ? c->d_vc : nullptr);
     else {
         if (!c->comm) return c->fail(FEA_E_STATE, "world > 1 requires fea_set_nccl");
-        ncclResult_t r = nccl().allGather(c->d_usend, c->d_ufull, (size_t)c->rows_per_rank, ncclDouble,
-                                          (ncclComm_t)c->comm, c->stream);
-        if (r != ncclSuccess) return c->fail(FEA_E_NCCL, "ncclAllGather: %s", nccl().getErrorString(r));
+        const fea_status st = exchange_u(c, c->d_usend);
+        if (st != FEA_OK) return st;
         s = fea_assemble(c, c->d_ufull, mass_host ? c->d_vm : nullptr, stiff_host ? c->d_vc : nullptr);
     }
     if (s != FEA_OK) return s;
@@ -1208,6 +1318,7 @@ fea_status fea_get_stat(fea_ctx c, int key, int64_t* value) {
             }
             return c->fail(FEA_E_ARG, "unknown stat key %d", key);
         case 11: *value = c->kver; break;
+        case 14: *value = c->maxI; break;
     }
     return FEA_OK;
 }

@@ -219,6 +219,11 @@ struct FeaTParams {
 int fea_launch_tensor(const FeaTParams& prm, int order, int smem_bytes, int grid, void* stream);
 int fea_tensor_occupancy(int order, int smem_bytes, int* ctas_per_sm, int* threads);
 
+// interface-only exchange of u (fea_kernels_x.cu)
+int fea_launch_pack(const double* u_owned, const int32_t* I, int nI, int64_t R0, int maxI, double* send, void* stream);
+int fea_launch_unpack(const double* recv, const int32_t* Iall, const int64_t* ioff, int world, int rank, int maxI,
+                      int64_t total, const double* u_owned, int64_t R0, int64_t n_own, double* u_full, void* stream);
+
 // Launch the fused reassembly kernel (defined in fea_kernels.cu).  Returns a cudaError_t.
 int fea_launch_reassemble(const FeaKParams& prm, int order, int smem_bytes, int grid, void* stream);
 // Per-SM CTA occupancy of the kernel variant and its block size (threads).

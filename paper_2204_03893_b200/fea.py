@@ -26,7 +26,8 @@ FEA_TUNE_SMEM_BUDGET, FEA_TUNE_KERNEL, FEA_TUNE_EMAX, FEA_TUNE_PLAN_WHICH = 1, 2
 SYMBOLS = ["fea_create", "fea_set_element", "fea_mesh_upload", "fea_set_tuning", "fea_build_pattern",
            "fea_get_pattern", "fea_get_dof_perm", "fea_get_elem_perm", "fea_set_coefficient",
            "fea_assemble_mass", "fea_assemble_stiffness", "fea_assemble", "fea_reassemble",
-           "fea_reassemble_host", "fea_assemble_tensor", "fea_nccl_unique_id", "fea_set_nccl", "fea_sync", "fea_get_stat",
+           "fea_reassemble_host", "fea_assemble_tensor", "fea_get_interface", "fea_exchange_pack",
+           "fea_exchange_unpack", "fea_nccl_unique_id", "fea_set_nccl", "fea_sync", "fea_get_stat",
            "fea_last_error", "fea_destroy"]
 
 
@@ -64,6 +65,9 @@ def load_library():
         "fea_reassemble": [P, P, P, P],
         "fea_reassemble_host": [P, P, P, P],
         "fea_assemble_tensor": [P, P, P, P, P],
+        "fea_get_interface": [P, P, P],
+        "fea_exchange_pack": [P, P, P],
+        "fea_exchange_unpack": [P, P, P, P],
         "fea_nccl_unique_id": [P],
         "fea_set_nccl": [P, P],
         "fea_sync": [P],
@@ -216,6 +220,23 @@ class Context:
                                                   _dev_ptr(v_full, "v_full", self.n_dof),
                                                   _dev_ptr(mt_vals, "mt_vals", self.nnz),
                                                   _dev_ptr(ct_vals, "ct_vals", self.nnz)))
+
+    def get_interface(self):
+        """Interface lists of every rank (NEXT-3): (offsets [world + 1], dofs)."""
+        off = np.zeros(self.world + 1, dtype=np.int64)
+        self._check(self._lib.fea_get_interface(self._h, _np_ptr(off), None))
+        dofs = np.zeros(max(int(off[-1]), 1), dtype=np.int32)
+        self._check(self._lib.fea_get_interface(self._h, _np_ptr(off), _np_ptr(dofs)))
+        return off, dofs[: int(off[-1])]
+
+    def exchange_pack(self, u_owned, send):
+        self._check(self._lib.fea_exchange_pack(self._h, _dev_ptr(u_owned, "u_owned", self.n_rows),
+                                                _dev_ptr(send, "send", self.stat(14))))
+
+    def exchange_unpack(self, u_owned, recv, u_full):
+        self._check(self._lib.fea_exchange_unpack(self._h, _dev_ptr(u_owned, "u_owned", self.n_rows),
+                                                  _dev_ptr(recv, "recv", self.stat(14) * self.world),
+                                                  _dev_ptr(u_full, "u_full", self.n_dof)))
 
     def reassemble_host(self, u_host, mass_host=None, stiff_host=None):
         """Host buffers (numpy float64; pinned torch CPU tensors also accepted via .numpy())."""
