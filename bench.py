@@ -352,9 +352,10 @@ def run_ours(args):
             desc["op"] = "tensor contractions (M o2 v, C o2 v), NEXT-1/2: u = u_r, v = u_{r+1} - u_r"
         if world > 1:
             mi = asm.ctx.stat(14)
+            rpr = -(-m.n_dof // world)
             desc["exchange"] = (f"interface-only ncclAllGather of {mi} float64 per rank "
-                                f"({8 * mi * world} B received per GPU per step; full vector would be "
-                                f"{8 * asm.ctx.rows_per_rank() * world if hasattr(asm.ctx, 'rows_per_rank') else 'n/a'} B)")
+                                f"({8 * mi * world} B received per GPU per step; the full-vector "
+                                f"allgather would be {8 * rpr * world} B)")
         desc.update({"l2": f"flushed ({flush_mb} MiB write) before every timed step" if flush_mb >= 256 else
                      f"NOT flushed ({flush_mb} MiB write): diagnostic run, not a bench value", "parallelism": f"rows{world}",
                      "nnz": int(nnz_local) if world == 1 else None, "setup_s": round(t_setup, 3),
