@@ -762,10 +762,13 @@ static fea_status build_blocks(fea_ctx c, bool v5, bool orient, int64_t e_max, i
             tab[4 * k2 + 1] = n;
             tab[4 * k2 + 2] = coff[k2];
             tab[4 * k2 + 3] = R;
+            // items in slot order within the class: neighbouring lanes store to nearby CSR slots
+            // (a bank-balanced reordering of the V reads measured slower: it scatters the stores)
             for (int it = 0; it < n; ++it) {
+                const int src = it;
                 uint16_t* w = reinterpret_cast<uint16_t*>(o.rec.data() + base + coff[k2] + (size_t)it * R);
-                w[0] = items[i0 + it];
-                for (int q = 0; q < C; ++q) w[1 + q] = contrib[cls[3 * k2 + 2] + (size_t)it * C + q];
+                w[0] = items[i0 + src];
+                for (int q = 0; q < C; ++q) w[1 + q] = contrib[cls[3 * k2 + 2] + (size_t)src * C + q];
             }
         }
         if (!v5) {

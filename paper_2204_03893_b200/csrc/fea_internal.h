@@ -136,20 +136,24 @@ __host__ __device__ inline void fea_smem_layout(int32_t* L, int rstages, int rec
     L[FEA_L_LAMM] = o; o = fea_align(o + 8 * nqp * e_max, 16);
     L[FEA_L_LAMC] = o; o = fea_align(o + 8 * nqp * e_max, 16);
     L[FEA_L_W] = o;    o = fea_align(o + 8 * 4 * e_max, 16);  // A00, A11, A01, |det B_e|
-    L[FEA_L_VM] = o;   o = fea_align(o + (do_m ? 8 * T * fea4_vstride(e_max) : 0), 16);
-    L[FEA_L_VC] = o;   o = fea_align(o + (do_c ? 8 * T * fea4_vstride(e_max) : 0), 16);
+    o = fea_align(o, 128);
+    L[FEA_L_VM] = o;   o = fea_align(o + (do_m ? 8 * T * fea4_vstride(e_max) : 0), 128);
+    L[FEA_L_VC] = o;   o = fea_align(o + (do_c ? 8 * T * fea4_vstride(e_max) : 0), 128);
     L[FEA_L_BARS] = o; o += 16 * 8;
     L[FEA_L_TOTAL] = o;
 }
 
+// one V buffer of k_reassemble5 (doubles): T rows of stride e_max | 1, padded to 128 bytes so every
+// buffer (and V_m vs V_c) has the same bank mapping (the planner balances phase B's banks)
+__host__ __device__ constexpr int fea5_vbuf(int T, int e_max) { return (T * (e_max | 1) + 15) & ~15; }
 // Shared-memory layout of k_reassemble5: V_m, V_c [2][T][e_max | 1], two record stages of
 // stride L[FEA_L_GU], mbarriers (6), descriptor ring (8 x 64 B at L[FEA_L_W]).
 __host__ __device__ inline void fea5_smem_layout(int32_t* L, int rec_max, int e_max, int p, int do_m, int do_c) {
     const int T = fea_T(p);
     for (int i = 0; i < FEA_L_N; ++i) L[i] = 0;
     int32_t o = 0;
-    L[FEA_L_VM] = o; o += do_m ? 2 * 8 * T * (e_max | 1) : 0;
-    L[FEA_L_VC] = o; o += do_c ? 2 * 8 * T * (e_max | 1) : 0;
+    L[FEA_L_VM] = o; o += do_m ? 2 * 8 * fea5_vbuf(T, e_max) : 0;
+    L[FEA_L_VC] = o; o += do_c ? 2 * 8 * fea5_vbuf(T, e_max) : 0;
     o = (o + 127) / 128 * 128;
     L[FEA_L_GU] = (rec_max + 127) / 128 * 128;  // record stage stride
     L[FEA_L_REC] = o; o += 2 * L[FEA_L_GU];
@@ -192,9 +196,9 @@ enum { FEA_LT_V1 = 0, FEA_LT_VUP = 1, FEA_LT_VDN = 2, FEA_LT_REC = 3, FEA_LT_TAB
 __host__ __device__ inline void fea_t_smem_layout(int32_t* L, int rec_max, int e_max, int p) {
     const int T = fea_T(p), np = fea_np(p), vs = e_max | 1;
     int32_t o = 0;
-    L[FEA_LT_V1] = o; o += 8 * T * vs;
-    L[FEA_LT_VUP] = o; o += 8 * T * vs;
-    L[FEA_LT_VDN] = o; o += 8 * T * vs;
+    L[FEA_LT_V1] = o; o = (o + 8 * T * vs + 127) / 128 * 128;
+    L[FEA_LT_VUP] = o; o = (o + 8 * T * vs + 127) / 128 * 128;
+    L[FEA_LT_VDN] = o; o = (o + 8 * T * vs + 127) / 128 * 128;
     o = (o + 127) / 128 * 128;
     L[FEA_LT_REC] = o; o += (rec_max + 127) / 128 * 128;
     L[FEA_LT_TAB] = o; o += 8 * (3 * np * 16 + 16);

@@ -77,7 +77,7 @@ __global__ void __launch_bounds__(fea5_threads(P), 1) k_reassemble5(const __grid
     extern __shared__ __align__(128) uint8_t smem[];
     double* const sVm0 = reinterpret_cast<double*>(smem + prm.lay[FEA_L_VM]);  // [2][T][vs]
     double* const sVc0 = reinterpret_cast<double*>(smem + prm.lay[FEA_L_VC]);
-    const int vbuf = fea_T(P) * vs;
+    const int vbuf = fea5_vbuf(fea_T(P), prm.e_max);
     uint8_t* const sRec0 = smem + prm.lay[FEA_L_REC];  // [2][rec_stride]
     const int rec_stride = prm.lay[FEA_L_GU];
     uint64_t* bars = reinterpret_cast<uint64_t*>(smem + prm.lay[FEA_L_BARS]);
