@@ -583,6 +583,39 @@ fea_status fea_set_tuning(fea_ctx c, int key, int64_t value) {
     return FEA_OK;
 }
 
+// Permutation of a class's n items (C contributor offsets each, item-major) that keeps every item
+// in its aligned group of 32 and assigns each group's items to the two half-warps (16 + 16)
+// greedily, minimising repeated 8-byte banks (offset mod 16, orientation bit masked) per
+// contributor index within a half.  Phase B's sums do not depend on the item order.
+static std::vector<int32_t> half_split_order(const uint16_t* off, int n, int C) {
+    std::vector<int32_t> ord(n);
+    for (int g = 0; g < n; g += 32) {
+        const int gn = std::min(32, n - g);
+        if (gn <= 16) {
+            for (int l = 0; l < gn; ++l) ord[g + l] = g + l;
+            continue;
+        }
+        std::vector<int32_t> half[2];
+        int cnt[2][16][8] = {};  // [half][bank][q] (C <= 8 tracked; more is rare)
+        const int Cq = std::min(C, 8);
+        for (int l = 0; l < gn; ++l) {
+            const int i = g + l;
+            int cost[2] = {0, 0};
+            for (int h = 0; h < 2; ++h)
+                for (int q = 0; q < Cq; ++q) cost[h] += cnt[h][(off[(size_t)i * C + q] & 0x7fff) & 15][q];
+            int h = cost[0] <= cost[1] ? 0 : 1;
+            if ((int)half[h].size() >= 16) h ^= 1;
+            if (h == 1 && (int)half[1].size() >= gn - 16) h = 0;  // the first half is always full
+            half[h].push_back(i);
+            for (int q = 0; q < Cq; ++q) cnt[h][(off[(size_t)i * C + q] & 0x7fff) & 15][q]++;
+        }
+        int l = 0;
+        for (int h = 0; h < 2; ++h)
+            for (int32_t i : half[h]) ord[g + l++] = i;
+    }
+    return ord;
+}
+
 // Host plan of one kernel family: row blocks of this rank's rows, each with its element set
 // (ghosts first), its CSR slots and the per-slot contributor lists (ascending library element),
 // encoded as the kernel's block record.  v5 = class/item record + separate DOF array; else the
@@ -762,10 +795,13 @@ static fea_status build_blocks(fea_ctx c, bool v5, bool orient, int64_t e_max, i
             tab[4 * k2 + 1] = n;
             tab[4 * k2 + 2] = coff[k2];
             tab[4 * k2 + 3] = R;
-            // items in slot order within the class: neighbouring lanes store to nearby CSR slots
-            // (a bank-balanced reordering of the V reads measured slower: it scatters the stores)
+            // items in slot order within the class, except that each aligned group of 32 items (one
+            // warp instruction of phase B) is split into its two half-warps so that the 8-byte V
+            // reads of each half hit distinct banks where possible (64-bit shared accesses only
+            // conflict within a half-warp); the group still stores the same 32 slots
+            const std::vector<int32_t> ord = half_split_order(&contrib[cls[3 * k2 + 2]], n, C);
             for (int it = 0; it < n; ++it) {
-                const int src = it;
+                const int src = ord[it];
                 uint16_t* w = reinterpret_cast<uint16_t*>(o.rec.data() + base + coff[k2] + (size_t)it * R);
                 w[0] = items[i0 + src];
                 for (int q = 0; q < C; ++q) w[1 + q] = contrib[cls[3 * k2 + 2] + (size_t)src * C + q];

@@ -203,13 +203,7 @@ __global__ void __launch_bounds__(fea5_threads(P), 1) k_reassemble5(const __grid
         // operands stay compile-time constant-bank offsets.
         auto J = [&](int a, int k, int q) { return prm.jtab[(a * NP + k) * NQ + q]; };
         const uint32_t jset = fea5_jset(h);
-        double g00[NQ], g01[NQ], g11[NQ];  // Lambda_q A_e (the symmetric 2 x 2 per point)
-#pragma unroll
-        for (int q = 0; q < NQ; ++q) {
-            g00[q] = LC(q) * A00;
-            g01[q] = LC(q) * A01;
-            g11[q] = LC(q) * A11;
-        }
+
 #pragma unroll 1
         for (int jj = 0; jj < NJ; ++jj) {
             const int j = NS == 1 ? jj : (int)((jset >> (4 * jj)) & 15u);
@@ -219,8 +213,8 @@ __global__ void __launch_bounds__(fea5_threads(P), 1) k_reassemble5(const __grid
                 if (DO_M) y[q] = prm.ctab[j * NQ + q] * lm[q];
                 if (DO_C) {
                     const double j0 = J(0, j, q), j1 = J(1, j, q);
-                    z0[q] = fma(g00[q], j0, g01[q] * j1);
-                    z1[q] = fma(g01[q], j0, g11[q] * j1);
+                    z0[q] = LC(q) * fma(A00, j0, A01 * j1);
+                    z1[q] = LC(q) * fma(A01, j0, A11 * j1);
                 }
             }
 #pragma unroll
