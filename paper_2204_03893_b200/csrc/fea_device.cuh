@@ -253,13 +253,15 @@ __device__ __forceinline__ int u16_of(const W& w, int k) { return (word_of(w, k 
 
 // ORIENT (tensor contractions): bit 15 of an offset selects sVd (entry (i, k) with local i > k)
 // over sVc for the nonsymmetric channel; the symmetric channel ignores it.
+// `first` is this thread's first item of the class (the classes continue one round-robin over
+// the threads, so no warp takes every class's tail)
 template <int C, bool DO_M, bool DO_C, int ILP, bool ORIENT = false>
 __device__ __forceinline__ void items5(const uint8_t* __restrict__ base, int n, const double* __restrict__ sVm,
-                                       const double* __restrict__ sVc, double* om, double* oc, int tid, int nthr,
+                                       const double* __restrict__ sVc, double* om, double* oc, int first, int nthr,
                                        const double* __restrict__ sVd = nullptr) {
     using W = typename ItemWord<fea5_item_bytes(C)>::T;
     const W* it = reinterpret_cast<const W*>(base);
-    for (int i0 = tid; i0 < n; i0 += ILP * nthr) {
+    for (int i0 = first; i0 < n; i0 += ILP * nthr) {
         W w[ILP];
 #pragma unroll
         for (int u = 0; u < ILP; ++u) w[u] = it[min(i0 + u * nthr, n - 1)];  // clamped: always valid
@@ -292,9 +294,9 @@ __device__ __forceinline__ void items5(const uint8_t* __restrict__ base, int n, 
 template <bool DO_M, bool DO_C, bool ORIENT = false>
 __device__ __forceinline__ void items5_generic(const uint8_t* __restrict__ base, int C, int n, int R,
                                                const double* __restrict__ sVm, const double* __restrict__ sVc,
-                                               double* om, double* oc, int tid, int nthr,
+                                               double* om, double* oc, int first, int nthr,
                                                const double* __restrict__ sVd = nullptr) {
-    for (int i = tid; i < n; i += nthr) {
+    for (int i = first; i < n; i += nthr) {
         const uint16_t* w = reinterpret_cast<const uint16_t*>(base + (size_t)i * R);
         double am = 0.0, ac = 0.0;
         for (int q = 0; q < C; ++q) {
@@ -314,17 +316,20 @@ __device__ __forceinline__ void phase_b5(const uint8_t* __restrict__ rec, int nc
                                          const double* __restrict__ sVc, double* om, double* oc, int tid, int nthr,
                                          const double* __restrict__ sVd = nullptr) {
     const int4* cls = reinterpret_cast<const int4*>(rec);
+    int start = 0;  // items of the previous classes (mod nthr): one round-robin over all classes
     for (int k = 0; k < ncls; ++k) {
         const int4 c = cls[k];  // {C, n_items, byte offset, item bytes}
         const uint8_t* base = rec + c.z;
+        const int first = tid >= start ? tid - start : tid - start + nthr;
         switch (c.x) {
-            case 1: items5<1, DO_M, DO_C, 4, ORIENT>(base, c.y, sVm, sVc, om, oc, tid, nthr, sVd); break;
-            case 2: items5<2, DO_M, DO_C, 4, ORIENT>(base, c.y, sVm, sVc, om, oc, tid, nthr, sVd); break;
-            case 3: items5<3, DO_M, DO_C, 2, ORIENT>(base, c.y, sVm, sVc, om, oc, tid, nthr, sVd); break;
-            case 4: items5<4, DO_M, DO_C, 2, ORIENT>(base, c.y, sVm, sVc, om, oc, tid, nthr, sVd); break;
-            case 6: items5<6, DO_M, DO_C, 2, ORIENT>(base, c.y, sVm, sVc, om, oc, tid, nthr, sVd); break;
-            default: items5_generic<DO_M, DO_C, ORIENT>(base, c.x, c.y, c.w, sVm, sVc, om, oc, tid, nthr, sVd);
+            case 1: items5<1, DO_M, DO_C, 4, ORIENT>(base, c.y, sVm, sVc, om, oc, first, nthr, sVd); break;
+            case 2: items5<2, DO_M, DO_C, 4, ORIENT>(base, c.y, sVm, sVc, om, oc, first, nthr, sVd); break;
+            case 3: items5<3, DO_M, DO_C, 2, ORIENT>(base, c.y, sVm, sVc, om, oc, first, nthr, sVd); break;
+            case 4: items5<4, DO_M, DO_C, 2, ORIENT>(base, c.y, sVm, sVc, om, oc, first, nthr, sVd); break;
+            case 6: items5<6, DO_M, DO_C, 2, ORIENT>(base, c.y, sVm, sVc, om, oc, first, nthr, sVd); break;
+            default: items5_generic<DO_M, DO_C, ORIENT>(base, c.x, c.y, c.w, sVm, sVc, om, oc, first, nthr, sVd);
         }
+        start = (start + c.y) % nthr;
     }
 }
 
