@@ -255,7 +255,8 @@ __device__ __forceinline__ int u16_of(const W& w, int k) { return (word_of(w, k 
 // over sVc for the nonsymmetric channel; the symmetric channel ignores it.
 // `first` is this thread's first item of the class (the classes continue one round-robin over
 // the threads, so no warp takes every class's tail)
-template <int C, bool DO_M, bool DO_C, int ILP, bool ORIENT = false>
+// IL: V_m and V_c interleaved ({m, c} double2 at sVm[2 off]): one 16-byte load per contributor
+template <int C, bool DO_M, bool DO_C, int ILP, bool ORIENT = false, bool IL = false>
 __device__ __forceinline__ void items5(const uint8_t* __restrict__ base, int n, const double* __restrict__ sVm,
                                        const double* __restrict__ sVc, double* om, double* oc, int first, int nthr,
                                        const double* __restrict__ sVd = nullptr) {
@@ -272,8 +273,14 @@ __device__ __forceinline__ void items5(const uint8_t* __restrict__ base, int n, 
             for (int q = 0; q < C; ++q) {
                 const int raw = u16_of(w[u], 1 + q);
                 const int off = ORIENT ? (raw & 0x7fff) : raw;
-                if (DO_M) vm[u][q] = sVm[off];
-                if (DO_C) vc[u][q] = (ORIENT && (raw & 0x8000)) ? sVd[off] : sVc[off];
+                if (IL) {
+                    const double2 v = reinterpret_cast<const double2*>(sVm)[off];
+                    vm[u][q] = v.x;
+                    vc[u][q] = v.y;
+                } else {
+                    if (DO_M) vm[u][q] = sVm[off];
+                    if (DO_C) vc[u][q] = (ORIENT && (raw & 0x8000)) ? sVd[off] : sVc[off];
+                }
             }
 #pragma unroll
         for (int u = 0; u < ILP; ++u)
@@ -291,7 +298,7 @@ __device__ __forceinline__ void items5(const uint8_t* __restrict__ base, int n, 
     }
 }
 
-template <bool DO_M, bool DO_C, bool ORIENT = false>
+template <bool DO_M, bool DO_C, bool ORIENT = false, bool IL = false>
 __device__ __forceinline__ void items5_generic(const uint8_t* __restrict__ base, int C, int n, int R,
                                                const double* __restrict__ sVm, const double* __restrict__ sVc,
                                                double* om, double* oc, int first, int nthr,
@@ -302,8 +309,14 @@ __device__ __forceinline__ void items5_generic(const uint8_t* __restrict__ base,
         for (int q = 0; q < C; ++q) {
             const int raw = w[1 + q];
             const int off = ORIENT ? (raw & 0x7fff) : raw;
-            if (DO_M) am += sVm[off];
-            if (DO_C) ac += (ORIENT && (raw & 0x8000)) ? sVd[off] : sVc[off];
+            if (IL) {
+                const double2 v = reinterpret_cast<const double2*>(sVm)[off];
+                am += v.x;
+                ac += v.y;
+            } else {
+                if (DO_M) am += sVm[off];
+                if (DO_C) ac += (ORIENT && (raw & 0x8000)) ? sVd[off] : sVc[off];
+            }
         }
         if (DO_M) om[w[0]] = am;
         if (DO_C) oc[w[0]] = ac;
@@ -311,7 +324,7 @@ __device__ __forceinline__ void items5_generic(const uint8_t* __restrict__ base,
 }
 
 // the classes of one block, threads tid of nthr (a block's B is split across all warps)
-template <bool DO_M, bool DO_C, bool ORIENT = false>
+template <bool DO_M, bool DO_C, bool ORIENT = false, bool IL = false>
 __device__ __forceinline__ void phase_b5(const uint8_t* __restrict__ rec, int ncls, const double* __restrict__ sVm,
                                          const double* __restrict__ sVc, double* om, double* oc, int tid, int nthr,
                                          const double* __restrict__ sVd = nullptr) {
@@ -322,12 +335,12 @@ __device__ __forceinline__ void phase_b5(const uint8_t* __restrict__ rec, int nc
         const uint8_t* base = rec + c.z;
         const int first = tid >= start ? tid - start : tid - start + nthr;
         switch (c.x) {
-            case 1: items5<1, DO_M, DO_C, 4, ORIENT>(base, c.y, sVm, sVc, om, oc, first, nthr, sVd); break;
-            case 2: items5<2, DO_M, DO_C, 4, ORIENT>(base, c.y, sVm, sVc, om, oc, first, nthr, sVd); break;
-            case 3: items5<3, DO_M, DO_C, 2, ORIENT>(base, c.y, sVm, sVc, om, oc, first, nthr, sVd); break;
-            case 4: items5<4, DO_M, DO_C, 2, ORIENT>(base, c.y, sVm, sVc, om, oc, first, nthr, sVd); break;
-            case 6: items5<6, DO_M, DO_C, 2, ORIENT>(base, c.y, sVm, sVc, om, oc, first, nthr, sVd); break;
-            default: items5_generic<DO_M, DO_C, ORIENT>(base, c.x, c.y, c.w, sVm, sVc, om, oc, first, nthr, sVd);
+            case 1: items5<1, DO_M, DO_C, 4, ORIENT, IL>(base, c.y, sVm, sVc, om, oc, first, nthr, sVd); break;
+            case 2: items5<2, DO_M, DO_C, 4, ORIENT, IL>(base, c.y, sVm, sVc, om, oc, first, nthr, sVd); break;
+            case 3: items5<3, DO_M, DO_C, 2, ORIENT, IL>(base, c.y, sVm, sVc, om, oc, first, nthr, sVd); break;
+            case 4: items5<4, DO_M, DO_C, 2, ORIENT, IL>(base, c.y, sVm, sVc, om, oc, first, nthr, sVd); break;
+            case 6: items5<6, DO_M, DO_C, 2, ORIENT, IL>(base, c.y, sVm, sVc, om, oc, first, nthr, sVd); break;
+            default: items5_generic<DO_M, DO_C, ORIENT, IL>(base, c.x, c.y, c.w, sVm, sVc, om, oc, first, nthr, sVd);
         }
         start = (start + c.y) % nthr;
     }

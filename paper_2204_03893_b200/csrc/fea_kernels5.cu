@@ -221,21 +221,24 @@ __global__ void __launch_bounds__(fea5_threads(P), 1) k_reassemble5(const __grid
             for (int i = 0; i < NP; ++i) {
                 if (i > j) break;
                 const int t = i * NP - i * (i - 1) / 2 + (j - i);  // row-major upper triangle
+                double m = 0.0, c0 = 0.0, c1 = 0.0;  // c: two chains (ILP)
                 if (DO_M) {
-                    double m = 0.0;
 #pragma unroll
                     for (int q = 0; q < NQ; ++q) m = fma(prm.ctab[i * NQ + q], y[q], m);
-                    sVm[t * vs + le] = m;
                 }
                 if (DO_C) {
-                    double c0 = 0.0, c1 = 0.0;  // two chains (ILP)
 #pragma unroll
                     for (int q = 0; q < NQ; ++q) {
                         c0 = fma(J(0, i, q), z0[q], c0);
                         c1 = fma(J(1, i, q), z1[q], c1);
                     }
-                    sVc[t * vs + le] = c0 + c1;
                 }
+                if (DO_M && DO_C)  // interleaved {m, c}: one 16-byte load per contributor in B
+                    reinterpret_cast<double2*>(sVm)[t * vs + le] = make_double2(m, c0 + c1);
+                else if (DO_M)
+                    sVm[t * vs + le] = m;
+                else
+                    sVc[t * vs + le] = c0 + c1;
             }
         }
     };
@@ -298,7 +301,7 @@ __global__ void __launch_bounds__(fea5_threads(P), 1) k_reassemble5(const __grid
                 }
                 if (s + PF < nb) prefetch_blk(s + PF);
             }
-            double* sVm = sVm0 + b * vbuf;
+            double* sVm = sVm0 + b * (DO_M && DO_C ? 2 : 1) * vbuf;  // M + K: one interleaved region
             double* sVc = sVc0 + b * vbuf;
             while (cs == s) {
                 const int le = (cu / NS) * 32 + lane;
@@ -323,7 +326,8 @@ __global__ void __launch_bounds__(fea5_threads(P), 1) k_reassemble5(const __grid
             {
                 double* om = DO_M ? prm.out_m + bk.slot0 : nullptr;
                 double* oc = DO_C ? prm.out_c + bk.slot0 : nullptr;
-                phase_b5<DO_M, DO_C>(sRec0 + b * rec_stride, bk.ncls, sVm0 + b * vbuf, sVc0 + b * vbuf, om, oc, tid,
+                phase_b5<DO_M, DO_C, false, DO_M && DO_C>(sRec0 + b * rec_stride, bk.ncls,
+                                     sVm0 + b * (DO_M && DO_C ? 2 : 1) * vbuf, sVc0 + b * vbuf, om, oc, tid,
                                      NW * 32);
             }
             tick(4);
