@@ -120,6 +120,7 @@ struct fea_ctx_s {
     // tuning
     int64_t tune_smem = 0;
     int tune_kver = 0;     // 0 = automatic, 4 = force kernel v4
+    int tune_lpt = 0;      // v5: LPT block order for few blocks per CTA (FEA_TUNE_LPT; measured no gain on C2)
     int64_t tune_emax = 0; // v5 element cap per block (0 = from the budget)
 
     // reassemble buffers
@@ -568,6 +569,10 @@ fea_status fea_set_tuning(fea_ctx c, int key, int64_t value) {
             if (value < 0 || value > 65535) return c->fail(FEA_E_ARG, "element cap out of range");
             c->tune_emax = value;
             break;
+        case 6:  // v5 LPT block order on (1, default) / off (0)
+            if (value != 0 && value != 1) return c->fail(FEA_E_ARG, "LPT flag must be 0 or 1");
+            c->tune_lpt = (int)value;
+            break;
         case 5:  // exchange of u between ranks: 0 = interface-only, 1 = full allgather
             if (value != 0 && value != 1) return c->fail(FEA_E_ARG, "exchange must be 0 or 1");
             c->exchange = (int)value;
@@ -1010,6 +1015,29 @@ fea_status fea_build_pattern(fea_ctx c, int64_t* row_begin, int64_t* n_rows_loca
     if (rc != 0) return c->fail(FEA_E_CUDA, "occupancy query: %s", cudaGetErrorString((cudaError_t)rc));
     if (occ < 1) return c->fail(FEA_E_UNSUPPORTED, "kernel does not fit: %d B shared memory", c->smem_bytes);
     c->grid = (int)std::min<int64_t>(std::max<int64_t>(nb, 1), (int64_t)occ * c->sm_count);
+    if (v5 && nb > c->grid && nb <= 16LL * c->grid && c->tune_lpt) {
+        // few blocks per CTA: the static schedule (CTA g runs blocks g, g + grid, ...) is balanced
+        // by an LPT order: blocks by descending cost estimate, each to the least-loaded CTA that
+        // still has a free position (CTA g has ceil/floor(nb / grid) positions).  Results do not
+        // depend on the order (disjoint slots, fixed per-slot order).
+        const int64_t G = c->grid;
+        std::vector<int64_t> idx(nb), cap(G), pos(G, 0);
+        std::vector<double> load(G, 0.0), cost(nb);
+        for (int64_t b = 0; b < nb; ++b) cost[b] = (double)blocks[b].nE * T + 0.5 * blocks[b].nslots;
+        std::iota(idx.begin(), idx.end(), 0);
+        std::stable_sort(idx.begin(), idx.end(), [&](int64_t a, int64_t b) { return cost[a] > cost[b]; });
+        for (int64_t g = 0; g < G; ++g) cap[g] = (nb - 1 - g) / G + 1;
+        std::vector<FeaBlock> perm(nb);
+        for (int64_t b : idx) {
+            int64_t best = -1;
+            for (int64_t g = 0; g < G; ++g)
+                if (pos[g] < cap[g] && (best < 0 || load[g] < load[best])) best = g;
+            perm[best + pos[best] * G] = blocks[b];
+            pos[best]++;
+            load[best] += cost[b];
+        }
+        FEA_CUDA(c, cudaMemcpy(c->d_blocks, perm.data(), nb * sizeof(FeaBlock), cudaMemcpyHostToDevice));
+    }
     c->have_plan = true;
     if (row_begin) *row_begin = R0;
     if (n_rows_local) *n_rows_local = nr;
