@@ -120,6 +120,11 @@ fea_status fea_build_pattern(fea_ctx ctx, int64_t* row_begin, int64_t* n_rows_lo
  * (nnz_local, int32, global library columns).  Host pointers. */
 fea_status fea_get_pattern(fea_ctx ctx, int64_t* row_ptr, int32_t* col_idx);
 
+/* Rows [r0, r1) of the local pattern (0 <= r0 <= r1 <= n_rows_local): row_ptr (host, r1 - r0 + 1
+ * int64, the local offsets row_ptr[r0 .. r1], not rebased) and col_idx (host, row_ptr[r1] -
+ * row_ptr[r0] int32).  Either may be NULL.  For checking large patterns window by window. */
+fea_status fea_get_pattern_rows(fea_ctx ctx, int64_t r0, int64_t r1, int64_t* row_ptr, int32_t* col_idx);
+
 /* lib_to_user[l] = user DOF id of library DOF l (host, n_dof). */
 fea_status fea_get_dof_perm(fea_ctx ctx, int64_t* lib_to_user);
 

@@ -1053,6 +1053,17 @@ fea_status fea_get_pattern(fea_ctx c, int64_t* row_ptr, int32_t* col_idx) {
     return FEA_OK;
 }
 
+fea_status fea_get_pattern_rows(fea_ctx c, int64_t r0, int64_t r1, int64_t* row_ptr, int32_t* col_idx) {
+    if (!c) return FEA_E_ARG;
+    if (!c->have_plan) return c->fail(FEA_E_STATE, "get_pattern_rows before build_pattern");
+    if (r0 < 0 || r1 < r0 || r1 > c->n_rows) return c->fail(FEA_E_ARG, "row range [%lld, %lld) outside [0, %lld)",
+                                                           (long long)r0, (long long)r1, (long long)c->n_rows);
+    if (row_ptr) std::memcpy(row_ptr, c->row_ptr.data() + r0, (size_t)(r1 - r0 + 1) * sizeof(int64_t));
+    if (col_idx && r1 > r0)
+        std::memcpy(col_idx, c->col_idx.data() + c->row_ptr[r0], (size_t)(c->row_ptr[r1] - c->row_ptr[r0]) * sizeof(int32_t));
+    return FEA_OK;
+}
+
 fea_status fea_get_dof_perm(fea_ctx c, int64_t* lib_to_user) {
     if (!c || !lib_to_user) return FEA_E_ARG;
     if (!c->have_mesh) return c->fail(FEA_E_STATE, "get_dof_perm before mesh_upload");

@@ -24,7 +24,7 @@ FEA_TUNE_SMEM_BUDGET, FEA_TUNE_KERNEL, FEA_TUNE_EMAX, FEA_TUNE_PLAN_WHICH = 1, 2
 
 # the exported C symbols (tests check every one of them against include/fea.h)
 SYMBOLS = ["fea_create", "fea_set_element", "fea_mesh_upload", "fea_set_tuning", "fea_build_pattern",
-           "fea_get_pattern", "fea_get_dof_perm", "fea_get_elem_perm", "fea_set_coefficient",
+           "fea_get_pattern", "fea_get_pattern_rows", "fea_get_dof_perm", "fea_get_elem_perm", "fea_set_coefficient",
            "fea_assemble_mass", "fea_assemble_stiffness", "fea_assemble", "fea_reassemble",
            "fea_reassemble_host", "fea_assemble_tensor", "fea_get_interface", "fea_exchange_pack",
            "fea_exchange_unpack", "fea_nccl_unique_id", "fea_set_nccl", "fea_sync", "fea_get_stat",
@@ -56,6 +56,7 @@ def load_library():
         "fea_set_tuning": [P, I, L],
         "fea_build_pattern": [P, P, P, P],
         "fea_get_pattern": [P, P, P],
+        "fea_get_pattern_rows": [P, L, L, P, P],
         "fea_get_dof_perm": [P, P],
         "fea_get_elem_perm": [P, P],
         "fea_set_coefficient": [P, I, I, I, P],
@@ -175,6 +176,14 @@ class Context:
         ci = np.zeros(max(self.nnz, 1), dtype=np.int32)
         self._check(self._lib.fea_get_pattern(self._h, _np_ptr(rp), _np_ptr(ci)))
         return rp, ci[: self.nnz]
+
+    def get_pattern_rows(self, r0: int, r1: int):
+        """Local rows [r0, r1): (row_ptr[r0..r1] (not rebased), col_idx of those rows)."""
+        rp = np.zeros(r1 - r0 + 1, dtype=np.int64)
+        self._check(self._lib.fea_get_pattern_rows(self._h, int(r0), int(r1), _np_ptr(rp), None))
+        ci = np.zeros(max(int(rp[-1] - rp[0]), 1), dtype=np.int32)
+        self._check(self._lib.fea_get_pattern_rows(self._h, int(r0), int(r1), _np_ptr(rp), _np_ptr(ci)))
+        return rp, ci[: int(rp[-1] - rp[0])]
 
     def get_dof_perm(self):
         p = np.zeros(self.n_dof, dtype=np.int64)

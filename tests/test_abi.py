@@ -120,3 +120,21 @@ def test_config_nnz_matches_survey():
         w = make_workload(cfg)
         ctx = _plan(w.mesh, cfg.p)
         assert ctx.nnz == {"C1": 7361, "C2": 3018753}[name]
+
+
+def test_pattern_rows_window_matches_full_pattern():
+    """fea_get_pattern_rows returns the rows [r0, r1) of the full local pattern (planning-only)."""
+    from fea_inputs import triangle_rule
+    from fea_inputs.mesh import random_mesh_from_structured
+    from paper_2204_03893_b200.fea import Context
+    m = random_mesh_from_structured(9, 2, seed=5)
+    ctx = Context(device=-1)
+    ctx.set_element(2, *triangle_rule(4))
+    ctx.mesh_upload(m.vert_xy, m.elem_vert, m.n_dof, m.elem_dof)
+    ctx.build_pattern()
+    rp, ci = ctx.get_pattern()
+    for r0, r1 in ((0, 5), (17, 60), (m.n_dof - 9, m.n_dof), (12, 12)):
+        wrp, wci = ctx.get_pattern_rows(r0, r1)
+        assert np.array_equal(wrp, rp[r0:r1 + 1])
+        assert np.array_equal(wci, ci[rp[r0]:rp[r1]])
+    ctx.close()
