@@ -1015,6 +1015,8 @@ fea_status fea_build_pattern(fea_ctx c, int64_t* row_begin, int64_t* n_rows_loca
     if (rc != 0) return c->fail(FEA_E_CUDA, "occupancy query: %s", cudaGetErrorString((cudaError_t)rc));
     if (occ < 1) return c->fail(FEA_E_UNSUPPORTED, "kernel does not fit: %d B shared memory", c->smem_bytes);
     c->grid = (int)std::min<int64_t>(std::max<int64_t>(nb, 1), (int64_t)occ * c->sm_count);
+    // our kernels per fea_reassemble: the assembly, plus pack + unpack of the exchange (world > 1)
+    c->launches_per_call = 1 + (c->world > 1 && c->exchange == 0 ? 2 : 0);
     if (v5 && nb > c->grid && nb <= 16LL * c->grid && c->tune_lpt) {
         // few blocks per CTA: the static schedule (CTA g runs blocks g, g + grid, ...) is balanced
         // by an LPT order: blocks by descending cost estimate, each to the least-loaded CTA that
