@@ -4,6 +4,9 @@
 #include <cstdint>
 
 #define FEA_MAX_ORDER 4
+#ifndef FEA5_SPEC
+#define FEA5_SPEC 0  // kernel v5: warp-specialised A / B (1; measured slower) or every warp does both (0)
+#endif
 #ifndef FEA5_NS2
 #define FEA5_NS2 2  // units per P2 tile in kernel v5 (column halves)
 #endif
