@@ -93,6 +93,14 @@ fea_status fea_create(fea_ctx* out, int cuda_device, void* stream, int rank, int
  * Errors: FEA_E_ARG (NULL, weights), FEA_E_UNSUPPORTED (order, n_q). */
 fea_status fea_set_element(fea_ctx ctx, int order, int n_q, const double* q_xy, const double* q_w);
 
+/* Separate quadrature rules per matrix ("a specific quadrature rule may be used
+ * for each matrix").  After fea_set_element (which sets one rule for both),
+ * replace the rule of the matrices in `which` (FEA_MASS, FEA_STIFF or both) by (n_q, q_xy, q_w),
+ * same conventions and errors as fea_set_element.  Keeps the mesh; invalidates the pattern (call
+ * fea_build_pattern again).  With two different rules every assembly runs one pass per matrix on
+ * kernel v4 (any rule); fea_assemble_tensor uses the rule of M for (M o2 v), of C for (C o2 v). */
+fea_status fea_set_rule(fea_ctx ctx, int which, int n_q, const double* q_xy, const double* q_w);
+
 /* Mesh (Algorithm 2 line 4): vertices a, b, c per element and
  * index sets N_e in the documented local order (reading 7).
  *   vert_xy  : host, n_vert x 2 float64

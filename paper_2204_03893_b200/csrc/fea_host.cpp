@@ -79,6 +79,13 @@ struct fea_ctx_s {
     int order = 0, np = 0, nq = 0, T = 0;
     std::vector<double> qxy, qw, tables, qfrag, jplain;  // tables = Phi, w; jplain = J (kernel parameters)
     double* d_ttab = nullptr;                             // tensor kernel: Phi, J0, J1 [np][16], w [16]
+    // separate quadrature rules per matrix (NEXT-4): the fields above hold the
+    // rule of M; when `split`, these hold the rule of C (both rules run on kernel v4, one pass each)
+    bool split = false;
+    int nq_c = 0;
+    std::vector<double> qxy_c, qw_c, tables_c, qfrag_c, jplain_c;
+    double* d_tables_c = nullptr;
+    double* d_ttab_c = nullptr;
 
     // mesh, library numbering
     bool have_mesh = false;
@@ -387,6 +394,8 @@ void fea_destroy(fea_ctx c) {
     c->free_mesh();
     dfree(c->d_tables);
     dfree(c->d_ttab);
+    dfree(c->d_tables_c);
+    dfree(c->d_ttab_c);
     dfree(c->d_dbg);
     if (c->comm && nccl().ok) nccl().commDestroy((ncclComm_t)c->comm);
     delete c;
@@ -394,25 +403,55 @@ void fea_destroy(fea_ctx c) {
 
 const char* fea_last_error(fea_ctx c) { return c ? c->err.c_str() : "null context"; }
 
-fea_status fea_set_element(fea_ctx c, int order, int n_q, const double* q_xy, const double* q_w) {
-    if (!c) return FEA_E_ARG;
-    if (!q_xy || !q_w) return c->fail(FEA_E_ARG, "set_element: NULL rule arrays");
-    if (order < 1 || order > FEA_MAX_ORDER) return c->fail(FEA_E_UNSUPPORTED, "order %d not in 1..4", order);
+// Rule checks and tables (Algorithm 2 lines 1-3) of one quadrature rule; device copies of the v4
+// fragments and of the tensor kernel's tables.
+static fea_status make_rule(fea_ctx c, int order, int n_q, const double* q_xy, const double* q_w,
+                            std::vector<double>& ctab, std::vector<double>& qfrag, std::vector<double>& jplain) {
+    if (!q_xy || !q_w) return c->fail(FEA_E_ARG, "NULL rule arrays");
     if (n_q < 1 || n_q > FEA_MAX_NQ) return c->fail(FEA_E_UNSUPPORTED, "n_q %d not in 1..16", n_q);
     long double s = 0;
     for (int q = 0; q < n_q; ++q) {
         if (!std::isfinite(q_w[q]) || !std::isfinite(q_xy[2 * q]) || !std::isfinite(q_xy[2 * q + 1]))
-            return c->fail(FEA_E_ARG, "set_element: non-finite rule entry %d", q);
+            return c->fail(FEA_E_ARG, "non-finite rule entry %d", q);
         s += q_w[q];
     }
     if (fabsl(s - 0.5L) > 1e-14L)
         return c->fail(FEA_E_ARG, "quadrature weights sum to %.17g, expected 1/2 (reference-triangle measure)", (double)s);
-    std::vector<double> ctab, qfrag, jplain;
     if (!build_tables(order, n_q, q_xy, q_w, ctab, qfrag, jplain)) return c->fail(FEA_E_UNSUPPORTED, "singular Vandermonde");
     if (ctab.size() > FEA_CTAB_MAX) return c->fail(FEA_E_UNSUPPORTED, "tables exceed the parameter bank");
+    return FEA_OK;
+}
+
+static fea_status upload_rule(fea_ctx c, int n_q, const std::vector<double>& ctab, const std::vector<double>& qfrag,
+                              const std::vector<double>& jplain, double*& d_qfrag, double*& d_ttab) {
+    dfree(d_qfrag);
+    dfree(d_ttab);
+    if (c->host_only) return FEA_OK;
+    FEA_CUDA(c, cudaMalloc(&d_qfrag, qfrag.size() * sizeof(double)));
+    FEA_CUDA(c, cudaMemcpy(d_qfrag, qfrag.data(), qfrag.size() * sizeof(double), cudaMemcpyHostToDevice));
+    const int np = c->np;  // tensor kernel tables: Phi, J0, J1 [np][16], w [16], zero padded
+    std::vector<double> tt((size_t)3 * np * 16 + 16, 0.0);
+    for (int i = 0; i < np; ++i)
+        for (int q = 0; q < n_q; ++q) {
+            tt[(size_t)i * 16 + q] = ctab[(size_t)i * n_q + q];
+            tt[(size_t)(np + i) * 16 + q] = jplain[(size_t)i * n_q + q];
+            tt[(size_t)(2 * np + i) * 16 + q] = jplain[(size_t)(np + i) * n_q + q];
+        }
+    const size_t oW = ((size_t)np * n_q + 1) & ~size_t(1);
+    for (int q = 0; q < n_q; ++q) tt[(size_t)3 * np * 16 + q] = ctab[oW + q];
+    FEA_CUDA(c, cudaMalloc(&d_ttab, tt.size() * sizeof(double)));
+    FEA_CUDA(c, cudaMemcpy(d_ttab, tt.data(), tt.size() * sizeof(double), cudaMemcpyHostToDevice));
+    return FEA_OK;
+}
+
+fea_status fea_set_element(fea_ctx c, int order, int n_q, const double* q_xy, const double* q_w) {
+    if (!c) return FEA_E_ARG;
+    if (order < 1 || order > FEA_MAX_ORDER) return c->fail(FEA_E_UNSUPPORTED, "order %d not in 1..4", order);
+    std::vector<double> ctab, qfrag, jplain;
+    fea_status st = make_rule(c, order, n_q, q_xy, q_w, ctab, qfrag, jplain);
+    if (st != FEA_OK) return st;
     if (!c->host_only) cudaSetDevice(c->device);
     c->free_mesh();
-    dfree(c->d_tables);
     c->order = order;
     c->nq = n_q;
     c->np = (order + 1) * (order + 2) / 2;
@@ -422,23 +461,71 @@ fea_status fea_set_element(fea_ctx c, int order, int n_q, const double* q_xy, co
     c->tables = ctab;
     c->qfrag = qfrag;
     c->jplain = jplain;
-    if (c->host_only) return FEA_OK;
-    FEA_CUDA(c, cudaMalloc(&c->d_tables, qfrag.size() * sizeof(double)));
-    FEA_CUDA(c, cudaMemcpy(c->d_tables, qfrag.data(), qfrag.size() * sizeof(double), cudaMemcpyHostToDevice));
-    {  // tensor kernel tables: Phi, J0, J1 [np][16], w [16], zero padded
-        const int np = c->np;
-        std::vector<double> tt((size_t)3 * np * 16 + 16, 0.0);
-        for (int i = 0; i < np; ++i)
-            for (int q = 0; q < n_q; ++q) {
-                tt[(size_t)i * 16 + q] = ctab[(size_t)i * n_q + q];
-                tt[(size_t)(np + i) * 16 + q] = jplain[(size_t)i * n_q + q];
-                tt[(size_t)(2 * np + i) * 16 + q] = jplain[(size_t)(np + i) * n_q + q];
-            }
-        const size_t oW = ((size_t)np * n_q + 1) & ~size_t(1);
-        for (int q = 0; q < n_q; ++q) tt[(size_t)3 * np * 16 + q] = ctab[oW + q];
-        dfree(c->d_ttab);
-        FEA_CUDA(c, cudaMalloc(&c->d_ttab, tt.size() * sizeof(double)));
-        FEA_CUDA(c, cudaMemcpy(c->d_ttab, tt.data(), tt.size() * sizeof(double), cudaMemcpyHostToDevice));
+    c->split = false;
+    dfree(c->d_tables_c);
+    dfree(c->d_ttab_c);
+    return upload_rule(c, n_q, ctab, qfrag, jplain, c->d_tables, c->d_ttab);
+}
+
+fea_status fea_set_rule(fea_ctx c, int which, int n_q, const double* q_xy, const double* q_w) {
+    if (!c) return FEA_E_ARG;
+    if (c->order == 0) return c->fail(FEA_E_STATE, "set_rule before set_element");
+    if (which < 1 || which > 3) return c->fail(FEA_E_ARG, "which must be a nonzero FEA_MASS|FEA_STIFF mask");
+    if (which == (FEA_MASS | FEA_STIFF)) {  // one rule for both: as set_element, keeping the mesh
+        std::vector<double> ctab, qfrag, jplain;
+        fea_status st = make_rule(c, c->order, n_q, q_xy, q_w, ctab, qfrag, jplain);
+        if (st != FEA_OK) return st;
+        if (!c->host_only) cudaSetDevice(c->device);
+        c->free_plan();
+        c->nq = n_q;
+        c->qxy.assign(q_xy, q_xy + 2 * n_q);
+        c->qw.assign(q_w, q_w + n_q);
+        c->tables = ctab;
+        c->qfrag = qfrag;
+        c->jplain = jplain;
+        c->split = false;
+        dfree(c->d_tables_c);
+        dfree(c->d_ttab_c);
+        return upload_rule(c, n_q, ctab, qfrag, jplain, c->d_tables, c->d_ttab);
+    }
+    std::vector<double> ctab, qfrag, jplain;
+    fea_status st = make_rule(c, c->order, n_q, q_xy, q_w, ctab, qfrag, jplain);
+    if (st != FEA_OK) return st;
+    if (!c->host_only) cudaSetDevice(c->device);
+    c->free_plan();
+    if (!c->split) {  // C keeps the current (common) rule
+        c->nq_c = c->nq;
+        c->qxy_c = c->qxy;
+        c->qw_c = c->qw;
+        c->tables_c = c->tables;
+        c->qfrag_c = c->qfrag;
+        c->jplain_c = c->jplain;
+        st = upload_rule(c, c->nq_c, c->tables_c, c->qfrag_c, c->jplain_c, c->d_tables_c, c->d_ttab_c);
+        if (st != FEA_OK) return st;
+        c->split = true;
+    }
+    if (which == FEA_MASS) {
+        c->nq = n_q;
+        c->qxy.assign(q_xy, q_xy + 2 * n_q);
+        c->qw.assign(q_w, q_w + n_q);
+        c->tables = ctab;
+        c->qfrag = qfrag;
+        c->jplain = jplain;
+        st = upload_rule(c, n_q, ctab, qfrag, jplain, c->d_tables, c->d_ttab);
+    } else {
+        c->nq_c = n_q;
+        c->qxy_c.assign(q_xy, q_xy + 2 * n_q);
+        c->qw_c.assign(q_w, q_w + n_q);
+        c->tables_c = ctab;
+        c->qfrag_c = qfrag;
+        c->jplain_c = jplain;
+        st = upload_rule(c, n_q, ctab, qfrag, jplain, c->d_tables_c, c->d_ttab_c);
+    }
+    if (st != FEA_OK) return st;
+    if (c->nq == c->nq_c && c->qxy == c->qxy_c && c->qw == c->qw_c) {  // the same rule again
+        c->split = false;
+        dfree(c->d_tables_c);
+        dfree(c->d_ttab_c);
     }
     return FEA_OK;
 }
@@ -899,7 +986,7 @@ fea_status fea_build_pattern(fea_ctx c, int64_t* row_begin, int64_t* n_rows_loca
     // ---- shared-memory budget -> elements per block (e_max) and record budget
     const int dm = (c->plan_which & FEA_MASS) ? 1 : 0, dcm = (c->plan_which & FEA_STIFF) ? 1 : 0;
     const int nmat = dm + dcm;
-    const bool v5 = fea5_supported(c->order, nq) && c->tune_kver != 4;
+    const bool v5 = fea5_supported(c->order, nq) && c->tune_kver != 4 && !c->split;
     c->kver = v5 ? 5 : 4;
     const int rstages = c->order <= 2 ? 3 : 2;  // fea_rstages (v4)
     int64_t e_max, rec_budget;
@@ -914,7 +1001,7 @@ fea_status fea_build_pattern(fea_ctx c, int64_t* row_begin, int64_t* n_rows_loca
     } else {
         const int ctas = c->order <= 2 ? 2 : 1;  // fea_ctas
         const int64_t budget = c->tune_smem ? c->tune_smem : (ctas == 2 ? 113 * 1024 : 226 * 1024);
-        const int nqp = 4 * fea_nk_kernel(c->order, nq);
+        const int nqp = c->split ? 16 : 4 * fea_nk_kernel(c->order, nq);  // split rules: room for either
         const int64_t per_el_smem = 8LL * T * nmat + 2 * (8LL * np + 48) + 2 * 8LL * nqp + 32;
         const double rec_el = 1.3 * (3.0 * np * np + 4.0 * np) + 8;  // record bytes per element (estimate)
         e_max = (int64_t)((budget - 256 - 3 * 128 - 16LL * T * nmat) / (per_el_smem + rstages * rec_el));
@@ -939,7 +1026,7 @@ fea_status fea_build_pattern(fea_ctx c, int64_t* row_begin, int64_t* n_rows_loca
     const int64_t visits = P.visits, owned = P.owned, ncon = P.ncon, rbytes = P.rbytes;
     int32_t L[FEA_L_N];
     if (v5) fea5_smem_layout(L, (int)rec_max, (int)e_max, c->order, dm, dcm);
-    else fea_smem_layout(L, rstages, (int)rec_max, (int)e_max, c->order, nq, dm, dcm);
+    else fea_smem_layout(L, rstages, (int)rec_max, (int)e_max, c->order, c->split ? 0 : nq, dm, dcm);
     c->nblocks = (int)nb;
     c->e_max = (int)e_max;
     c->rec_max = (int)rec_max;
@@ -1108,24 +1195,26 @@ static bool same_coef(const FeaCoef& a, const FeaCoef& b) {
     return true;
 }
 
-static fea_status launch(fea_ctx c, const double* u, double* vm, double* vc) {
+// rule_c: run with the rule of C (split rules; vm must then be NULL)
+static fea_status launch(fea_ctx c, const double* u, double* vm, double* vc, bool rule_c = false) {
     FeaKParams prm{};
     prm.blocks = c->d_blocks;
     prm.records = c->d_records;
     prm.xy = c->d_xy;
     prm.dofs = c->d_dofs;
     prm.u = u;
-    prm.qfrag = c->d_tables;
+    prm.qfrag = rule_c ? c->d_tables_c : c->d_tables;
     prm.out_m = vm;
     prm.out_c = vc;
     prm.nblocks = c->nblocks;
     prm.e_max = c->e_max;
-    prm.nq = c->nq;
+    prm.nq = rule_c ? c->nq_c : c->nq;
     prm.same_coef = same_coef(c->coef_m, c->coef_c) ? 1 : 0;
     std::memcpy(prm.lay, c->lay, sizeof(prm.lay));
     prm.coef_m = c->coef_m;
     prm.coef_c = c->coef_c;
-    std::memcpy(prm.ctab, c->tables.data(), c->tables.size() * sizeof(double));
+    const std::vector<double>& tab = rule_c ? c->tables_c : c->tables;
+    std::memcpy(prm.ctab, tab.data(), tab.size() * sizeof(double));
     if (c->kver == 5) std::memcpy(prm.jtab, c->jplain.data(), c->jplain.size() * sizeof(double));
     if (const char* dm = getenv("FEA_DEBUG_MODE")) prm.dbg_mode = atoi(dm);
     if (getenv("FEA_DEBUG_TIMING")) {
@@ -1153,6 +1242,10 @@ fea_status fea_assemble(fea_ctx c, const double* u_full, double* mass_vals, doub
     cudaSetDevice(c->device);
     const bool pm = c->plan_which & FEA_MASS, pc = c->plan_which & FEA_STIFF;
     fea_status s;
+    if (c->split) {  // separate rules: one pass per matrix, each with its rule's tables
+        if (mass_vals && (s = launch(c, u_full, mass_vals, nullptr)) != FEA_OK) return s;
+        return stiff_vals ? launch(c, u_full, nullptr, stiff_vals, true) : FEA_OK;
+    }
     if (mass_vals && stiff_vals && !(pm && pc)) {  // plan sized for one matrix: two passes
         if ((s = launch(c, u_full, mass_vals, nullptr)) != FEA_OK) return s;
         return launch(c, u_full, nullptr, stiff_vals);
@@ -1323,15 +1416,25 @@ fea_status fea_assemble_tensor(fea_ctx c, const double* u_full, const double* v_
     prm.v = v_full;
     prm.tab = c->d_ttab;
     prm.out_m = mt_vals;
-    prm.out_c = ct_vals;
+    prm.out_c = c->split ? nullptr : ct_vals;
     prm.nblocks = c->t_nblocks;
     prm.e_max = c->t_emax;
     prm.nq = c->nq;
     std::memcpy(prm.lay, c->t_lay, sizeof(prm.lay));
     prm.coef_m = c->coef_m;
     prm.coef_c = c->coef_c;
-    const int rc = fea_launch_tensor(prm, c->order, c->t_smem, c->t_grid, c->stream);
-    if (rc != 0) return c->fail(FEA_E_CUDA, "k_tensor launch: %s", cudaGetErrorString((cudaError_t)rc));
+    if (prm.out_m || prm.out_c) {
+        const int rc = fea_launch_tensor(prm, c->order, c->t_smem, c->t_grid, c->stream);
+        if (rc != 0) return c->fail(FEA_E_CUDA, "k_tensor launch: %s", cudaGetErrorString((cudaError_t)rc));
+    }
+    if (c->split && ct_vals) {  // C o2 v with the rule of C
+        prm.tab = c->d_ttab_c;
+        prm.nq = c->nq_c;
+        prm.out_m = nullptr;
+        prm.out_c = ct_vals;
+        const int rc = fea_launch_tensor(prm, c->order, c->t_smem, c->t_grid, c->stream);
+        if (rc != 0) return c->fail(FEA_E_CUDA, "k_tensor launch: %s", cudaGetErrorString((cudaError_t)rc));
+    }
     return FEA_OK;
 }
 

@@ -23,7 +23,7 @@ FEA_K_POLY, FEA_K_EXP, FEA_K_PWL = 0, 1, 2
 FEA_TUNE_SMEM_BUDGET, FEA_TUNE_KERNEL, FEA_TUNE_EMAX, FEA_TUNE_PLAN_WHICH = 1, 2, 3, 4
 
 # the exported C symbols (tests check every one of them against include/fea.h)
-SYMBOLS = ["fea_create", "fea_set_element", "fea_mesh_upload", "fea_set_tuning", "fea_build_pattern",
+SYMBOLS = ["fea_create", "fea_set_element", "fea_set_rule", "fea_mesh_upload", "fea_set_tuning", "fea_build_pattern",
            "fea_get_pattern", "fea_get_pattern_rows", "fea_get_dof_perm", "fea_get_elem_perm", "fea_set_coefficient",
            "fea_assemble_mass", "fea_assemble_stiffness", "fea_assemble", "fea_reassemble",
            "fea_reassemble_host", "fea_assemble_tensor", "fea_get_interface", "fea_exchange_pack",
@@ -52,6 +52,7 @@ def load_library():
     sig = {
         "fea_create": [C.POINTER(P), I, P, I, I],
         "fea_set_element": [P, I, I, P, P],
+        "fea_set_rule": [P, I, I, P, P],
         "fea_mesh_upload": [P, L, P, L, P, L, P, I],
         "fea_set_tuning": [P, I, L],
         "fea_build_pattern": [P, P, P, P],
@@ -152,6 +153,12 @@ class Context:
         q_w = np.ascontiguousarray(q_w, dtype=np.float64)
         self._check(self._lib.fea_set_element(self._h, order, q_w.shape[0], _np_ptr(q_xy), _np_ptr(q_w)))
         self.order = order
+
+    def set_rule(self, which: int, q_xy, q_w):
+        """A separate quadrature rule for the matrices in `which` (NEXT-4)."""
+        xy = np.ascontiguousarray(q_xy, dtype=np.float64)
+        w = np.ascontiguousarray(q_w, dtype=np.float64)
+        self._check(self._lib.fea_set_rule(self._h, int(which), w.shape[0], _np_ptr(xy), _np_ptr(w)))
 
     def mesh_upload(self, vert_xy, elem_vert, n_dof: int, elem_dof, reorder: bool = True):
         vxy = np.ascontiguousarray(vert_xy, dtype=np.float64)

@@ -190,3 +190,66 @@ def test_reassemble_and_host_entry_points():
     assert np.array_equal(Mh, M.cpu().numpy()) and np.array_equal(Kh, K.cpu().numpy())
     ref = oracle_for(wl.mesh, wl.q_xy, wl.q_w, wl.u0, asm.lib_to_user, coef, coef, 3)
     assert maxabs_rel(Mh, ref.M) <= TOL and maxabs_rel(Kh, ref.K) <= TOL
+
+
+@pytest.mark.parametrize("p", [1, 2, 3, 4])
+def test_separate_rules_per_matrix(p):
+    """NEXT-4 / PAPER.md:137: M with one rule, C with another (fea_set_rule); each matrix must
+    equal the oracle run with its own rule.  Also the tensor contractions (M o2 v with M's rule,
+    C o2 v with C's rule), and going back to one common rule."""
+    import copy
+
+    import torch
+    from paper_2204_03893_b200.fea import FEA_MASS, FEA_STIFF, Context
+    m = random_mesh_from_structured(6, p, seed=400 + p)
+    rng = np.random.default_rng(40 + p)
+    u = rng.uniform(-1, 1, m.n_dof)
+    v = rng.normal(size=m.n_dof)
+    km, kc = (K_POLY, (1.0, 0.0, 1.0)), (K_EXP, (0.8, 0.4))
+    rm, rc = triangle_rule(2 * p), triangle_rule(min(8, 2 * p + 2))
+    ctx = Context(device=0)
+    ctx.set_element(p, *rm)
+    ctx.mesh_upload(m.vert_xy, m.elem_vert, m.n_dof, m.elem_dof)
+    ctx.set_rule(FEA_STIFF, *rc)
+    ctx.build_pattern()
+    ctx.set_coefficient(FEA_MASS, *km)
+    ctx.set_coefficient(FEA_STIFF, *kc)
+    perm = ctx.get_dof_perm()
+    dev = "cuda:0"
+    ul = torch.tensor(u[perm], dtype=torch.float64, device=dev)
+    vl = torch.tensor(v[perm], dtype=torch.float64, device=dev)
+    n = max(ctx.nnz, 1)
+    M = torch.zeros(n, dtype=torch.float64, device=dev)
+    K = torch.zeros(n, dtype=torch.float64, device=dev)
+    ctx.assemble(ul, M, K)
+    MT = torch.zeros(n, dtype=torch.float64, device=dev)
+    CT = torch.zeros(n, dtype=torch.float64, device=dev)
+    ctx.assemble_tensor(ul, vl, MT, CT)
+    ctx.sync()
+    mlib = copy.copy(m)
+    from tests.helpers import lib_numbering
+    mlib.elem_dof = lib_numbering(m, perm)
+    refm = oracle.assemble(mlib, *rm, u[perm], m_coef=km, c_coef=kc, which=MASS)
+    refc = oracle.assemble(mlib, *rc, u[perm], m_coef=km, c_coef=kc, which=STIFF)
+    assert maxabs_rel(M[: ctx.nnz].cpu().numpy(), refm.M) <= TOL
+    assert maxabs_rel(K[: ctx.nnz].cpu().numpy(), refc.K) <= TOL
+    tm = oracle.assemble_tensor_contraction(mlib, *rm, u[perm], v[perm], m_coef=km)
+    tc = oracle.assemble_tensor_contraction(mlib, *rc, u[perm], v[perm], c_coef=kc)
+    assert maxabs_rel(MT[: ctx.nnz].cpu().numpy(), tm.M) <= TOL
+    assert maxabs_rel(CT[: ctx.nnz].cpu().numpy(), tc.K) <= TOL
+    # a different rule for M, then one common rule again
+    ctx.set_rule(FEA_MASS, *rc)
+    ctx.build_pattern()
+    ctx.assemble(ul, M, K)
+    ctx.sync()
+    refm2 = oracle.assemble(mlib, *rc, u[perm], m_coef=km, c_coef=kc, which=MASS)
+    assert maxabs_rel(M[: ctx.nnz].cpu().numpy(), refm2.M) <= TOL
+    assert maxabs_rel(K[: ctx.nnz].cpu().numpy(), refc.K) <= TOL
+    ctx.set_rule(FEA_MASS | FEA_STIFF, *rm)
+    ctx.build_pattern()
+    ctx.assemble(ul, M, K)
+    ctx.sync()
+    refb = oracle.assemble(mlib, *rm, u[perm], m_coef=km, c_coef=kc, which=MASS | STIFF)
+    assert maxabs_rel(M[: ctx.nnz].cpu().numpy(), refb.M) <= TOL
+    assert maxabs_rel(K[: ctx.nnz].cpu().numpy(), refb.K) <= TOL
+    ctx.close()
