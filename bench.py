@@ -124,7 +124,7 @@ def workload_desc(cfg, wl):
     return {"workload": f"{cfg.name}: {cfg.description}", "config_index": cfg.index, "p": cfg.p, "N": cfg.N,
             "n_e": m.n_e, "n_dof": m.n_dof, "n_q": int(wl.q_w.shape[0]),
             "matrices": ("M+K" if cfg.which == 3 else "M" if cfg.which == 1 else "K"),
-            "k": {0: "poly", 1: "exp"}[cfg.k_kind] + str(list(cfg.k_par)),
+            "k": {0: "poly", 1: "exp", 2: "pwl"}[cfg.k_kind] + str(list(cfg.k_par)),
             "reorder": "morton" if cfg.reorder else "none"}
 
 
@@ -142,17 +142,17 @@ def cpu_oracle_run(wl, cfg, target_s: float, nthreads: int, lib_to_user=None, te
         u = np.ascontiguousarray(wl.u0[lib_to_user])
     else:
         u = wl.u0
-    coef = (cfg.k_kind, tuple(cfg.k_par))
+    coef, mcoef = cfg.coef_c, cfg.coef_m
     if tensor:  # the oracle's tensor contraction (single-threaded: it has no OpenMP path)
         v = np.full_like(u, 0.01)
         nthreads = 1
 
         def run(r1, pat):
-            oracle.assemble_tensor_contraction(m, wl.q_xy, wl.q_w, u, v, m_coef=coef if cfg.which & MASS else None,
+            oracle.assemble_tensor_contraction(m, wl.q_xy, wl.q_w, u, v, m_coef=mcoef if cfg.which & MASS else None,
                                                c_coef=coef if cfg.which & STIFF else None, r0=0, r1=r1, pat=pat)
     else:
         def run(r1, pat):
-            oracle.assemble(m, wl.q_xy, wl.q_w, u, m_coef=coef, c_coef=coef, which=cfg.which, r0=0, r1=r1,
+            oracle.assemble(m, wl.q_xy, wl.q_w, u, m_coef=mcoef, c_coef=coef, which=cfg.which, r0=0, r1=r1,
                             nthreads=nthreads, pat=pat)
     n_p = cfg.n_p
     nmat = cfg.n_matrices
@@ -220,10 +220,10 @@ def run_ours(args):
     t_setup = time.perf_counter()
     wl = make_workload(cfg)
     m = wl.mesh
-    coef = (cfg.k_kind, tuple(cfg.k_par))
+    coef, mcoef = cfg.coef_c, cfg.coef_m
     tuning = {int(kv.split("=")[0]): int(kv.split("=")[1]) for kv in args.tune}
     asm = Assembler(cfg.p, wl.q_xy, wl.q_w, m.vert_xy, m.elem_vert, m.n_dof, m.elem_dof, device=local,
-                    reorder=cfg.reorder, which=cfg.which, coef_m=coef, coef_c=coef, rank=rank, world=world,
+                    reorder=cfg.reorder, which=cfg.which, coef_m=mcoef, coef_c=coef, rank=rank, world=world,
                     tuning=tuning)
     t_setup = time.perf_counter() - t_setup
     nmat = cfg.n_matrices

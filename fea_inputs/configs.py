@@ -37,6 +37,16 @@ class Config:
     reorder: bool       # library Morton reorder requested
     description: str = ""
     extra: dict = field(default_factory=dict)
+    m_coef: tuple | None = None  # mass coefficient (kind, par) if it differs from k (else k)
+    length: float = 1.0          # side of the square domain
+
+    @property
+    def coef_c(self) -> tuple:
+        return (self.k_kind, tuple(self.k_par))
+
+    @property
+    def coef_m(self) -> tuple:
+        return self.m_coef if self.m_coef is not None else self.coef_c
 
     @property
     def n_p(self) -> int:
@@ -62,6 +72,14 @@ CONFIGS = {
                  "P1 4096x4096 permuted then Morton-reordered, deg-2, k=1+u^2, u~U[0,1], K only, 10 reassemblies"),
     "C5": Config("C5", 5, 2048, 4, 0.2, False, "U01", K_POLY, (1.0, 0.0, 0.0, 0.0, 1.0), MASS | STIFF, 1, True,
                  "P4 2048x2048 jittered, 16-pt deg-8, k=1+u^4, u~U[0,1], M+K"),
+    # stand-in for the paper's Experiment 2: the (0, 0.2 m)^2
+    # square with P2 elements (43 x 43 grid: 7,569 DOFs; the paper's mesh has 7,593 nodes), mass
+    # coefficient c rho = 1000 * 2400, conductivity k(T) piecewise linear through (0, 1.5),
+    # (200, 0.7), (1000, 0.5), T in degrees C between T_0 = 0 and T_a = 1000
+    "E2": Config("E2", 6, 43, 2, 0.0, False, "heat", K_PWL, (0.0, 1.5, 200.0, 0.7, 1000.0, 0.5), MASS | STIFF, 10,
+                 True, "Exp. 2 stand-in: P2 43x43 on (0,0.2)^2, 6-pt deg-4, c rho = 2.4e6, k(T) PWL, "
+                 "T = 1000 (1 - sin sin) + 10 N(0,1), M+K, 10 reassemblies",
+                 m_coef=(K_POLY, (2.4e6,)), length=0.2),
 }
 
 
@@ -102,12 +120,18 @@ def make_workload(cfg: Config) -> Workload:
     r_jit, r_u, r_perm, r_pert = seeds(cfg)
     mesh = structured_mesh(cfg.N, cfg.p, jitter=cfg.jitter, rng=r_jit,
                            perm_rng=r_perm if cfg.permute else None)
+    if cfg.length != 1.0:
+        mesh.vert_xy = mesh.vert_xy * cfg.length
+        mesh._dof_xy = None  # recomputed from the scaled vertices
     q_xy, q_w = triangle_rule(cfg.rule_degree)
     n = mesh.n_dof
     if cfg.u_kind == "U01":
         u0 = r_u.uniform(0.0, 1.0, n)
     elif cfg.u_kind == "U11":
         u0 = r_u.uniform(-1.0, 1.0, n)
+    elif cfg.u_kind == "heat":  # hot boundary (T_a = 1000 C), cold centre, a little noise
+        xy = mesh.dof_xy / cfg.length
+        u0 = 1000.0 * (1.0 - np.sin(np.pi * xy[:, 0]) * np.sin(np.pi * xy[:, 1])) + 10.0 * r_u.standard_normal(n)
     elif cfg.u_kind == "sinsin":
         xy = mesh.dof_xy
         u0 = np.sin(np.pi * xy[:, 0]) * np.sin(np.pi * xy[:, 1]) + 0.1 * r_u.standard_normal(n)

@@ -19,6 +19,11 @@ def coef_of(cfg):
     return (cfg.k_kind, tuple(cfg.k_par))
 
 
+def coefs_of(cfg):
+    """(mass, conductivity) coefficients of a config (they differ for E2)."""
+    return cfg.coef_m, cfg.coef_c
+
+
 def oracle_for(mesh, q_xy, q_w, u_user, lib_to_user, m_coef, c_coef, which, r0=0, r1=None, nthreads=1):
     """Oracle M/C rows [r0, r1) in library numbering."""
     import copy

@@ -16,7 +16,7 @@ from tests.helpers import lib_numbering
 
 pytestmark = pytest.mark.gpu
 TOL = 1e-12
-WINDOW = {"C2": 4000, "C3": 1500, "C4": 4000, "C5": 600}
+WINDOW = {"C2": 4000, "C3": 1500, "C4": 4000, "C5": 600, "E2": 2000}
 
 
 def _run(name):
@@ -25,9 +25,9 @@ def _run(name):
     cfg = CONFIGS[name]
     wl = make_workload(cfg)
     m = wl.mesh
-    coef = (cfg.k_kind, tuple(cfg.k_par))
+    coef, mcoef = cfg.coef_c, cfg.coef_m
     asm = Assembler(cfg.p, wl.q_xy, wl.q_w, m.vert_xy, m.elem_vert, m.n_dof, m.elem_dof, device=0,
-                    reorder=cfg.reorder, which=cfg.which, coef_m=coef, coef_c=coef)
+                    reorder=cfg.reorder, which=cfg.which, coef_m=mcoef, coef_c=coef)
     us = list(wl.u_sequence(2))
     u_user = us[-1]  # a perturbed iterate (reading 14)
     u_lib = asm.to_library(u_user)
@@ -40,7 +40,7 @@ def _run(name):
     for r0 in (0, n // 2 - w // 2, n - w):
         r1 = r0 + w
         rp, ci = asm.ctx.get_pattern_rows(r0, r1)
-        ref = oracle.assemble(mlib, wl.q_xy, wl.q_w, u_lib, m_coef=coef, c_coef=coef, which=cfg.which,
+        ref = oracle.assemble(mlib, wl.q_xy, wl.q_w, u_lib, m_coef=mcoef, c_coef=coef, which=cfg.which,
                               r0=r0, r1=r1, nthreads=oracle.max_threads())
         assert np.array_equal(rp - rp[0], ref.row_ptr), f"row_ptr window {r0}"
         assert np.array_equal(ci, ref.col_idx), f"col_idx window {r0}"
@@ -54,7 +54,7 @@ def _run(name):
     return asm, K
 
 
-@pytest.mark.parametrize("name", ["C2", "C3", "C4"])
+@pytest.mark.parametrize("name", ["C2", "C3", "C4", "E2"])
 def test_fullsize_sampled_windows_and_row_sums(name):
     import torch
     asm, K = _run(name)
@@ -74,7 +74,7 @@ def test_fullsize_C5_sampled_windows():
     asm.close()
 
 
-@pytest.mark.parametrize("name", ["C2", "C3", "C4"])
+@pytest.mark.parametrize("name", ["C2", "C3", "C4", "E2"])
 def test_fullsize_tensor_sampled_windows(name):
     """NEXT-1/2 at full size (bench --op tensor): (M o2 v), (C o2 v) at u = u_1, v = u_1 - u_0."""
     import torch
@@ -82,9 +82,9 @@ def test_fullsize_tensor_sampled_windows(name):
     cfg = CONFIGS[name]
     wl = make_workload(cfg)
     m = wl.mesh
-    coef = (cfg.k_kind, tuple(cfg.k_par))
+    coef, mcoef = cfg.coef_c, cfg.coef_m
     asm = Assembler(cfg.p, wl.q_xy, wl.q_w, m.vert_xy, m.elem_vert, m.n_dof, m.elem_dof, device=0,
-                    reorder=cfg.reorder, which=cfg.which, coef_m=coef, coef_c=coef)
+                    reorder=cfg.reorder, which=cfg.which, coef_m=mcoef, coef_c=coef)
     u0, u1 = list(wl.u_sequence(2))
     u_lib, v_lib = asm.to_library(u1), asm.to_library(u1 - u0)
     dev = "cuda:0"
@@ -99,13 +99,17 @@ def test_fullsize_tensor_sampled_windows(name):
     for r0 in (0, m.n_dof // 2 - w // 2, m.n_dof - w):
         rp, ci = asm.ctx.get_pattern_rows(r0, r0 + w)
         ref = oracle.assemble_tensor_contraction(mlib, wl.q_xy, wl.q_w, u_lib, v_lib,
-                                                 m_coef=coef if mt is not None else None,
+                                                 m_coef=mcoef if mt is not None else None,
                                                  c_coef=coef if ct is not None else None, r0=r0, r1=r0 + w)
         assert np.array_equal(rp - rp[0], ref.row_ptr) and np.array_equal(ci, ref.col_idx)
         for got, want in ((mt, ref.M), (ct, ref.K)):
             if got is None:
                 continue
             g = got[int(rp[0]):int(rp[-1])].cpu().numpy()
-            err = np.abs(g - want).max() / np.abs(want).max()
+            scale = np.abs(want).max()
+            if scale == 0.0:  # e.g. M o2 v with a constant mass coefficient (m' = 0): exactly zero
+                assert np.abs(g).max() == 0.0
+                continue
+            err = np.abs(g - want).max() / scale
             assert err <= TOL, f"window {r0}: {err:.3e}"
     asm.close()

@@ -10,7 +10,7 @@ import oracle
 from fea_inputs import CONFIGS, K_EXP, K_POLY, K_PWL, MASS, STIFF, make_workload, scaled, single_element_mesh, \
     structured_mesh, triangle_rule, two_element_mesh
 from fea_inputs.mesh import random_mesh_from_structured
-from tests.helpers import coef_of, library_assemble, maxabs_rel, oracle_for
+from tests.helpers import coef_of, coefs_of, library_assemble, maxabs_rel, oracle_for
 
 pytestmark = pytest.mark.gpu
 TOL = 1e-12
@@ -28,7 +28,7 @@ def _check(res, ref, which):
 
 
 # configs at sizes the oracle finishes in seconds; several CTA blocks and a ragged tail each
-SMALL = [("C1", 32), ("C2", 48), ("C3", 24), ("C4", 96), ("C5", 12)]
+SMALL = [("C1", 32), ("C2", 48), ("C3", 24), ("C4", 96), ("C5", 12), ("E2", 43)]
 
 
 @pytest.mark.parametrize("name,N", SMALL)
@@ -37,13 +37,13 @@ def test_config_parity_small(name, N, kernel):
     """kernel 0: automatic (v5 for p <= 2 with the native rule), 4: v4 forced (FEA_TUNE_KERNEL)."""
     cfg = scaled(CONFIGS[name], N)
     w = make_workload(cfg)
-    coef = coef_of(cfg)
+    mcoef, ccoef = coefs_of(cfg)
     for u in w.u_sequence(min(cfg.reassemblies, 2)):
-        res = library_assemble(w.mesh, w.q_xy, w.q_w, u, cfg.p, coef, coef, which=cfg.which,
+        res = library_assemble(w.mesh, w.q_xy, w.q_w, u, cfg.p, mcoef, ccoef, which=cfg.which,
                                tuning={2: kernel} if kernel else None)
         assert res["ctx"].stat(11) == (5 if cfg.p <= 2 and kernel == 0 else 4)
         assert res["ctx"].stat(1) >= 2  # several blocks
-        ref = oracle_for(w.mesh, w.q_xy, w.q_w, u, res["perm"], coef, coef, cfg.which)
+        ref = oracle_for(w.mesh, w.q_xy, w.q_w, u, res["perm"], mcoef, ccoef, cfg.which)
         _check(res, ref, cfg.which)
 
 
