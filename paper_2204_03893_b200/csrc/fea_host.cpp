@@ -127,6 +127,10 @@ struct fea_ctx_s {
     // tuning
     int64_t tune_smem = 0;
     int tune_kver = 0;     // 0 = automatic, 4 = force kernel v4
+    int tune_overlap = 1;  // world > 1: interior blocks assemble while u is exchanged (FEA_TUNE_OVERLAP)
+    int n_int = 0;         // interior blocks (first n_int of the plan when world > 1)
+    cudaStream_t stream2 = nullptr;  // exchange stream of the overlap
+    cudaEvent_t ev_own = nullptr, ev_halo = nullptr;
     int tune_lpt = 0;      // v5: LPT block order for few blocks per CTA (FEA_TUNE_LPT; measured no gain on C2)
     int64_t tune_emax = 0; // v5 element cap per block (0 = from the budget)
 
@@ -392,6 +396,9 @@ void fea_destroy(fea_ctx c) {
     if (!c) return;
     if (!c->host_only) cudaSetDevice(c->device);
     c->free_mesh();
+    if (c->stream2) cudaStreamDestroy(c->stream2);
+    if (c->ev_own) cudaEventDestroy(c->ev_own);
+    if (c->ev_halo) cudaEventDestroy(c->ev_halo);
     dfree(c->d_tables);
     dfree(c->d_ttab);
     dfree(c->d_tables_c);
@@ -656,6 +663,10 @@ fea_status fea_set_tuning(fea_ctx c, int key, int64_t value) {
             if (value < 0 || value > 65535) return c->fail(FEA_E_ARG, "element cap out of range");
             c->tune_emax = value;
             break;
+        case 7:  // world > 1: overlap the exchange with the interior blocks (1, default) or not (0)
+            if (value != 0 && value != 1) return c->fail(FEA_E_ARG, "overlap flag must be 0 or 1");
+            c->tune_overlap = (int)value;
+            break;
         case 6:  // v5 LPT block order on (1, default) / off (0)
             if (value != 0 && value != 1) return c->fail(FEA_E_ARG, "LPT flag must be 0 or 1");
             c->tune_lpt = (int)value;
@@ -800,6 +811,15 @@ static fea_status build_blocks(fea_ctx c, bool v5, bool orient, int64_t e_max, i
         std::sort(E.begin(), E.end());
         E.erase(std::unique(E.begin(), E.end()), E.end());
         for (int32_t e : E) (c->elem_min[e] < ga ? o.nghost : o.nown)++;
+        {  // interior: every DOF of every element of the block is owned by this rank (overlap, NEXT-3)
+            bool inside = true;
+            for (int32_t e : E)
+                for (int i = 0; i < np && inside; ++i) {
+                    const int32_t d = c->ed[(size_t)e * np + i];
+                    inside = d >= R0 && d < R1;
+                }
+            o.fb.spare_[0] = inside ? 1 : 0;
+        }
         struct Rec { int32_t row, col, le, t; };  // t: symmetric row (| 0x8000 if orient and i > j)
         std::vector<Rec> recs;
         for (int64_t le = 0; le < (int64_t)E.size(); ++le) {
@@ -1018,6 +1038,11 @@ fea_status fea_build_pattern(fea_ctx c, int64_t* row_begin, int64_t* n_rows_loca
     }
     const int64_t nb = (int64_t)P.blocks.size();
     const int64_t nnz = P.nnz, rec_max = P.rec_max;
+    c->n_int = 0;
+    if (c->world > 1) {  // interior blocks first (they read only owned u): assembled during the exchange
+        std::stable_partition(P.blocks.begin(), P.blocks.end(), [](const FeaBlock& b) { return b.spare_[0] != 0; });
+        for (const FeaBlock& b : P.blocks) c->n_int += b.spare_[0] != 0;
+    }
     c->row_ptr.swap(P.row_ptr);
     c->col_idx.swap(P.col_idx);
     std::vector<FeaBlock>& blocks = P.blocks;
@@ -1103,8 +1128,8 @@ fea_status fea_build_pattern(fea_ctx c, int64_t* row_begin, int64_t* n_rows_loca
     if (occ < 1) return c->fail(FEA_E_UNSUPPORTED, "kernel does not fit: %d B shared memory", c->smem_bytes);
     c->grid = (int)std::min<int64_t>(std::max<int64_t>(nb, 1), (int64_t)occ * c->sm_count);
     // our kernels per fea_reassemble: the assembly, plus pack + unpack of the exchange (world > 1)
-    c->launches_per_call = 1 + (c->world > 1 && c->exchange == 0 ? 2 : 0);
-    if (v5 && nb > c->grid && nb <= 16LL * c->grid && c->tune_lpt) {
+    c->launches_per_call = c->world > 1 ? 2 + (c->exchange == 0 ? 2 : 0) : 1;
+    if (v5 && c->world == 1 && nb > c->grid && nb <= 16LL * c->grid && c->tune_lpt) {
         // few blocks per CTA: the static schedule (CTA g runs blocks g, g + grid, ...) is balanced
         // by an LPT order: blocks by descending cost estimate, each to the least-loaded CTA that
         // still has a free position (CTA g has ceil/floor(nb / grid) positions).  Results do not
@@ -1195,10 +1220,13 @@ static bool same_coef(const FeaCoef& a, const FeaCoef& b) {
     return true;
 }
 
-// rule_c: run with the rule of C (split rules; vm must then be NULL)
-static fea_status launch(fea_ctx c, const double* u, double* vm, double* vc, bool rule_c = false) {
+// rule_c: run with the rule of C (split rules; vm must then be NULL).  Blocks [b0, b1) of the plan
+// (b1 < 0: all).
+static fea_status launch(fea_ctx c, const double* u, double* vm, double* vc, bool rule_c = false, int b0 = 0,
+                         int b1 = -1) {
+    if (b1 < 0) b1 = c->nblocks;
     FeaKParams prm{};
-    prm.blocks = c->d_blocks;
+    prm.blocks = c->d_blocks + b0;
     prm.records = c->d_records;
     prm.xy = c->d_xy;
     prm.dofs = c->d_dofs;
@@ -1206,7 +1234,7 @@ static fea_status launch(fea_ctx c, const double* u, double* vm, double* vc, boo
     prm.qfrag = rule_c ? c->d_tables_c : c->d_tables;
     prm.out_m = vm;
     prm.out_c = vc;
-    prm.nblocks = c->nblocks;
+    prm.nblocks = b1 - b0;
     prm.e_max = c->e_max;
     prm.nq = rule_c ? c->nq_c : c->nq;
     prm.same_coef = same_coef(c->coef_m, c->coef_c) ? 1 : 0;
@@ -1224,11 +1252,30 @@ static fea_status launch(fea_ctx c, const double* u, double* vm, double* vc, boo
         }
         prm.dbg = c->d_dbg;
     }
-    if (c->nblocks == 0) return FEA_OK;
-    const int rc = c->kver == 5 ? fea_launch_reassemble5(prm, c->order, c->smem_bytes, c->grid, c->stream)
-                                : fea_launch_reassemble(prm, c->order, c->smem_bytes, c->grid, c->stream);
+    if (b1 <= b0) return FEA_OK;
+    const int grid = std::min(c->grid, b1 - b0);
+    const int rc = c->kver == 5 ? fea_launch_reassemble5(prm, c->order, c->smem_bytes, grid, c->stream)
+                                : fea_launch_reassemble(prm, c->order, c->smem_bytes, grid, c->stream);
     if (rc != 0) return c->fail(FEA_E_CUDA, "k_reassemble launch: %s", cudaGetErrorString((cudaError_t)rc));
     return FEA_OK;
+}
+
+// all blocks, or (world > 1) the interior blocks [0, n_int) / the boundary blocks [n_int, nb)
+enum { FEA_PART_ALL = 0, FEA_PART_INT = 1, FEA_PART_BND = 2 };
+static fea_status assemble_part(fea_ctx c, const double* u_full, double* mass_vals, double* stiff_vals, int part) {
+    const int b0 = part == FEA_PART_BND ? c->n_int : 0;
+    const int b1 = part == FEA_PART_INT ? c->n_int : c->nblocks;
+    const bool pm = c->plan_which & FEA_MASS, pc = c->plan_which & FEA_STIFF;
+    fea_status s;
+    if (c->split) {  // separate rules: one pass per matrix, each with its rule's tables
+        if (mass_vals && (s = launch(c, u_full, mass_vals, nullptr, false, b0, b1)) != FEA_OK) return s;
+        return stiff_vals ? launch(c, u_full, nullptr, stiff_vals, true, b0, b1) : FEA_OK;
+    }
+    if (mass_vals && stiff_vals && !(pm && pc)) {  // plan sized for one matrix: two passes
+        if ((s = launch(c, u_full, mass_vals, nullptr, false, b0, b1)) != FEA_OK) return s;
+        return launch(c, u_full, nullptr, stiff_vals, false, b0, b1);
+    }
+    return launch(c, u_full, mass_vals, stiff_vals, false, b0, b1);
 }
 
 fea_status fea_assemble(fea_ctx c, const double* u_full, double* mass_vals, double* stiff_vals) {
@@ -1240,17 +1287,9 @@ fea_status fea_assemble(fea_ctx c, const double* u_full, double* mass_vals, doub
         return c->fail(FEA_E_ARG, "vals must be 16-byte aligned");
     if (!mass_vals && !stiff_vals) return FEA_OK;
     cudaSetDevice(c->device);
-    const bool pm = c->plan_which & FEA_MASS, pc = c->plan_which & FEA_STIFF;
-    fea_status s;
-    if (c->split) {  // separate rules: one pass per matrix, each with its rule's tables
-        if (mass_vals && (s = launch(c, u_full, mass_vals, nullptr)) != FEA_OK) return s;
-        return stiff_vals ? launch(c, u_full, nullptr, stiff_vals, true) : FEA_OK;
-    }
-    if (mass_vals && stiff_vals && !(pm && pc)) {  // plan sized for one matrix: two passes
-        if ((s = launch(c, u_full, mass_vals, nullptr)) != FEA_OK) return s;
-        return launch(c, u_full, nullptr, stiff_vals);
-    }
-    return launch(c, u_full, mass_vals, stiff_vals);
+    if (c->world == 1) return assemble_part(c, u_full, mass_vals, stiff_vals, FEA_PART_ALL);
+    const fea_status s = assemble_part(c, u_full, mass_vals, stiff_vals, FEA_PART_INT);
+    return s != FEA_OK ? s : assemble_part(c, u_full, mass_vals, stiff_vals, FEA_PART_BND);
 }
 
 fea_status fea_assemble_mass(fea_ctx c, const double* u_full, double* vals) {
@@ -1288,6 +1327,38 @@ static fea_status exchange_u(fea_ctx c, const double* u_owned) {
                                       (ncclComm_t)c->comm, c->stream);
     if (r != ncclSuccess) return c->fail(FEA_E_NCCL, "ncclAllGather: %s", nccl().getErrorString(r));
     return FEA_OK;
+}
+
+// NEXT-3 overlap: the owned rows go into u_full on the ctx stream, the interior blocks (which read
+// only owned entries) assemble on the ctx stream while pack -> ncclAllGather -> unpack of the halo
+// run on a second stream; the boundary blocks wait for the halo.
+static fea_status reassemble_overlap(fea_ctx c, const double* u_owned, double* mass_vals, double* stiff_vals) {
+    if (!c->stream2) {
+        FEA_CUDA(c, cudaStreamCreateWithFlags(&c->stream2, cudaStreamNonBlocking));
+        FEA_CUDA(c, cudaEventCreateWithFlags(&c->ev_own, cudaEventDisableTiming));
+        FEA_CUDA(c, cudaEventCreateWithFlags(&c->ev_halo, cudaEventDisableTiming));
+    }
+    if (c->n_rows)
+        FEA_CUDA(c, cudaMemcpyAsync(c->d_ufull + c->row_begin, u_owned, c->n_rows * sizeof(double),
+                                    cudaMemcpyDeviceToDevice, c->stream));
+    FEA_CUDA(c, cudaEventRecord(c->ev_own, c->stream));
+    FEA_CUDA(c, cudaStreamWaitEvent(c->stream2, c->ev_own, 0));
+    int rc = fea_launch_pack(u_owned, c->d_iface + c->ioff[c->rank], (int)(c->ioff[c->rank + 1] - c->ioff[c->rank]),
+                             c->row_begin, c->maxI, c->d_isend, c->stream2);
+    if (rc) return c->fail(FEA_E_CUDA, "pack: %s", cudaGetErrorString((cudaError_t)rc));
+    if (c->maxI > 0) {
+        ncclResult_t r = nccl().allGather(c->d_isend, c->d_irecv, (size_t)c->maxI, ncclDouble, (ncclComm_t)c->comm,
+                                          c->stream2);
+        if (r != ncclSuccess) return c->fail(FEA_E_NCCL, "ncclAllGather: %s", nccl().getErrorString(r));
+    }
+    rc = fea_launch_unpack(c->d_irecv, c->d_iface, c->d_ioff, c->world, c->rank, c->maxI, c->ioff[c->world],
+                           u_owned, c->row_begin, 0 /* owned rows already copied */, c->d_ufull, c->stream2);
+    if (rc) return c->fail(FEA_E_CUDA, "unpack: %s", cudaGetErrorString((cudaError_t)rc));
+    FEA_CUDA(c, cudaEventRecord(c->ev_halo, c->stream2));
+    fea_status s = assemble_part(c, c->d_ufull, mass_vals, stiff_vals, FEA_PART_INT);
+    if (s != FEA_OK) return s;
+    FEA_CUDA(c, cudaStreamWaitEvent(c->stream, c->ev_halo, 0));
+    return assemble_part(c, c->d_ufull, mass_vals, stiff_vals, FEA_PART_BND);
 }
 
 fea_status fea_get_interface(fea_ctx c, int64_t* offsets, int32_t* dofs) {
@@ -1328,6 +1399,10 @@ fea_status fea_reassemble(fea_ctx c, const double* u_owned, double* mass_vals, d
     cudaSetDevice(c->device);
     if (c->world == 1) return fea_assemble(c, u_owned, mass_vals, stiff_vals);
     if (!c->comm) return c->fail(FEA_E_STATE, "world > 1 requires fea_set_nccl");
+    if ((mass_vals && ((uintptr_t)mass_vals & 15)) || (stiff_vals && ((uintptr_t)stiff_vals & 15)))
+        return c->fail(FEA_E_ARG, "vals must be 16-byte aligned");
+    if (c->exchange == 0 && c->tune_overlap)
+        return reassemble_overlap(c, u_owned, mass_vals, stiff_vals);
     const fea_status st = exchange_u(c, u_owned);
     if (st != FEA_OK) return st;
     return fea_assemble(c, c->d_ufull, mass_vals, stiff_vals);
@@ -1348,9 +1423,7 @@ fea_status fea_reassemble_host(fea_ctx c, const double* u_host, double* mass_hos
     if (c->world == 1) s = fea_assemble(c, c->d_ufull, mass_host ? c->d_vm : nullptr, stiff_host ? c->d_vc : nullptr);
     else {
         if (!c->comm) return c->fail(FEA_E_STATE, "world > 1 requires fea_set_nccl");
-        const fea_status st = exchange_u(c, c->d_usend);
-        if (st != FEA_OK) return st;
-        s = fea_assemble(c, c->d_ufull, mass_host ? c->d_vm : nullptr, stiff_host ? c->d_vc : nullptr);
+        s = fea_reassemble(c, c->d_usend, mass_host ? c->d_vm : nullptr, stiff_host ? c->d_vc : nullptr);
     }
     if (s != FEA_OK) return s;
     if (mass_host) FEA_CUDA(c, cudaMemcpyAsync(mass_host, c->d_vm, c->nnz * sizeof(double), cudaMemcpyDeviceToHost, c->stream));
@@ -1502,6 +1575,7 @@ fea_status fea_get_stat(fea_ctx c, int key, int64_t* value) {
             return c->fail(FEA_E_ARG, "unknown stat key %d", key);
         case 11: *value = c->kver; break;
         case 14: *value = c->maxI; break;
+        case 15: *value = c->n_int; break;
     }
     return FEA_OK;
 }

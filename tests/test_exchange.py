@@ -48,8 +48,22 @@ def test_interface_lists_complete_and_minimal(p, world):
         for x in iface[t]:
             assert any(x in needed[s] for s in range(world) if s != t)       # minimal
     assert max(len(s) for s in iface) == ctxs[0].stat(14)
-    for c in ctxs:
+    for c in ctxs:  # interior blocks (assembled during the exchange) come first; some exist
+        assert 0 <= c.stat(15) <= c.stat(1)
         c.close()
+
+
+def test_interior_blocks_on_a_larger_mesh():
+    """Overlap (NEXT-3): on a config-sized mesh split over 2 and 4 ranks most blocks are interior
+    (all their elements' DOFs owned) and a few are boundary blocks."""
+    cfg = scaled(CONFIGS["C2"], 64)
+    wl = make_workload(cfg)
+    for world in (2, 4):
+        for r in range(world):
+            c = _plan(wl.mesh, cfg.p, wl.q_xy, wl.q_w, r, world)
+            nb, ni = c.stat(1), c.stat(15)
+            assert 0 < ni < nb, (world, r, ni, nb)
+            c.close()
 
 
 @pytest.mark.gpu
