@@ -73,8 +73,6 @@ enum {
     FEA_TUNE_OVERLAP = 7,       /* world > 1: 1 = the interior blocks (reading only owned u) assemble
                                    while the interface exchange runs on a second stream (default),
                                    0 = exchange, then assemble                                      */
-    FEA_TUNE_LPT = 6,           /* v5, <= 16 blocks per CTA: 1 = cost-balanced (LPT) block order,
-                                   0 = row-block order (default; LPT measured no gain on C2)         */
     FEA_TUNE_PLAN_WHICH = 4     /* FEA_MASS | FEA_STIFF: matrices the plan's shared memory is sized
                                    for (default both); assembling more than planned runs one pass
                                    per matrix                                                        */

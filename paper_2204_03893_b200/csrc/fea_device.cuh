@@ -1,7 +1,7 @@
-// fea_device.cuh -- device helpers shared by the sm_100a reassembly kernels (fea_kernels.cu: v4,
-// p >= 3 and generic rules; fea_kernels5.cu: v5, p <= 2): PTX wrappers (mbarrier, TMA bulk copy,
-// cp.async, DMMA), the coefficient k(u), element geometry, and phase B (fixed-order segmented
-// sums of the contributor stream into the CSR slots).
+// fea_device.cuh -- device helpers shared by the sm_100a kernels (fea_kernels.cu: v4, p >= 3 and
+// generic rules; fea_kernels5.cu: v5, p <= 2; fea_kernels_t.cu: tensor contractions): PTX wrappers
+// (mbarrier, TMA bulk copy, cp.async, DMMA, L2 prefetch), the coefficient k(u) and k'(u), element
+// geometry, and phase B (fixed-order sums of each CSR slot's contributors).
 #pragma once
 #include <cuda_runtime.h>
 #include <cstdint>
@@ -141,99 +141,6 @@ __device__ __forceinline__ void geometry(const double2* __restrict__ gX, int e_m
     A01 = -(B00 * B01 + B10 * B11) * inv;
 }
 
-// ------------------------------------------------------------------ phase B helpers
-// Sum of the C contributors of one slot in the fixed (stored) order, all loads issued first.
-template <int C, bool DO_M, bool DO_C>
-__device__ __forceinline__ void slot_sum(const uint16_t* __restrict__ cp, const double* __restrict__ sVm,
-                                         const double* __restrict__ sVc, double& am, double& ac) {
-    int off[C];
-#pragma unroll
-    for (int q = 0; q < C; ++q) off[q] = cp[q];
-    double vm[C], vc[C];
-#pragma unroll
-    for (int q = 0; q < C; ++q) {
-        if (DO_M) vm[q] = sVm[off[q]];
-        if (DO_C) vc[q] = sVc[off[q]];
-    }
-    am = 0.0;
-    ac = 0.0;
-#pragma unroll
-    for (int q = 0; q < C; ++q) {
-        if (DO_M) am += vm[q];
-        if (DO_C) ac += vc[q];
-    }
-}
-
-template <int C, bool DO_M, bool DO_C>
-__device__ __forceinline__ void class_items(int i0, int i1, int cb, const uint16_t* __restrict__ items,
-                                            const uint16_t* __restrict__ con, const double* __restrict__ sVm,
-                                            const double* __restrict__ sVc, double* om, double* oc, int tid,
-                                            int nthr) {
-    int it = i0 + tid;
-    for (; it + nthr < i1; it += 2 * nthr) {  // two items per thread in flight
-        const int s0 = items[it], s1 = items[it + nthr];
-        double am0, ac0, am1, ac1;
-        slot_sum<C, DO_M, DO_C>(con + cb + (it - i0) * C, sVm, sVc, am0, ac0);
-        slot_sum<C, DO_M, DO_C>(con + cb + (it + nthr - i0) * C, sVm, sVc, am1, ac1);
-        if (DO_M) {
-            om[s0] = am0;
-            om[s1] = am1;
-        }
-        if (DO_C) {
-            oc[s0] = ac0;
-            oc[s1] = ac1;
-        }
-    }
-    if (it < i1) {
-        const int s0 = items[it];
-        double am0, ac0;
-        slot_sum<C, DO_M, DO_C>(con + cb + (it - i0) * C, sVm, sVc, am0, ac0);
-        if (DO_M) om[s0] = am0;
-        if (DO_C) oc[s0] = ac0;
-    }
-}
-
-template <bool DO_M, bool DO_C>
-__device__ __forceinline__ void class_items_generic(int c, int i0, int i1, int cb, const uint16_t* __restrict__ items,
-                                                    const uint16_t* __restrict__ con, const double* __restrict__ sVm,
-                                                    const double* __restrict__ sVc, double* om, double* oc, int tid,
-                                                    int nthr) {
-    for (int it = i0 + tid; it < i1; it += nthr) {
-        const uint16_t* cp = con + cb + (it - i0) * c;
-        double am = 0.0, ac = 0.0;
-        for (int q = 0; q < c; ++q) {
-            const int off = cp[q];
-            if (DO_M) am += sVm[off];
-            if (DO_C) ac += sVc[off];
-        }
-        const int s = items[it];
-        if (DO_M) om[s] = am;
-        if (DO_C) oc[s] = ac;
-    }
-}
-
-// Phase B of one row block: every CSR slot of the block = the sum of its contributors in the
-// stored (ascending library element) order, class by class (uniform trip counts per class).
-template <bool DO_M, bool DO_C>
-__device__ __forceinline__ void phase_b(const uint8_t* __restrict__ rec, const FeaBlock& blk,
-                                        const double* __restrict__ sVm, const double* __restrict__ sVc, double* om,
-                                        double* oc, int tid, int nthr) {
-    const int32_t* cls = reinterpret_cast<const int32_t*>(rec);
-    const uint16_t* items = reinterpret_cast<const uint16_t*>(rec + fea_rec_off_items(blk));
-    const uint16_t* con = reinterpret_cast<const uint16_t*>(rec + fea_rec_off_contrib(blk));
-    for (int k = 0; k < blk.ncls; ++k) {
-        const int c = cls[3 * k], i0 = cls[3 * k + 1], cb = cls[3 * k + 2];
-        const int i1 = k + 1 < blk.ncls ? cls[3 * k + 4] : blk.nslots;
-        switch (c) {
-            case 1: class_items<1, DO_M, DO_C>(i0, i1, cb, items, con, sVm, sVc, om, oc, tid, nthr); break;
-            case 2: class_items<2, DO_M, DO_C>(i0, i1, cb, items, con, sVm, sVc, om, oc, tid, nthr); break;
-            case 3: class_items<3, DO_M, DO_C>(i0, i1, cb, items, con, sVm, sVc, om, oc, tid, nthr); break;
-            case 4: class_items<4, DO_M, DO_C>(i0, i1, cb, items, con, sVm, sVc, om, oc, tid, nthr); break;
-            case 6: class_items<6, DO_M, DO_C>(i0, i1, cb, items, con, sVm, sVc, om, oc, tid, nthr); break;
-            default: class_items_generic<DO_M, DO_C>(c, i0, i1, cb, items, con, sVm, sVc, om, oc, tid, nthr);
-        }
-    }
-}
 
 // ---- phase B of kernel v5 (record format: fea_internal.h fea5_item_bytes): one vector load per
 // item gives its slot and its C contributor offsets; ILP items per thread are in flight.  Each

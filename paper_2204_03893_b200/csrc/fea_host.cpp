@@ -131,7 +131,6 @@ struct fea_ctx_s {
     int n_int = 0;         // interior blocks (first n_int of the plan when world > 1)
     cudaStream_t stream2 = nullptr;  // exchange stream of the overlap
     cudaEvent_t ev_own = nullptr, ev_halo = nullptr;
-    int tune_lpt = 0;      // v5: LPT block order for few blocks per CTA (FEA_TUNE_LPT; measured no gain on C2)
     int64_t tune_emax = 0; // v5 element cap per block (0 = from the budget)
 
     // reassemble buffers
@@ -667,10 +666,6 @@ fea_status fea_set_tuning(fea_ctx c, int key, int64_t value) {
             if (value != 0 && value != 1) return c->fail(FEA_E_ARG, "overlap flag must be 0 or 1");
             c->tune_overlap = (int)value;
             break;
-        case 6:  // v5 LPT block order on (1, default) / off (0)
-            if (value != 0 && value != 1) return c->fail(FEA_E_ARG, "LPT flag must be 0 or 1");
-            c->tune_lpt = (int)value;
-            break;
         case 5:  // exchange of u between ranks: 0 = interface-only, 1 = full allgather
             if (value != 0 && value != 1) return c->fail(FEA_E_ARG, "exchange must be 0 or 1");
             c->exchange = (int)value;
@@ -1129,29 +1124,6 @@ fea_status fea_build_pattern(fea_ctx c, int64_t* row_begin, int64_t* n_rows_loca
     c->grid = (int)std::min<int64_t>(std::max<int64_t>(nb, 1), (int64_t)occ * c->sm_count);
     // our kernels per fea_reassemble: the assembly, plus pack + unpack of the exchange (world > 1)
     c->launches_per_call = c->world > 1 ? 2 + (c->exchange == 0 ? 2 : 0) : 1;
-    if (v5 && c->world == 1 && nb > c->grid && nb <= 16LL * c->grid && c->tune_lpt) {
-        // few blocks per CTA: the static schedule (CTA g runs blocks g, g + grid, ...) is balanced
-        // by an LPT order: blocks by descending cost estimate, each to the least-loaded CTA that
-        // still has a free position (CTA g has ceil/floor(nb / grid) positions).  Results do not
-        // depend on the order (disjoint slots, fixed per-slot order).
-        const int64_t G = c->grid;
-        std::vector<int64_t> idx(nb), cap(G), pos(G, 0);
-        std::vector<double> load(G, 0.0), cost(nb);
-        for (int64_t b = 0; b < nb; ++b) cost[b] = (double)blocks[b].nE * T + 0.5 * blocks[b].nslots;
-        std::iota(idx.begin(), idx.end(), 0);
-        std::stable_sort(idx.begin(), idx.end(), [&](int64_t a, int64_t b) { return cost[a] > cost[b]; });
-        for (int64_t g = 0; g < G; ++g) cap[g] = (nb - 1 - g) / G + 1;
-        std::vector<FeaBlock> perm(nb);
-        for (int64_t b : idx) {
-            int64_t best = -1;
-            for (int64_t g = 0; g < G; ++g)
-                if (pos[g] < cap[g] && (best < 0 || load[g] < load[best])) best = g;
-            perm[best + pos[best] * G] = blocks[b];
-            pos[best]++;
-            load[best] += cost[b];
-        }
-        FEA_CUDA(c, cudaMemcpy(c->d_blocks, perm.data(), nb * sizeof(FeaBlock), cudaMemcpyHostToDevice));
-    }
     c->have_plan = true;
     if (row_begin) *row_begin = R0;
     if (n_rows_local) *n_rows_local = nr;

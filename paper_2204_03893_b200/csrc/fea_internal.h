@@ -4,12 +4,6 @@
 #include <cstdint>
 
 #define FEA_MAX_ORDER 4
-#ifndef FEA5_SPEC
-#define FEA5_SPEC 0  // kernel v5: warp-specialised A / B (1; measured slower) or every warp does both (0)
-#endif
-#ifndef FEA5_NS2
-#define FEA5_NS2 2  // units per P2 tile in kernel v5 (column halves)
-#endif
 #define FEA_MAX_NP 15
 #define FEA_MAX_NQ 16
 #define FEA_MAX_PAR 16
@@ -40,16 +34,9 @@ __host__ __device__ constexpr bool fea_interp_mma(int p) { return p >= 2; }
 __host__ __device__ constexpr int fea_kt(int p) { return (fea_np(p) + 3) / 4; }
 
 // One unit of CTA work: a contiguous block of library rows whose CSR slots
-// [slot0, slot0 + nslots) are produced by exactly one CTA.  Everything the block streams
-// from HBM sits in ONE contiguous, 16-byte aligned record at rec_off (one TMA bulk copy):
-//   classes  int32  [ncls][3]   (count c, first item, first contributor); slots with the
-//                               same contributor count form a class, so a warp's lanes all
-//                               run the same trip count                                (pad16)
-//   items    uint16 [nslots]    block-local slot of each item, sorted by (count, slot)   (pad16)
-//   contrib  uint16 [ncontrib]  V offsets t * e_max + le, item by item; within an item in
-//                               ascending library element order (the fixed summation order)
-//                                                                                        (pad16)
-//   dofs     int32  [n_p][pad4(nE)]  library DOFs of the block's elements (SoA)
+// [slot0, slot0 + nslots) are produced by exactly one CTA.  Its phase-B data sit in ONE
+// contiguous, 16-byte aligned record at rec_off (one TMA bulk copy); formats below (v5:
+// class/item records; v4: a FeaRecHdr4 header, the same class/item part, then the element DOFs).
 // The block's elements (le = 0 .. nE-1) are in ascending library element order: ghost
 // elements (owned by earlier blocks) first, then the block's own elements.
 struct FeaBlock {
@@ -65,22 +52,13 @@ struct FeaBlock {
     int32_t pad_;
     int32_t r0, nr;    // v5: the block's own rows [r0, r0 + nr) (library DOFs): the bulk of the u and
                        // xy entries its gathers touch (L2-prefetched blocks ahead)
-    int32_t spare_[2]; // 64 bytes: the v5 kernel copies descriptors with 16-byte cp.async
+    int32_t spare_[2]; // [0]: interior block (all element DOFs owned; world > 1 overlap); 64 bytes:
+                       // the v5 kernel copies descriptors with 16-byte cp.async
 };
 static_assert(sizeof(FeaBlock) == 64, "FeaBlock must stay 64 bytes");
 
 __host__ __device__ inline int32_t fea_pad16(int32_t b) { return (b + 15) & ~15; }
 __host__ __device__ inline int32_t fea_pad4(int32_t n) { return (n + 3) & ~3; }
-__host__ __device__ inline int32_t fea_rec_off_items(const FeaBlock& b) { return fea_pad16(12 * b.ncls); }
-__host__ __device__ inline int32_t fea_rec_off_contrib(const FeaBlock& b) {
-    return fea_rec_off_items(b) + fea_pad16(2 * b.nslots);
-}
-__host__ __device__ inline int32_t fea_rec_off_dofs(const FeaBlock& b) {
-    return fea_rec_off_contrib(b) + fea_pad16(2 * b.ncontrib);
-}
-__host__ __device__ inline int32_t fea_rec_bytes(const FeaBlock& b, int np) {
-    return fea_rec_off_dofs(b) + 4 * np * fea_pad4(b.nE);
-}
 // v4 record (p >= 3, generic rules): a 32-byte header (FeaRecHdr4), the v5 class/item part
 // below (offsets relative to byte 32), then the block's element DOFs int32 [n_p][pad4(nE)] at
 // dofs_off.  The header lets the consumer warps read the block descriptor from shared memory.
@@ -106,7 +84,7 @@ __host__ __device__ constexpr int fea5_item_bytes(int C) {
 // NW warps per CTA (no producer warp), one CTA per SM, and the units per 32-element tile.
 __host__ __device__ constexpr int fea5_nw(int p) { return p == 1 ? 16 : 16; }
 __host__ __device__ constexpr int fea5_ctas(int p) { return 1; }
-__host__ __device__ constexpr int fea5_nsplit(int p) { return p == 2 ? FEA5_NS2 : 1; }  // units per tile
+__host__ __device__ constexpr int fea5_nsplit(int p) { return p == 2 ? 2 : 1; }  // units per tile (P2: column halves)
 __host__ __device__ constexpr int fea5_threads(int p) { return fea5_nw(p) * 32; }
 __host__ __device__ constexpr bool fea5_supported(int p, int nq) { return p <= 2 && nq == fea_nq_native(p); }
 // reference gradients in the kernel parameters: jtab[a][k][q] = d phi_k / d xhat_a at x_q

@@ -69,11 +69,9 @@ __global__ void __launch_bounds__(fea5_threads(P), 1) k_reassemble5(const __grid
     if (prm.dbg_mode & 64) return;  // diagnostics: empty launch (fixed launch overhead)
 #endif
     const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
-    // SPEC: warps [0, NC) compute (A) and warps [NC, NW) run phase B, concurrently on consecutive
-    // blocks; otherwise every warp does both in turn
-    constexpr bool SPEC = FEA5_SPEC != 0;
-    constexpr int NC = SPEC ? NW / 2 : NW;  // warps running A
-    constexpr int NBW = SPEC ? NW - NC : NW;  // warps running B
+    // every warp runs both A and B (warp-specialised A / B warps measured slower: DESIGN.md 7.7)
+    constexpr int NC = NW;   // warps running A
+    constexpr int NBW = NW;  // warps running B
     const int vs = prm.e_max | 1;
     const int G = gridDim.x, b0 = blockIdx.x;
     const int nb = prm.nblocks > b0 ? (prm.nblocks - 1 - b0) / G + 1 : 0;
@@ -278,139 +276,69 @@ __global__ void __launch_bounds__(fea5_threads(P), 1) k_reassemble5(const __grid
     auto tick = [](int) {};
 #endif
 
-    if constexpr (SPEC) {
-        if (warp < NC) {
-            // ---- A warps: units of block s -> V[s & 1], gated by free[s & 1] (B of block s - 2)
-            Gath<NP> ga, gb;
-            if (ls < nb) load_dofs(ls, lu);
-            refill(ga);
-            refill(gb);
-            tick(6);
-            for (int s = 0; s < nb; ++s) {
-                const int b = s & 1;
-                if (s >= 2) mbar_wait(&freeb[b], (uint32_t)(((s - 2) >> 1) & 1));
-                win = max(s + 6, 6);  // ring entries published with free[] (B warps, step s - 1)
-                tick(5);
-                double* sVm = sVm0 + b * (DO_M && DO_C ? 2 : 1) * vbuf;
-                double* sVc = sVc0 + b * vbuf;
-                while (cs == s) {
-                    const int le = (cu / NS) * 32 + lane;
-                    if (le < blk_of(s).nE) compute(ga, sVm, sVc, le, cu % NS);
-                    tick(0);
-                    ga = gb;
-                    refill(gb);
-                    tick(1);
-                    advance(cs, cu);
-                }
-                __syncwarp();
-                if (lane == 0) mbar_arrive(&full[b]);
-            }
-        } else {
-            // ---- B warps: step s issues the record of block s (its stage freed by B of s - 2),
-            // the descriptor of block s + 6 and the L2 prefetch, then runs phase B of block s - 1
-            const int bt = tid - NC * 32;
-            for (int s = 0; s <= nb; ++s) {
-                if (s < nb && bt == 0) {
-                    const int b = s & 1;
-                    if (s >= 2) mbar_wait(&freeb[b], (uint32_t)(((s - 2) >> 1) & 1));
-                    const FeaBlock& bk = sBlk[s & (DR - 1)];
-                    fence_proxy_async();
-                    mbar_expect_tx(&recb[b], (uint32_t)bk.rec_bytes);
-                    tma_load_1d(sRec0 + b * rec_stride, prm.records + bk.rec_off, (uint32_t)bk.rec_bytes, &recb[b]);
-                    if (s + 6 < nb) {  // slot of block s - 2 (its B is done)
-                        const uint8_t* src = reinterpret_cast<const uint8_t*>(prm.blocks + b0 + (s + 6) * G);
-                        uint8_t* dst = reinterpret_cast<uint8_t*>(sBlk + ((s + 6) & (DR - 1)));
-#pragma unroll
-                        for (int w = 0; w < 4; ++w) cp_async16(dst + 16 * w, src + 16 * w);
-                        asm volatile("cp.async.commit_group;" ::: "memory");
-                    }
-                    if (s + PF < nb) prefetch_blk(s + PF);
-                }
-                if (s >= 1) {
-                    const int s1 = s - 1, b = s1 & 1;
-                    mbar_wait(&full[b], (uint32_t)((s1 >> 1) & 1));
-                    win = s1 + 1;  // B reads only block s1's descriptor (ring, written >= 6 steps ago)
-                    tick(2);
-                    mbar_wait(&recb[b], (uint32_t)((s1 >> 1) & 1));
-                    tick(3);
-                    const FeaBlock& bk = sBlk[s1 & (DR - 1)];
-                    double* om = DO_M ? prm.out_m + bk.slot0 : nullptr;
-                    double* oc = DO_C ? prm.out_c + bk.slot0 : nullptr;
-                    phase_b5<DO_M, DO_C, false, DO_M && DO_C>(sRec0 + b * rec_stride, bk.ncls,
-                                                              sVm0 + b * (DO_M && DO_C ? 2 : 1) * vbuf,
-                                                              sVc0 + b * vbuf, om, oc, bt, NBW * 32);
-                    tick(4);
-                    if (bt == 0) asm volatile("cp.async.wait_all;" ::: "memory");  // publish the ring entry
-                    __syncwarp();
-                    if (lane == 0) mbar_arrive(&freeb[b]);
-                }
-            }
-        }
-    } else {
     // ---- prologue: DOFs of the first unit, then two units of gathers in flight
-        Gath<NP> ga, gb;  // ga: the compute cursor's unit, gb: the one after it
-        if (ls < nb) load_dofs(ls, lu);
-        refill(ga);
-        refill(gb);
-        tick(6);
-    
-        for (int s = 0; s <= nb; ++s) {
-            win = max(s + 4, 6);  // ring entries published by the full barrier of step s - 1
-            if (s < nb) {
-                const int b = s & 1;
-                if (s >= 2) mbar_wait(&freeb[b], (uint32_t)(((s - 2) >> 1) & 1));  // B of block s - 2 done
-                tick(5);
-                if (tid == 0) {
-                    asm volatile("cp.async.wait_all;" ::: "memory");  // ring entry of block s + 5
-                    const FeaBlock& bk = sBlk[s & (DR - 1)];
-                    fence_proxy_async();
-                    mbar_expect_tx(&recb[b], (uint32_t)bk.rec_bytes);
-                    tma_load_1d(sRec0 + b * rec_stride, prm.records + bk.rec_off, (uint32_t)bk.rec_bytes, &recb[b]);
-                    if (s + 6 < nb) {  // slot of block s - 2, whose phase B is done
-                        const uint8_t* src = reinterpret_cast<const uint8_t*>(prm.blocks + b0 + (s + 6) * G);
-                        uint8_t* dst = reinterpret_cast<uint8_t*>(sBlk + ((s + 6) & (DR - 1)));
+    Gath<NP> ga, gb;  // ga: the compute cursor's unit, gb: the one after it
+    if (ls < nb) load_dofs(ls, lu);
+    refill(ga);
+    refill(gb);
+    tick(6);
+
+    for (int s = 0; s <= nb; ++s) {
+        win = max(s + 4, 6);  // ring entries published by the full barrier of step s - 1
+        if (s < nb) {
+            const int b = s & 1;
+            if (s >= 2) mbar_wait(&freeb[b], (uint32_t)(((s - 2) >> 1) & 1));  // B of block s - 2 done
+            tick(5);
+            if (tid == 0) {
+                asm volatile("cp.async.wait_all;" ::: "memory");  // ring entry of block s + 5
+                const FeaBlock& bk = sBlk[s & (DR - 1)];
+                fence_proxy_async();
+                mbar_expect_tx(&recb[b], (uint32_t)bk.rec_bytes);
+                tma_load_1d(sRec0 + b * rec_stride, prm.records + bk.rec_off, (uint32_t)bk.rec_bytes, &recb[b]);
+                if (s + 6 < nb) {  // slot of block s - 2, whose phase B is done
+                    const uint8_t* src = reinterpret_cast<const uint8_t*>(prm.blocks + b0 + (s + 6) * G);
+                    uint8_t* dst = reinterpret_cast<uint8_t*>(sBlk + ((s + 6) & (DR - 1)));
     #pragma unroll
-                        for (int w = 0; w < 4; ++w) cp_async16(dst + 16 * w, src + 16 * w);
-                        asm volatile("cp.async.commit_group;" ::: "memory");
-                    }
-                    if (s + PF < nb) prefetch_blk(s + PF);
+                    for (int w = 0; w < 4; ++w) cp_async16(dst + 16 * w, src + 16 * w);
+                    asm volatile("cp.async.commit_group;" ::: "memory");
                 }
-                double* sVm = sVm0 + b * (DO_M && DO_C ? 2 : 1) * vbuf;  // M + K: one interleaved region
-                double* sVc = sVc0 + b * vbuf;
-                while (cs == s) {
-                    const int le = (cu / NS) * 32 + lane;
-                    if (le < blk_of(s).nE) compute(ga, sVm, sVc, le, cu % NS);
-                    tick(0);
-                    ga = gb;
-                    refill(gb);
-                    tick(1);
-                    advance(cs, cu);
-                }
-                __syncwarp();
-                if (lane == 0) mbar_arrive(&full[b]);
+                if (s + PF < nb) prefetch_blk(s + PF);
             }
-            if (s >= 1) {
-                const int s1 = s - 1, b = s1 & 1;
-                mbar_wait(&full[b], (uint32_t)((s1 >> 1) & 1));
-                win = max(s + 5, 6);
-                tick(2);
-                mbar_wait(&recb[b], (uint32_t)((s1 >> 1) & 1));
-                tick(3);
-                const FeaBlock& bk = blk_of(s1);
-                {
-                    double* om = DO_M ? prm.out_m + bk.slot0 : nullptr;
-                    double* oc = DO_C ? prm.out_c + bk.slot0 : nullptr;
-                    phase_b5<DO_M, DO_C, false, DO_M && DO_C>(sRec0 + b * rec_stride, bk.ncls,
-                                         sVm0 + b * (DO_M && DO_C ? 2 : 1) * vbuf, sVc0 + b * vbuf, om, oc, tid,
-                                         NW * 32);
-                }
-                tick(4);
-                __syncwarp();
-                if (lane == 0) mbar_arrive(&freeb[b]);
+            double* sVm = sVm0 + b * (DO_M && DO_C ? 2 : 1) * vbuf;  // M + K: one interleaved region
+            double* sVc = sVc0 + b * vbuf;
+            while (cs == s) {
+                const int le = (cu / NS) * 32 + lane;
+                if (le < blk_of(s).nE) compute(ga, sVm, sVc, le, cu % NS);
+                tick(0);
+                ga = gb;
+                refill(gb);
+                tick(1);
+                advance(cs, cu);
             }
+            __syncwarp();
+            if (lane == 0) mbar_arrive(&full[b]);
         }
-    
+        if (s >= 1) {
+            const int s1 = s - 1, b = s1 & 1;
+            mbar_wait(&full[b], (uint32_t)((s1 >> 1) & 1));
+            win = max(s + 5, 6);
+            tick(2);
+            mbar_wait(&recb[b], (uint32_t)((s1 >> 1) & 1));
+            tick(3);
+            const FeaBlock& bk = blk_of(s1);
+            {
+                double* om = DO_M ? prm.out_m + bk.slot0 : nullptr;
+                double* oc = DO_C ? prm.out_c + bk.slot0 : nullptr;
+                phase_b5<DO_M, DO_C, false, DO_M && DO_C>(sRec0 + b * rec_stride, bk.ncls,
+                                     sVm0 + b * (DO_M && DO_C ? 2 : 1) * vbuf, sVc0 + b * vbuf, om, oc, tid,
+                                     NW * 32);
+            }
+            tick(4);
+            __syncwarp();
+            if (lane == 0) mbar_arrive(&freeb[b]);
+        }
     }
+
 
 #ifdef FEA5_DIAG
     if (prm.dbg && lane == 0)
