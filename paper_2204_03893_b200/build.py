@@ -33,6 +33,7 @@ def build(force: bool = False, verbose: bool = False) -> str:
         return LIB
     os.makedirs(OBJ, exist_ok=True)
     inc = ["-I", os.path.join(ROOT, "include"), "-I", CSRC]
+    inc += os.environ.get("FEA_BUILD_DEFS", "").split()  # experiment switches, e.g. "-DFEA5_MMA=0"
 
     def compile_one(src):
         obj = os.path.join(OBJ, src + ".o")
