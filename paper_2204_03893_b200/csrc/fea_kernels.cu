@@ -145,21 +145,17 @@ __global__ void __launch_bounds__(fea_threads(P), fea_ctas(P)) k_reassemble(cons
             tcl = now;
         }
     };
-    tick(-1);
     const int vs = fea4_vstride(e_max);  // V row stride (fea_internal.h)
-    for (int j = 0; j < ncta_blocks; ++j) {
+
+    // ---------------- A1 of block j: geometry (W_e, b_e), u_q = Phi^T u_e, k(u_q), Lambda
+    auto phase_a1 = [&](int j) {
         const int rs = j % RS, gs = j & 1;
-        const uint8_t* rec = sRec(rs);
         const double* gU = gUb(gs);
         const double2* gX = gXb(gs);
         mbar_wait(&full_rec[rs], (uint32_t)((j / RS) & 1));
-        const FeaRecHdr4 blk = *reinterpret_cast<const FeaRecHdr4*>(rec);  // descriptor from the record
-        const int nE = blk.nE;
+        const int nE = reinterpret_cast<const FeaRecHdr4*>(sRec(rs))->nE;
         const int net = (nE + 7) >> 3;
         mbar_wait(&full_gat[gs], (uint32_t)((j >> 1) & 1));
-        tick(0);
-
-        // ---------------- A1: geometry (W_e, b_e), u_q = Phi^T u_e, k(u_q), Lambda
         if constexpr (!INTERP_MMA) {
             for (int le = tid; le < net * 8; le += NCT) {
                 if (le < nE) {
@@ -194,19 +190,9 @@ __global__ void __launch_bounds__(fea_threads(P), fea_ctas(P)) k_reassemble(cons
                     sW[le] = sW[e_max + le] = sW[2 * e_max + le] = 0.0;
                 }
             }
-            consumer_sync(NCT);
         } else {
-            // A1a: geometry per element
-            for (int le = tid; le < net * 8; le += NCT) {
-                double absdet = 0.0, A00 = 0.0, A11 = 0.0, A01 = 0.0;
-                if (le < nE) geometry(gX, e_max, le, absdet, A00, A11, A01);
-                sW[le] = A00;
-                sW[e_max + le] = A11;
-                sW[2 * e_max + le] = A01;
-                sW[3 * e_max + le] = absdet;
-            }
-            consumer_sync(NCT);
-            // A1b: U = Phi^T U_e on DMMA; epilogue Lambda_qe = w_q b_e k(u_qe)
+            // U = Phi^T U_e on DMMA; epilogue Lambda_qe = w_q b_e k(u_qe) with the geometry of the
+            // lane's two accumulator columns (recomputed per m-tile; the m-tile 0, g = 0 lanes store W_e)
             constexpr int MT = MTN, KT = KTN;
             for (int un = warp; un < MT * net; un += NTT * S) {
                 const int mt = un % MT, et = un / MT;
@@ -221,12 +207,18 @@ __global__ void __launch_bounds__(fea_threads(P), fea_ctas(P)) k_reassemble(cons
                     dmma(u0, u1, a, b);
                 }
                 const int q = mt * 8 + g, le0 = et * 8 + 2 * cq;
+                double d0 = 0.0, d1 = 0.0, w00 = 0.0, w01 = 0.0, w10 = 0.0, w11 = 0.0, w20 = 0.0, w21 = 0.0;
+                if (le0 < nE) geometry(gX, e_max, le0, d0, w00, w10, w20);
+                if (le0 + 1 < nE) geometry(gX, e_max, le0 + 1, d1, w01, w11, w21);
+                if (mt == 0 && g == 0) {
+                    *reinterpret_cast<double2*>(sW + le0) = make_double2(w00, w01);
+                    *reinterpret_cast<double2*>(sW + e_max + le0) = make_double2(w10, w11);
+                    *reinterpret_cast<double2*>(sW + 2 * e_max + le0) = make_double2(w20, w21);
+                }
                 if (q < NQP) {
                     double lm0 = 0.0, lm1 = 0.0, lc0 = 0.0, lc1 = 0.0;
                     if (q < nq) {
                         const double w = cW[q];
-                        const double d0 = le0 < nE ? sW[3 * e_max + le0] : 0.0;
-                        const double d1 = le0 + 1 < nE ? sW[3 * e_max + le0 + 1] : 0.0;
                         const FeaCoef& cf = DO_M ? prm.coef_m : prm.coef_c;
                         if (le0 < nE) lm0 = w * d0 * keval(cf, u0);
                         if (le0 + 1 < nE) lm1 = w * d1 * keval(cf, u1);
@@ -239,11 +231,24 @@ __global__ void __launch_bounds__(fea_threads(P), fea_ctas(P)) k_reassemble(cons
                     if (two_lam) *reinterpret_cast<double2*>(sLc + q * e_max + le0) = make_double2(lc0, lc1);
                 }
             }
-            consumer_sync(NCT);
         }
-        // gather stage consumed: the producer may refill it
-        if (tid == 0) mbar_arrive(&gdone[gs]);
-        tick(1);
+    };
+
+    // Software pipeline over the CTA's blocks, two CTA barriers per block:
+    //   A1(0) | for j: A2(j) | B(j) and A1(j + 1) |
+    // (A1 writes Lambda / W, which A2(j) has finished reading; B reads V and the record of block j).
+    if (ncta_blocks > 0) {
+        phase_a1(0);
+        consumer_sync(NCT);
+        if (tid == 0) mbar_arrive(&gdone[0]);
+    }
+    tick(-1);
+    for (int j = 0; j < ncta_blocks; ++j) {
+        const int rs = j % RS;
+        const uint8_t* rec = sRec(rs);
+        const FeaRecHdr4 blk = *reinterpret_cast<const FeaRecHdr4*>(rec);  // descriptor from the record
+        const int nE = blk.nE;
+        const int net = (nE + 7) >> 3;
 
         // ---------------- A2: V = Q Lambda on the FP64 tensor cores (DMMA m8n8k4)
         {
@@ -281,16 +286,23 @@ __global__ void __launch_bounds__(fea_threads(P), fea_ctas(P)) k_reassemble(cons
             }
         }
         tick(2);
-        consumer_sync(NCT);
+        consumer_sync(NCT);  // V complete; Lambda / W free
         tick(5);
 
-        // ---------------- Phase B: fixed-order segmented reduction into the CSR slots.
+        // ---------------- Phase B of block j (fixed-order segmented reduction into the CSR slots)
+        // and A1 of block j + 1, in alternating order across warps so the two overlap.
+        const bool a1_first = (warp & 1) && j + 1 < ncta_blocks;
+        if (a1_first) phase_a1(j + 1);
         phase_b5<DO_M, DO_C>(rec + 32, blk.ncls, sVm, sVc, DO_M ? prm.out_m + blk.slot0 : nullptr,
                              DO_C ? prm.out_c + blk.slot0 : nullptr, tid, NCT);
+        if (!a1_first && j + 1 < ncta_blocks) phase_a1(j + 1);
         tick(3);
-        consumer_sync(NCT);  // V and the record stage are free
+        consumer_sync(NCT);  // V and the record stage of block j free; Lambda / W of block j + 1 ready
         tick(5);
-        if (tid == 0) mbar_arrive(&rdone[rs]);
+        if (tid == 0) {
+            mbar_arrive(&rdone[rs]);
+            if (j + 1 < ncta_blocks) mbar_arrive(&gdone[(j + 1) & 1]);
+        }
     }
     if (prm.dbg && tid == 0)
         for (int i = 0; i < 6; ++i) atomicAdd(prm.dbg + i, tacc[i]);
