@@ -296,7 +296,10 @@ def run_ours(args):
     kern_ms = statistics.median(step_ms)
     achieved = B / (kern_ms * 1e-3) / 1e9
     traffic = None
-    kname = "k_tensor" if tensor else ("k_reassemble5" if asm.ctx.stat(11) == 5 else "k_reassemble")
+    if tensor:
+        kname = "k_tensor4" if asm.ctx.stat(12) == 4 else "k_tensor"
+    else:
+        kname = "k_reassemble5" if asm.ctx.stat(11) == 5 else "k_reassemble"
     prof = os.path.join(ROOT, "profiles", f"ncu_traffic_{cfg.name}_{kname}.json")
     if os.path.exists(prof):  # an ncu --set full capture of this kernel on this config
         with open(prof) as f:
@@ -359,8 +362,11 @@ def run_ours(args):
         desc.update({"l2": f"flushed ({flush_mb} MiB write) before every timed step" if flush_mb >= 256 else
                      f"NOT flushed ({flush_mb} MiB write): diagnostic run, not a bench value", "parallelism": f"rows{world}",
                      "nnz": int(nnz_local) if world == 1 else None, "setup_s": round(t_setup, 3),
-                     "blocks": asm.ctx.stat(1), "elem_visits_over_owned": round(asm.ctx.stat(2) / max(1, asm.ctx.stat(3)), 4),
-                     "smem_per_cta": asm.ctx.stat(6), "grid": asm.ctx.stat(8), "tuning": tuning})
+                     "tuning": tuning})
+        sk = (16, 17, 18, 19, 13) if tensor else (1, 2, 3, 6, 8)  # tensor plan / matrix plan statistics
+        desc.update({"blocks": asm.ctx.stat(sk[0]),
+                     "elem_visits_over_owned": round(asm.ctx.stat(sk[1]) / max(1, asm.ctx.stat(sk[2])), 4),
+                     "smem_per_cta": asm.ctx.stat(sk[3]), "grid": asm.ctx.stat(sk[4])})
         if os.environ.get("FEA_DEBUG_TIMING"):
             if asm.ctx.stat(11) == 5:  # per-warp timeline of k_reassemble5 (lane 0 of every warp)
                 names = ["compute", "move_refill", "full_wait", "rec_wait", "phaseB", "free_wait", "prologue"]

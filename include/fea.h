@@ -67,15 +67,19 @@ enum {
                                    smaller row blocks (more, finer CTA tiles)                        */
     FEA_TUNE_KERNEL = 2,        /* kernel generation: 0 = automatic (v5 for p <= 2 with the native
                                    3/6-point rules, v4 otherwise), 4 = force v4                      */
-    FEA_TUNE_EMAX = 3,          /* v5: cap on elements per row block (0 = from the smem budget)      */
+    FEA_TUNE_EMAX = 3,          /* v5 and k_tensor4: cap on elements per row block (0 = from the
+                                   shared-memory budget)                                             */
     FEA_TUNE_EXCHANGE = 5,      /* world > 1: 0 = interface-only exchange of u (default), 1 = full-
                                    vector allgather                                                 */
     FEA_TUNE_OVERLAP = 7,       /* world > 1: 1 = the interior blocks (reading only owned u) assemble
                                    while the interface exchange runs on a second stream (default),
                                    0 = exchange, then assemble                                      */
-    FEA_TUNE_PLAN_WHICH = 4     /* FEA_MASS | FEA_STIFF: matrices the plan's shared memory is sized
+    FEA_TUNE_PLAN_WHICH = 4,    /* FEA_MASS | FEA_STIFF: matrices the plan's shared memory is sized
                                    for (default both); assembling more than planned runs one pass
                                    per matrix                                                        */
+    FEA_TUNE_TENSOR_KERNEL = 8  /* fea_assemble_tensor kernel: 0 = automatic (DMMA k_tensor4 for p >= 2
+                                   or a non-native rule, k_tensor otherwise), 1 = k_tensor (one
+                                   thread per element), 4 = k_tensor4 (FP64 tensor cores)            */
 };
 
 /* Create a context on CUDA device `cuda_device`.  `stream` is a cudaStream_t (NULL = the
@@ -205,7 +209,11 @@ fea_status fea_sync(fea_ctx ctx);
 
 /* Statistics of the plan (for reports): key 1 = number of CTA blocks, 2 = element-visits
  * including ghosts, 3 = owned elements, 4 = local entries (sum over blocks of contributor
- * count), 5 = kernel launches per fea_assemble call, 6 = smem bytes per CTA. */
+ * count), 5 = kernel launches per fea_assemble call, 6 = smem bytes per CTA, 7 = elements per
+ * block (max), 8 = grid, 10 = largest block record (bytes), 11 = matrix kernel (4 or 5),
+ * 14 = max interface size, 15 = interior blocks (world > 1).  Tensor plan (after the first
+ * fea_assemble_tensor, else -1): 12 = tensor kernel (1 or 4), 13 = its grid, 16 = blocks,
+ * 17 = element visits, 18 = owned elements, 19 = smem bytes per CTA. */
 fea_status fea_get_stat(fea_ctx ctx, int key, int64_t* value);
 
 const char* fea_last_error(fea_ctx ctx);

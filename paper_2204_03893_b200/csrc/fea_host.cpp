@@ -118,7 +118,9 @@ struct fea_ctx_s {
     FeaBlock* dt_blocks = nullptr;
     uint8_t* dt_records = nullptr;
     int32_t* dt_dofs = nullptr;
-    int t_nblocks = 0, t_emax = 0, t_smem = 0, t_grid = 0;
+    int t_nblocks = 0, t_emax = 0, t_smem = 0, t_grid = 0, t_kver = 0;
+    int64_t t_visits = 0, t_owned = 0;
+    double t_rec_el = 0;  // k_tensor4 plan: record bytes per element of the first plan (re-plan)
     int32_t t_lay[FEA_LT_N] = {0};
 
     // coefficients
@@ -127,6 +129,7 @@ struct fea_ctx_s {
     // tuning
     int64_t tune_smem = 0;
     int tune_kver = 0;     // 0 = automatic, 4 = force kernel v4
+    int tune_tker = 0;     // tensor kernel: 0 = automatic, 1 = k_tensor, 4 = k_tensor4 (FEA_TUNE_TENSOR_KERNEL)
     int tune_overlap = 1;  // world > 1: interior blocks assemble while u is exchanged (FEA_TUNE_OVERLAP)
     int n_int = 0;         // interior blocks (first n_int of the plan when world > 1)
     cudaStream_t stream2 = nullptr;  // exchange stream of the overlap
@@ -167,6 +170,7 @@ struct fea_ctx_s {
         dfree(dt_records);
         dfree(dt_dofs);
         have_tplan = false;
+        t_rec_el = 0;
         dfree(d_vm);
         dfree(d_vc);
         row_ptr.clear();
@@ -321,6 +325,21 @@ bool build_tables(int p, int nq, const double* qxy, const double* qw, std::vecto
                 const int q = mt * 8 + (lane >> 2), i = kt * 4 + (lane & 3);
                 qfrag.push_back(q < nq && i < np ? (double)phi[i * nq + q] : 0.0);
             }
+    // (4) R_d as DMMA A-fragments [NTC][2][NK][32] (k_tensor4, C o2 v): lane (g, c) holds
+    //     R_d[r = 8 rt + g][q = 4 kk + c] = J_d,i(q) phi_k(q), r = i np + k (all np^2 pairs)
+    const int NTC = (np * np + 7) / 8;
+    for (int rt = 0; rt < NTC; ++rt)
+        for (int d = 0; d < 2; ++d)
+            for (int kk = 0; kk < NK; ++kk)
+                for (int lane = 0; lane < 32; ++lane) {
+                    const int r = rt * 8 + (lane >> 2), q = kk * 4 + (lane & 3);
+                    double v = 0.0;
+                    if (r < np * np && q < nq) {
+                        const int i = r / np, k = r % np;
+                        v = (double)((d == 0 ? gx[i * nq + q] : gy[i * nq + q]) * phi[k * nq + q]);
+                    }
+                    qfrag.push_back(v);
+                }
     return true;
 }
 
@@ -669,6 +688,10 @@ fea_status fea_set_tuning(fea_ctx c, int key, int64_t value) {
         case 5:  // exchange of u between ranks: 0 = interface-only, 1 = full allgather
             if (value != 0 && value != 1) return c->fail(FEA_E_ARG, "exchange must be 0 or 1");
             c->exchange = (int)value;
+            break;
+        case 8:  // tensor kernel: 0 = automatic, 1 = lane per element (k_tensor), 4 = DMMA (k_tensor4)
+            if (value != 0 && value != 1 && value != 4) return c->fail(FEA_E_ARG, "tensor kernel must be 0, 1 or 4");
+            c->tune_tker = (int)value;
             break;
         case 4:  // plan matrices bitmask (FEA_MASS | FEA_STIFF)
             if (value < 1 || value > 3) return c->fail(FEA_E_ARG, "plan matrices must be a nonzero MASS|STIFF mask");
@@ -1410,19 +1433,48 @@ static fea_status build_tensor_plan(fea_ctx c) {
     const int np = c->np, T = c->T;
     const int64_t budget = 227 * 1024;
     const int64_t tabs = 8LL * (3 * np * 16 + 16) + 256;
-    const double rec_el = 1.1 * 2.0 * np * np + 8;
-    int64_t e_max = (int64_t)((budget - tabs - 1024) / (3 * 8.0 * T + rec_el));
-    e_max = std::min<int64_t>(e_max, 32767 / T - 1) / 8 * 8;
-    const int64_t rec_budget = (budget - tabs - 1024 - 3 * 8LL * T * (e_max | 1)) & ~int64_t(15);
+    // kernel: k_tensor4 (DMMA) for p >= 2 or any non-native rule, k_tensor (lane per element) for
+    // P1 with its 3-point rule (measured faster there: 3.26 vs 5.20 ms on C4)
+    const bool native = c->nq == fea_nq_native(c->order) && (!c->split || c->nq_c == fea_nq_native(c->order));
+    c->t_kver = c->tune_tker ? c->tune_tker : (c->order >= 2 || !native ? 4 : 1);
+    const bool k4 = c->t_kver == 4;
+    int64_t e_max, rec_budget;
+    if (k4) {  // V1, Vup, Vdn [T][e_max + 2], two record and gather stages, Lambda and p (fea_t4_smem_layout)
+        const int nqp = c->split ? 16 : 4 * fea_nk_kernel(c->order, c->nq);
+        const int64_t per_el = 3 * 8LL * T + 2 * (16LL * np + 48) + 3 * 8LL * nqp;
+        // record bytes per element: an estimate, then (below) the planned blocks' own ratio
+        const double rec_el = c->t_rec_el > 0 ? c->t_rec_el : 1.3 * (3.0 * np * np + 4.0 * np) + 8;
+        const int64_t r0 = 32 * FEA_MAX_CLASSES + 1024;  // per-record constant part (class table, padding)
+        e_max = (int64_t)((budget - tabs - 1024 - 3 * 16LL * T - 2 * r0) / (per_el + 2 * rec_el));
+        if (c->tune_emax) e_max = std::min(e_max, c->tune_emax);
+        e_max = std::min<int64_t>(e_max, 32767 / T - 2) / 8 * 8;
+        rec_budget = ((int64_t)(rec_el * e_max) + r0 + 15) & ~int64_t(15);
+    } else {
+        const double rec_el = 1.1 * 2.0 * np * np + 8;
+        e_max = (int64_t)((budget - tabs - 1024) / (3 * 8.0 * T + rec_el));
+        e_max = std::min<int64_t>(e_max, 32767 / T - 1) / 8 * 8;
+        rec_budget = (budget - tabs - 1024 - 3 * 8LL * T * (e_max | 1)) & ~int64_t(15);
+    }
     PlanData P;
-    const fea_status st = build_blocks(c, true, true, e_max, rec_budget, e_max | 1, P);
+    const fea_status st = build_blocks(c, !k4, true, e_max, rec_budget, k4 ? fea4_vstride((int32_t)e_max) : (e_max | 1), P);
     if (st != FEA_OK) return st;
     if (P.nnz != c->nnz || P.row_ptr != c->row_ptr) return c->fail(FEA_E_STATE, "tensor plan: pattern mismatch");
     const int64_t nb = (int64_t)P.blocks.size();
-    fea_t_smem_layout(c->t_lay, (int)P.rec_max, (int)e_max, c->order);
+    if (k4) {
+        fea_t4_smem_layout(c->t_lay, (int)P.rec_max, (int)e_max, c->order, c->split ? 0 : c->nq);
+        c->t_smem = c->t_lay[FEA_LT4_TOTAL];
+        if (c->t_rec_el == 0 && e_max > 0) {  // one re-plan with the measured record bytes per element
+            c->t_rec_el = 1.02 * (double)P.rec_max / (double)e_max;
+            if (budget - c->t_smem > 8 * 1024) return build_tensor_plan(c);
+        }
+    } else {
+        fea_t_smem_layout(c->t_lay, (int)P.rec_max, (int)e_max, c->order);
+        c->t_smem = c->t_lay[FEA_LT_TOTAL];
+    }
     c->t_nblocks = (int)nb;
     c->t_emax = (int)e_max;
-    c->t_smem = c->t_lay[FEA_LT_TOTAL];
+    c->t_visits = P.visits;
+    c->t_owned = P.owned;
     FEA_CUDA(c, cudaMalloc((void**)&c->dt_blocks, std::max<int64_t>(nb, 1) * sizeof(FeaBlock)));
     if (nb) FEA_CUDA(c, cudaMemcpy(c->dt_blocks, P.blocks.data(), nb * sizeof(FeaBlock), cudaMemcpyHostToDevice));
     FEA_CUDA(c, cudaMalloc((void**)&c->dt_records, P.records.size()));
@@ -1430,7 +1482,7 @@ static fea_status build_tensor_plan(fea_ctx c) {
     FEA_CUDA(c, cudaMalloc((void**)&c->dt_dofs, P.dofs.size() * sizeof(int32_t)));
     FEA_CUDA(c, cudaMemcpy(c->dt_dofs, P.dofs.data(), P.dofs.size() * sizeof(int32_t), cudaMemcpyHostToDevice));
     int occ = 0, thr = 0;
-    const int rc = fea_tensor_occupancy(c->order, c->t_smem, &occ, &thr);
+    const int rc = fea_tensor_occupancy(c->order, c->nq, c->t_kver, c->t_smem, &occ, &thr);
     if (rc != 0) return c->fail(FEA_E_CUDA, "tensor occupancy: %s", cudaGetErrorString((cudaError_t)rc));
     if (occ < 1) return c->fail(FEA_E_UNSUPPORTED, "tensor kernel does not fit: %d B shared memory", c->t_smem);
     c->t_grid = (int)std::min<int64_t>(std::max<int64_t>(nb, 1), (int64_t)occ * c->sm_count);
@@ -1460,6 +1512,8 @@ fea_status fea_assemble_tensor(fea_ctx c, const double* u_full, const double* v_
     prm.u = u_full;
     prm.v = v_full;
     prm.tab = c->d_ttab;
+    prm.qfrag = c->d_tables;
+    prm.kver = c->t_kver;
     prm.out_m = mt_vals;
     prm.out_c = c->split ? nullptr : ct_vals;
     prm.nblocks = c->t_nblocks;
@@ -1474,6 +1528,7 @@ fea_status fea_assemble_tensor(fea_ctx c, const double* u_full, const double* v_
     }
     if (c->split && ct_vals) {  // C o2 v with the rule of C
         prm.tab = c->d_ttab_c;
+        prm.qfrag = c->d_tables_c;
         prm.nq = c->nq_c;
         prm.out_m = nullptr;
         prm.out_c = ct_vals;
@@ -1546,6 +1601,12 @@ fea_status fea_get_stat(fea_ctx c, int key, int64_t* value) {
             }
             return c->fail(FEA_E_ARG, "unknown stat key %d", key);
         case 11: *value = c->kver; break;
+        case 16: *value = c->have_tplan ? c->t_nblocks : -1; break;
+        case 17: *value = c->have_tplan ? c->t_visits : -1; break;
+        case 18: *value = c->have_tplan ? c->t_owned : -1; break;
+        case 19: *value = c->have_tplan ? c->t_smem : -1; break;
+        case 12: *value = c->have_tplan ? c->t_kver : -1; break;
+        case 13: *value = c->have_tplan ? c->t_grid : -1; break;
         case 14: *value = c->maxI; break;
         case 15: *value = c->n_int; break;
     }

@@ -172,7 +172,7 @@ struct FeaKParams {
 // i <= k / i > k, indexed by the symmetric row of (min, max)), one record stage, reference tables
 // (Phi [np][16], J [2][np][16], w [16]), mbarrier.
 enum { FEA_LT_V1 = 0, FEA_LT_VUP = 1, FEA_LT_VDN = 2, FEA_LT_REC = 3, FEA_LT_TAB = 4, FEA_LT_BAR = 5,
-       FEA_LT_TOTAL = 6, FEA_LT_N = 8 };
+       FEA_LT_TOTAL = 6, FEA_LT_N = 20 };
 #define FEA_T_WARPS 8
 __host__ __device__ inline void fea_t_smem_layout(int32_t* L, int rec_max, int e_max, int p) {
     const int T = fea_T(p), np = fea_np(p), vs = e_max | 1;
@@ -187,6 +187,49 @@ __host__ __device__ inline void fea_t_smem_layout(int32_t* L, int rec_max, int e
     L[FEA_LT_TOTAL] = o;
     L[7] = 0;
 }
+// k_tensor4 (DMMA tensor kernel, fea_kernels_t.cu): row tiles of 8 output rows = the T symmetric rows
+// of (M o2 v) (Q_m A-fragments, shared with the matrix kernel) and the np^2 rows (i, k) of (C o2 v)
+// (R_d A-fragments, R_d[(i, k), q] = J_d,i(q) phi_k(q), d = 0, 1); consumer warp group g of NG keeps
+// the M tiles g, g + NG, ... (RM of them) and the C tiles g, g + NG, ... (RC) as register fragments;
+// S warps per group split the element tiles.
+__host__ __device__ constexpr int fea_ntc(int p) { return (fea_np(p) * fea_np(p) + 7) / 8; }
+__host__ __device__ constexpr int fea_t4_ntm(int p, bool m) { return m ? fea_ntt(p) : 0; }
+__host__ __device__ constexpr int fea_t4_ntcm(int p, bool c) { return c ? fea_ntc(p) : 0; }
+__host__ __device__ constexpr int fea_t4_wmax(int p) { return p == 4 ? 8 : p == 3 ? 10 : 16; }
+__host__ __device__ constexpr int fea_t4_ng(int p, bool m, bool c) {
+    return fea_t4_ntm(p, m) > fea_t4_ntcm(p, c) ? (fea_t4_ntm(p, m) < fea_t4_wmax(p) ? fea_t4_ntm(p, m) : fea_t4_wmax(p))
+                                                : (fea_t4_ntcm(p, c) < fea_t4_wmax(p) ? fea_t4_ntcm(p, c) : fea_t4_wmax(p));
+}
+__host__ __device__ constexpr int fea_t4_rm(int p, bool m, bool c) { return (fea_t4_ntm(p, m) + fea_t4_ng(p, m, c) - 1) / fea_t4_ng(p, m, c); }
+__host__ __device__ constexpr int fea_t4_rc(int p, bool m, bool c) { return (fea_t4_ntcm(p, c) + fea_t4_ng(p, m, c) - 1) / fea_t4_ng(p, m, c); }
+__host__ __device__ constexpr int fea_t4_s(int p, bool m, bool c) { return fea_t4_wmax(p) / fea_t4_ng(p, m, c) > 1 ? fea_t4_wmax(p) / fea_t4_ng(p, m, c) : 1; }
+__host__ __device__ constexpr int fea_t4_threads(int p, bool m, bool c) { return (fea_t4_ng(p, m, c) * fea_t4_s(p, m, c) + 1) * 32; }
+// offset (doubles) of the R_d fragments [NTC][2][NK][32] in the rule's fragment buffer (after Q_f and Phi^T)
+__host__ __device__ constexpr int fea_rfrag_off(int p, int nk) { return 4 * fea_ntt(p) * nk * 32 + ((4 * nk + 7) / 8) * fea_kt(p) * 32; }
+enum { FEA_LT4_REC = 0, FEA_LT4_GU = 2, FEA_LT4_GV = 4, FEA_LT4_GX = 6, FEA_LT4_LM = 8, FEA_LT4_P0 = 9, FEA_LT4_P1 = 10,
+       FEA_LT4_TAB = 11, FEA_LT4_V1 = 12, FEA_LT4_VUP = 13, FEA_LT4_VDN = 14, FEA_LT4_BARS = 15, FEA_LT4_TOTAL = 16 };
+// e_max == 8 mod 16 (as v4); V row stride fea4_vstride(e_max); two record and gather stages
+__host__ __device__ inline void fea_t4_smem_layout(int32_t* L, int rec_max, int e_max, int p, int nq) {
+    const int T = fea_T(p), np = fea_np(p), vs = fea4_vstride(e_max);
+    const int nqp = 4 * fea_nk_kernel(p, nq);
+    for (int i = 0; i < FEA_LT_N; ++i) L[i] = 0;
+    int32_t o = 0;
+    for (int s = 0; s < 2; ++s) { L[FEA_LT4_REC + s] = o; o = fea_align(o + rec_max, 128); }
+    for (int s = 0; s < 2; ++s) {
+        L[FEA_LT4_GU + s] = o; o = fea_align(o + 8 * np * e_max, 16);
+        L[FEA_LT4_GV + s] = o; o = fea_align(o + 8 * np * e_max, 16);
+        L[FEA_LT4_GX + s] = o; o = fea_align(o + 16 * 3 * e_max, 16);
+    }
+    L[FEA_LT4_LM] = o; o = fea_align(o + 8 * nqp * e_max, 16);
+    L[FEA_LT4_P0] = o; o = fea_align(o + 8 * nqp * e_max, 16);
+    L[FEA_LT4_P1] = o; o = fea_align(o + 8 * nqp * e_max, 16);
+    L[FEA_LT4_TAB] = o; o = fea_align(o + 8 * (3 * np * 16 + 16), 128);
+    L[FEA_LT4_V1] = o; o = fea_align(o + 8 * T * vs, 128);
+    L[FEA_LT4_VUP] = o; o = fea_align(o + 8 * T * vs, 128);
+    L[FEA_LT4_VDN] = o; o = fea_align(o + 8 * T * vs, 128);
+    L[FEA_LT4_BARS] = o; o += 8 * 8;
+    L[FEA_LT4_TOTAL] = o;
+}
 struct FeaTParams {
     const FeaBlock* blocks;
     const uint8_t* records;
@@ -197,12 +240,13 @@ struct FeaTParams {
     const double* tab;    // Phi [np][16], J [2][np][16], w [16] (zero padded)
     double* out_m;        // (M o2 v) values or nullptr
     double* out_c;        // (C o2 v) values or nullptr
-    int32_t nblocks, e_max, nq, pad_;
+    const double* qfrag;  // k_tensor4: the rule's fragment buffer (Q_m at 0, R_d at fea_rfrag_off)
+    int32_t nblocks, e_max, nq, kver;  // kver: 1 = k_tensor (lane per element), 4 = k_tensor4 (DMMA)
     int32_t lay[FEA_LT_N];
     FeaCoef coef_m, coef_c;  // k' of these
 };
 int fea_launch_tensor(const FeaTParams& prm, int order, int smem_bytes, int grid, void* stream);
-int fea_tensor_occupancy(int order, int smem_bytes, int* ctas_per_sm, int* threads);
+int fea_tensor_occupancy(int order, int nq, int kver, int smem_bytes, int* ctas_per_sm, int* threads);
 
 // interface-only exchange of u (fea_kernels_x.cu)
 int fea_launch_pack(const double* u_owned, const int32_t* I, int nI, int64_t R0, int maxI, double* send, void* stream);

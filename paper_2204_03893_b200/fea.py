@@ -21,6 +21,7 @@ FEA_REORDER_NONE, FEA_REORDER_MORTON = 0, 1
 FEA_MASS, FEA_STIFF = 1, 2
 FEA_K_POLY, FEA_K_EXP, FEA_K_PWL = 0, 1, 2
 FEA_TUNE_SMEM_BUDGET, FEA_TUNE_KERNEL, FEA_TUNE_EMAX, FEA_TUNE_PLAN_WHICH = 1, 2, 3, 4
+FEA_TUNE_TENSOR_KERNEL = 8
 
 # the exported C symbols (tests check every one of them against include/fea.h)
 SYMBOLS = ["fea_create", "fea_set_element", "fea_set_rule", "fea_mesh_upload", "fea_set_tuning", "fea_build_pattern",

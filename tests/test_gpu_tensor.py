@@ -16,12 +16,13 @@ pytestmark = pytest.mark.gpu
 TOL = 1e-12
 
 
-def _run(mesh, q_xy, q_w, u_user, v_user, p, mcoef, ccoef, do_m=True, do_c=True, reorder=True):
+def _run(mesh, q_xy, q_w, u_user, v_user, p, mcoef, ccoef, do_m=True, do_c=True, reorder=True, tker=0):
     import torch
-    from paper_2204_03893_b200.fea import FEA_MASS, FEA_STIFF, Context
+    from paper_2204_03893_b200.fea import FEA_MASS, FEA_STIFF, FEA_TUNE_TENSOR_KERNEL, Context
     ctx = Context(device=0)
     ctx.set_element(p, q_xy, q_w)
     ctx.mesh_upload(mesh.vert_xy, mesh.elem_vert, mesh.n_dof, mesh.elem_dof, reorder=reorder)
+    ctx.set_tuning(FEA_TUNE_TENSOR_KERNEL, tker)
     ctx.build_pattern()
     ctx.set_coefficient(FEA_MASS, mcoef[0], mcoef[1])
     ctx.set_coefficient(FEA_STIFF, ccoef[0], ccoef[1])
@@ -34,6 +35,7 @@ def _run(mesh, q_xy, q_w, u_user, v_user, p, mcoef, ccoef, do_m=True, do_c=True,
     ct = torch.full((n,), np.nan, dtype=torch.float64, device=dev) if do_c else None
     ctx.assemble_tensor(u, v, mt, ct)
     ctx.sync()
+    assert ctx.stat(12) == (tker or ctx.stat(12)) and ctx.stat(12) in (1, 4)
     rp, ci = ctx.get_pattern()
     mlib = copy.copy(mesh)
     mlib.elem_dof = lib_numbering(mesh, perm)
@@ -54,8 +56,12 @@ def _run(mesh, q_xy, q_w, u_user, v_user, p, mcoef, ccoef, do_m=True, do_c=True,
     return out
 
 
+TKER = [1, 4]  # FEA_TUNE_TENSOR_KERNEL: k_tensor (lane per element), k_tensor4 (DMMA)
+
+
+@pytest.mark.parametrize("tker", TKER)
 @pytest.mark.parametrize("p", [1, 2, 3, 4])
-def test_tensor_parity_random_mesh(p):
+def test_tensor_parity_random_mesh(p, tker):
     """Both contractions, every order, the configs' minimal rule, polynomial and exp k."""
     m = random_mesh_from_structured(8, p, seed=300 + p)
     rng = np.random.default_rng(p)
@@ -64,12 +70,13 @@ def test_tensor_parity_random_mesh(p):
     xy, w = triangle_rule(2 * p)
     for mc, cc in (((K_POLY, (1.0, 0.0, 1.0)), (K_POLY, (1.0, 0.0, 0.0, 0.0, 1.0))),
                    ((K_EXP, (1.3, 0.5)), (K_EXP, (0.7, -0.3)))):
-        err = _run(m, xy, w, u, v, p, mc, cc)
+        err = _run(m, xy, w, u, v, p, mc, cc, tker=tker)
         assert err["M"] <= TOL and err["C"] <= TOL, err
 
 
+@pytest.mark.parametrize("tker", TKER)
 @pytest.mark.parametrize("p", [1, 2, 3, 4])
-def test_tensor_modes_generic_rule_pwl(p):
+def test_tensor_modes_generic_rule_pwl(p, tker):
     """Mass-only / conductivity-only launches, a non-minimal rule (generic kernel), PWL k
     (k' = segment slope), user numbering."""
     m = random_mesh_from_structured(6, p, seed=310 + p)
@@ -78,28 +85,30 @@ def test_tensor_modes_generic_rule_pwl(p):
     v = rng.uniform(-2, 2, m.n_dof)
     pwl = (K_PWL, (-1.0, 1.5, 0.0, 0.7, 1.0, 0.5))
     xy, w = triangle_rule(min(8, 2 * p + 2))
-    assert _run(m, xy, w, u, v, p, pwl, pwl, do_c=False, reorder=False)["M"] <= TOL
-    assert _run(m, xy, w, u, v, p, pwl, pwl, do_m=False, reorder=False)["C"] <= TOL
+    assert _run(m, xy, w, u, v, p, pwl, pwl, do_c=False, reorder=False, tker=tker)["M"] <= TOL
+    assert _run(m, xy, w, u, v, p, pwl, pwl, do_m=False, reorder=False, tker=tker)["C"] <= TOL
 
 
+@pytest.mark.parametrize("tker", TKER)
 @pytest.mark.parametrize("p", [1, 2, 3, 4])
-def test_tensor_single_element(p):
+def test_tensor_single_element(p, tker):
     for mesh in (single_element_mesh((0.0, 0.0), (1.0, 0.0), (0.0, 1.0), p=p),
                  single_element_mesh((0.3, -0.2), (1.7, 0.4), (0.1, 2.0), p=p)):
         rng = np.random.default_rng(p)
         u = rng.uniform(0, 1, mesh.n_dof)
         v = rng.normal(size=mesh.n_dof)
         xy, w = triangle_rule(2 * p)
-        err = _run(mesh, xy, w, u, v, p, (K_POLY, (1.0, 0.0, 1.0)), (K_POLY, (1.0, 0.0, 1.0)))
+        err = _run(mesh, xy, w, u, v, p, (K_POLY, (1.0, 0.0, 1.0)), (K_POLY, (1.0, 0.0, 1.0)), tker=tker)
         assert err["M"] <= TOL and err["C"] <= TOL, err
 
 
-@pytest.mark.parametrize("name,N", [("C2", 40), ("C3", 20)])
-def test_tensor_config_shapes(name, N):
+@pytest.mark.parametrize("tker", TKER)
+@pytest.mark.parametrize("name,N", [("C2", 40), ("C3", 20), ("C5", 10)])
+def test_tensor_config_shapes(name, N, tker):
     """Config-shaped meshes (several blocks, ragged tail): u, v = two iterates of the workload."""
     cfg = scaled(CONFIGS[name], N)
     wl = make_workload(cfg)
     us = list(wl.u_sequence(2))
     coef = (cfg.k_kind, tuple(cfg.k_par))
-    err = _run(wl.mesh, wl.q_xy, wl.q_w, us[0], us[1] - us[0], cfg.p, coef, coef)
+    err = _run(wl.mesh, wl.q_xy, wl.q_w, us[0], us[1] - us[0], cfg.p, coef, coef, tker=tker)
     assert err["M"] <= TOL and err["C"] <= TOL, err
