@@ -1041,11 +1041,25 @@ fea_status fea_build_pattern(fea_ctx c, int64_t* row_begin, int64_t* n_rows_loca
         const int64_t budget = c->tune_smem ? c->tune_smem : (ctas == 2 ? 113 * 1024 : 226 * 1024);
         const int nqp = c->split ? 16 : 4 * fea_nk_kernel(c->order, nq);  // split rules: room for either
         const int64_t per_el_smem = 8LL * T * nmat + 2 * (8LL * np + 48) + 2 * 8LL * nqp + 32;
-        const double rec_el = 1.3 * (3.0 * np * np + 4.0 * np) + 8;  // record bytes per element (estimate)
-        e_max = (int64_t)((budget - 256 - 3 * 128 - 16LL * T * nmat) / (per_el_smem + rstages * rec_el));
-        e_max = std::min<int64_t>(e_max, 65535 / T);
-        e_max = e_max >= 8 ? ((e_max - 8) / 16) * 16 + 8 : 0;  // multiple of 8, == 8 mod 16
-        rec_budget = ((int64_t)(rec_el * e_max) + 15) & ~int64_t(15);
+        double rec_el = 1.3 * (3.0 * np * np + 4.0 * np) + 8;  // record bytes per element (estimate)
+        const int64_t r0 = 32 * FEA_MAX_CLASSES + 1024;            // per-record constant part
+        for (int pass = 0; pass < 2; ++pass) {  // pass 1: the first plan's own record bytes per element
+            e_max = (int64_t)((budget - 256 - 3 * 128 - 16LL * T * nmat - rstages * r0) / (per_el_smem + rstages * rec_el));
+            e_max = std::min<int64_t>(e_max, 65535 / T);
+            e_max = e_max >= 8 ? ((e_max - 8) / 16) * 16 + 8 : 0;  // multiple of 8, == 8 mod 16
+            rec_budget = ((int64_t)(rec_el * e_max) + r0 + 15) & ~int64_t(15);
+            if (pass == 1 || e_max < 8) break;
+            PlanData P0;  // on the first rows only (a sample: records of interior blocks are alike)
+            const int64_t nr_all = c->n_rows;
+            c->n_rows = std::min<int64_t>(nr_all, 20000);
+            const fea_status st0 = build_blocks(c, false, false, e_max, rec_budget, fea4_vstride((int32_t)e_max), P0);
+            c->n_rows = nr_all;
+            if (st0 != FEA_OK) break;
+            int32_t L0[FEA_L_N];
+            fea_smem_layout(L0, rstages, (int)P0.rec_max, (int)e_max, c->order, c->split ? 0 : nq, dm, dcm);
+            if (budget - L0[FEA_L_TOTAL] < 8 * 1024) break;
+            rec_el = 1.02 * (double)std::max<int64_t>(P0.rec_max - r0, 16) / (double)e_max;
+        }
     }
 
     const int64_t EM = v5 ? (e_max | 1) : fea4_vstride((int32_t)e_max);  // V row strides (fea_internal.h)
