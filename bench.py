@@ -371,7 +371,7 @@ def run_ours(args):
             if asm.ctx.stat(11) == 5:  # per-warp timeline of k_reassemble5 (lane 0 of every warp)
                 names = ["compute", "move_refill", "full_wait", "rec_wait", "phaseB", "free_wait", "prologue"]
             else:
-                names = ["rec_wait", "gather", "phaseA", "phaseB", "issue", "barriers"]
+                names = ["unused0", "unused1", "A2_dmma", "B_and_next_A1", "unused4", "barrier_wait"]
             ph = [asm.ctx.stat(20 + i) for i in range(len(names))]
             tot = sum(ph) or 1
             desc["phase_cycles_pct"] = dict(zip(names, [round(100.0 * x / tot, 1) for x in ph]))

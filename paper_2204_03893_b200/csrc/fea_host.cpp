@@ -1536,6 +1536,7 @@ fea_status fea_assemble_tensor(fea_ctx c, const double* u_full, const double* v_
     std::memcpy(prm.lay, c->t_lay, sizeof(prm.lay));
     prm.coef_m = c->coef_m;
     prm.coef_c = c->coef_c;
+    prm.same_coef = same_coef(c->coef_m, c->coef_c) ? 1 : 0;
     if (prm.out_m || prm.out_c) {
         const int rc = fea_launch_tensor(prm, c->order, c->t_smem, c->t_grid, c->stream);
         if (rc != 0) return c->fail(FEA_E_CUDA, "k_tensor launch: %s", cudaGetErrorString((cudaError_t)rc));

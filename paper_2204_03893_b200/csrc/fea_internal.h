@@ -23,11 +23,17 @@ __host__ __device__ constexpr int fea_nk(int nq) { return (nq + 3) / 4; }
 // generic kernel, which pads the quadrature dimension to 16 (4 k-steps)
 __host__ __device__ constexpr int fea_nq_native(int p) { return p == 1 ? 3 : p == 2 ? 6 : p == 3 ? 12 : 16; }
 __host__ __device__ constexpr int fea_nk_kernel(int p, int nq) { return nq == fea_nq_native(p) ? fea_nk(nq) : 4; }
-// element-tile subsets per row tile (consumer warps = NTT * S)
+// element-tile subsets per warp group (consumer warps = fea_ngrp * S)
 __host__ __device__ constexpr int fea_S(int p) { return p == 1 ? 8 : p == 2 ? 3 : p == 3 ? 2 : 1; }
 __host__ __device__ constexpr int fea_ctas(int p) { return p <= 2 ? 2 : 1; }
 __host__ __device__ constexpr int fea_rstages(int p) { return p <= 2 ? 3 : 2; }
-__host__ __device__ constexpr int fea_threads(int p) { return (fea_ntt(p) * fea_S(p) + 1) * 32; }
+// row tiles per consumer warp (B-fragment loads shared by RT tiles); warp groups = ceil(NTT / RT)
+#ifndef FEA4_RT4
+#define FEA4_RT4 1
+#endif
+__host__ __device__ constexpr int fea_rt(int p) { return p == 4 ? FEA4_RT4 : 1; }
+__host__ __device__ constexpr int fea_ngrp(int p) { return (fea_ntt(p) + fea_rt(p) - 1) / fea_rt(p); }
+__host__ __device__ constexpr int fea_threads(int p) { return (fea_ngrp(p) * fea_S(p) + 1) * 32; }
 // p >= 2: the interpolation U = Phi^T U_e also runs on DMMA (M = quadrature points in tiles of
 // 8, K = element nodes in k-steps of 4); A-fragments of Phi^T [MT][KT][32] follow Q_f in qfrag.
 __host__ __device__ constexpr bool fea_interp_mma(int p) { return p >= 2; }
@@ -195,7 +201,7 @@ __host__ __device__ inline void fea_t_smem_layout(int32_t* L, int rec_max, int e
 __host__ __device__ constexpr int fea_ntc(int p) { return (fea_np(p) * fea_np(p) + 7) / 8; }
 __host__ __device__ constexpr int fea_t4_ntm(int p, bool m) { return m ? fea_ntt(p) : 0; }
 __host__ __device__ constexpr int fea_t4_ntcm(int p, bool c) { return c ? fea_ntc(p) : 0; }
-__host__ __device__ constexpr int fea_t4_wmax(int p) { return p == 4 ? 8 : p == 3 ? 10 : 16; }
+__host__ __device__ constexpr int fea_t4_wmax(int p) { return p == 4 ? 8 : p == 3 ? 13 : 16; }
 __host__ __device__ constexpr int fea_t4_ng(int p, bool m, bool c) {
     return fea_t4_ntm(p, m) > fea_t4_ntcm(p, c) ? (fea_t4_ntm(p, m) < fea_t4_wmax(p) ? fea_t4_ntm(p, m) : fea_t4_wmax(p))
                                                 : (fea_t4_ntcm(p, c) < fea_t4_wmax(p) ? fea_t4_ntcm(p, c) : fea_t4_wmax(p));
@@ -242,6 +248,7 @@ struct FeaTParams {
     double* out_c;        // (C o2 v) values or nullptr
     const double* qfrag;  // k_tensor4: the rule's fragment buffer (Q_m at 0, R_d at fea_rfrag_off)
     int32_t nblocks, e_max, nq, kver;  // kver: 1 = k_tensor (lane per element), 4 = k_tensor4 (DMMA)
+    int32_t same_coef, pad_;           // m == c: k_tensor4 evaluates the derivative once
     int32_t lay[FEA_LT_N];
     FeaCoef coef_m, coef_c;  // k' of these
 };

@@ -43,7 +43,8 @@ __global__ void __launch_bounds__(fea_threads(P), fea_ctas(P)) k_reassemble(cons
     const int nq = NQ_T > 0 ? NQ_T : prm.nq;
     const int e_max = prm.e_max;
     const int tid = threadIdx.x;
-    constexpr int NCT = NTT * S * 32;  // consumer threads
+    constexpr int RT = fea_rt(P), NGRP = fea_ngrp(P);
+    constexpr int NCT = NGRP * S * 32;  // consumer threads
     const bool producer = tid >= NCT;
     const int lane = tid & 31, warp = tid >> 5;
 
@@ -116,15 +117,20 @@ __global__ void __launch_bounds__(fea_threads(P), fea_ctas(P)) k_reassemble(cons
     }
 
     // ------------------------------------------------------------------ consumers
-    // This warp's row tile of Q_f as DMMA A-fragments, for the whole kernel (registers).
-    const int tt = warp % NTT, sub = warp / NTT;
+    // This warp's row tiles (grp, grp + NGRP, ...) of Q_f as DMMA A-fragments, for the whole kernel.
+    const int grp = warp % NGRP, sub = warp / NGRP;
     const int g = lane >> 2, cq = lane & 3;
-    double afr[4][NK];
+    double afr[RT][4][NK];
 #pragma unroll
-    for (int f = 0; f < 4; ++f)
+    for (int r = 0; r < RT; ++r)
 #pragma unroll
-        for (int kk = 0; kk < NK; ++kk)
-            afr[f][kk] = (f == 0 ? DO_M : DO_C) ? __ldg(prm.qfrag + ((f * NTT + tt) * NK + kk) * 32 + lane) : 0.0;
+        for (int f = 0; f < 4; ++f)
+#pragma unroll
+            for (int kk = 0; kk < NK; ++kk) {
+                const int tt = grp + r * NGRP;
+                afr[r][f][kk] = (f == 0 ? DO_M : DO_C) && tt < NTT
+                                    ? __ldg(prm.qfrag + ((f * NTT + tt) * NK + kk) * 32 + lane) : 0.0;
+            }
     constexpr bool INTERP_MMA = fea_interp_mma(P);
     constexpr int MTN = INTERP_MMA ? (NQP + 7) / 8 : 1, KTN = INTERP_MMA ? fea_kt(P) : 1;
     double pfr[MTN][KTN];  // Phi^T A-fragments (p >= 2)
@@ -194,7 +200,7 @@ __global__ void __launch_bounds__(fea_threads(P), fea_ctas(P)) k_reassemble(cons
             // U = Phi^T U_e on DMMA; epilogue Lambda_qe = w_q b_e k(u_qe) with the geometry of the
             // lane's two accumulator columns (recomputed per m-tile; the m-tile 0, g = 0 lanes store W_e)
             constexpr int MT = MTN, KT = KTN;
-            for (int un = warp; un < MT * net; un += NTT * S) {
+            for (int un = warp; un < MT * net; un += NGRP * S) {
                 const int mt = un % MT, et = un / MT;
                 double u0 = 0.0, u1 = 0.0;
 #pragma unroll
@@ -253,7 +259,6 @@ __global__ void __launch_bounds__(fea_threads(P), fea_ctas(P)) k_reassemble(cons
         // ---------------- A2: V = Q Lambda on the FP64 tensor cores (DMMA m8n8k4)
         {
             const double* Lc = two_lam ? sLc : sLm;
-            const int t = tt * 8 + g;
             for (int et = sub; et < net; et += S) {
                 const int col = et * 8 + g;       // B fragment column (element) of this lane
                 const int le0 = et * 8 + 2 * cq;  // the two accumulator columns of this lane
@@ -263,24 +268,31 @@ __global__ void __launch_bounds__(fea_threads(P), fea_ctas(P)) k_reassemble(cons
                     bm[kk] = sLm[(kk * 4 + cq) * e_max + col];
                     bc[kk] = Lc[(kk * 4 + cq) * e_max + col];
                 }
-                double m0 = 0.0, m1 = 0.0, a0 = 0.0, a1 = 0.0, b0 = 0.0, b1 = 0.0, c0 = 0.0, c1 = 0.0;
-#pragma unroll
-                for (int kk = 0; kk < NK; ++kk) {
-                    if (DO_M) dmma(m0, m1, afr[0][kk], bm[kk]);
-                    if (DO_C) {
-                        dmma(a0, a1, afr[1][kk], bc[kk]);
-                        dmma(b0, b1, afr[2][kk], bc[kk]);
-                        dmma(c0, c1, afr[3][kk], bc[kk]);
-                    }
+                double2 w0, w1, w2;
+                if (DO_C) {
+                    w0 = *reinterpret_cast<const double2*>(sW + le0);
+                    w1 = *reinterpret_cast<const double2*>(sW + e_max + le0);
+                    w2 = *reinterpret_cast<const double2*>(sW + 2 * e_max + le0);
                 }
-                if (t < T) {
-                    if (DO_M) *reinterpret_cast<double2*>(sVm + t * vs + le0) = make_double2(m0, m1);
-                    if (DO_C) {
-                        const double2 w0 = *reinterpret_cast<const double2*>(sW + le0);
-                        const double2 w1 = *reinterpret_cast<const double2*>(sW + e_max + le0);
-                        const double2 w2 = *reinterpret_cast<const double2*>(sW + 2 * e_max + le0);
-                        *reinterpret_cast<double2*>(sVc + t * vs + le0) =
-                            make_double2(fma(w0.x, a0, fma(w1.x, b0, w2.x * c0)), fma(w0.y, a1, fma(w1.y, b1, w2.y * c1)));
+#pragma unroll
+                for (int r = 0; r < RT; ++r) {
+                    const int t = (grp + r * NGRP) * 8 + g;
+                    if (RT > 1 && grp + r * NGRP >= NTT) continue;
+                    double m0 = 0.0, m1 = 0.0, a0 = 0.0, a1 = 0.0, b0 = 0.0, b1 = 0.0, c0 = 0.0, c1 = 0.0;
+#pragma unroll
+                    for (int kk = 0; kk < NK; ++kk) {
+                        if (DO_M) dmma(m0, m1, afr[r][0][kk], bm[kk]);
+                        if (DO_C) {
+                            dmma(a0, a1, afr[r][1][kk], bc[kk]);
+                            dmma(b0, b1, afr[r][2][kk], bc[kk]);
+                            dmma(c0, c1, afr[r][3][kk], bc[kk]);
+                        }
+                    }
+                    if (t < T) {
+                        if (DO_M) *reinterpret_cast<double2*>(sVm + t * vs + le0) = make_double2(m0, m1);
+                        if (DO_C)
+                            *reinterpret_cast<double2*>(sVc + t * vs + le0) =
+                                make_double2(fma(w0.x, a0, fma(w1.x, b0, w2.x * c0)), fma(w0.y, a1, fma(w1.y, b1, w2.y * c1)));
                     }
                 }
             }

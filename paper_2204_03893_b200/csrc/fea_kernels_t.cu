@@ -318,9 +318,11 @@ __global__ void __launch_bounds__(fea_t4_threads(P, DO_M, DO_C), 1) k_tensor4(co
                         double absdet, A00, A11, A01;
                         geometry(gX, e_max, le, absdet, A00, A11, A01);
                         const double uq = h ? u1 : u0, wb = W[q] * absdet;
-                        if (DO_M) lm[h] = wb * dkeval(prm.coef_m, uq) * (h ? v1 : v0);
+                        const double dm = DO_M ? dkeval(prm.coef_m, uq) : 0.0;
+                        if (DO_M) lm[h] = wb * dm * (h ? v1 : v0);
                         if (DO_C) {
-                            const double lc = wb * dkeval(prm.coef_c, uq), gx = h ? x1 : x0, gy = h ? y1 : y0;
+                            const double dc = DO_M && prm.same_coef ? dm : dkeval(prm.coef_c, uq);
+                            const double lc = wb * dc, gx = h ? x1 : x0, gy = h ? y1 : y0;
                             p0[h] = lc * fma(A00, gx, A01 * gy);
                             p1[h] = lc * fma(A01, gx, A11 * gy);
                         }
