@@ -838,15 +838,17 @@ static fea_status build_blocks(fea_ctx c, bool v5, bool orient, int64_t e_max, i
                 }
             o.fb.spare_[0] = inside ? 1 : 0;
         }
-        struct Rec { int32_t row, col, le, t; };  // t: symmetric row (| 0x8000 if orient and i > j)
+        struct Rec { int32_t row, col, le, t; };  // t: V row (| 0x10000 if orient and i > j: Vdn)
         std::vector<Rec> recs;
         for (int64_t le = 0; le < (int64_t)E.size(); ++le) {
             const int32_t* d = &c->ed[(size_t)E[le] * np];
             for (int i = 0; i < np; ++i) {
                 if (d[i] < ga || d[i] >= gb) continue;
                 for (int j = 0; j < np; ++j)
-                    recs.push_back({d[i], d[j], (int32_t)le, tri_index(np, std::min(i, j), std::max(i, j)) |
-                                                                 (orient && i > j ? 0x10000 : 0)});
+                    // tensor plans (orient): V row fea_trow (off-diagonal pairs first), flag i > j
+                    recs.push_back({d[i], d[j], (int32_t)le,
+                                    orient ? fea_trow(np, std::min(i, j), std::max(i, j)) | (i > j ? 0x10000 : 0)
+                                           : tri_index(np, std::min(i, j), std::max(i, j))});
             }
         }
         // stable: within a (row, col) slot the contributors stay in ascending le (= library element)
@@ -1044,7 +1046,8 @@ fea_status fea_build_pattern(fea_ctx c, int64_t* row_begin, int64_t* n_rows_loca
         double rec_el = 1.3 * (3.0 * np * np + 4.0 * np) + 8;  // record bytes per element (estimate)
         const int64_t r0 = 32 * FEA_MAX_CLASSES + 1024;            // per-record constant part
         for (int pass = 0; pass < 2; ++pass) {  // pass 1: the first plan's own record bytes per element
-            e_max = (int64_t)((budget - 256 - 3 * 128 - 16LL * T * nmat - rstages * r0) / (per_el_smem + rstages * rec_el));
+            e_max = (int64_t)((budget - 256 - 3 * 128 - 16LL * T * nmat - 32LL * (np + 2 * nqp) - rstages * r0) /
+                              (per_el_smem + rstages * rec_el));
             e_max = std::min<int64_t>(e_max, 65535 / T);
             e_max = e_max >= 8 ? ((e_max - 8) / 16) * 16 + 8 : 0;  // multiple of 8, == 8 mod 16
             rec_budget = ((int64_t)(rec_el * e_max) + r0 + 15) & ~int64_t(15);
@@ -1455,19 +1458,19 @@ static fea_status build_tensor_plan(fea_ctx c) {
     int64_t e_max, rec_budget;
     if (k4) {  // V1, Vup, Vdn [T][e_max + 2], two record and gather stages, Lambda and p (fea_t4_smem_layout)
         const int nqp = c->split ? 16 : 4 * fea_nk_kernel(c->order, c->nq);
-        const int64_t per_el = 3 * 8LL * T + 2 * (16LL * np + 48) + 3 * 8LL * nqp;
+        const int64_t per_el = 8LL * (3 * T - np) + 2 * (16LL * np + 48) + 3 * 8LL * nqp;
         // record bytes per element: an estimate, then (below) the planned blocks' own ratio
         const double rec_el = c->t_rec_el > 0 ? c->t_rec_el : 1.3 * (3.0 * np * np + 4.0 * np) + 8;
         const int64_t r0 = 32 * FEA_MAX_CLASSES + 1024;  // per-record constant part (class table, padding)
-        e_max = (int64_t)((budget - tabs - 1024 - 3 * 16LL * T - 2 * r0) / (per_el + 2 * rec_el));
+        e_max = (int64_t)((budget - tabs - 1024 - 64LL * (np + nqp) - 2 * r0) / (per_el + 2 * rec_el));
         if (c->tune_emax) e_max = std::min(e_max, c->tune_emax);
         e_max = std::min<int64_t>(e_max, 32767 / T - 2) / 8 * 8;
         rec_budget = ((int64_t)(rec_el * e_max) + r0 + 15) & ~int64_t(15);
     } else {
         const double rec_el = 1.1 * 2.0 * np * np + 8;
-        e_max = (int64_t)((budget - tabs - 1024) / (3 * 8.0 * T + rec_el));
+        e_max = (int64_t)((budget - tabs - 1024) / (8.0 * (3 * T - np) + rec_el));
         e_max = std::min<int64_t>(e_max, 32767 / T - 1) / 8 * 8;
-        rec_budget = (budget - tabs - 1024 - 3 * 8LL * T * (e_max | 1)) & ~int64_t(15);
+        rec_budget = (budget - tabs - 1024 - 8LL * (3 * T - np) * (e_max | 1)) & ~int64_t(15);
     }
     PlanData P;
     const fea_status st = build_blocks(c, !k4, true, e_max, rec_budget, k4 ? fea4_vstride((int32_t)e_max) : (e_max | 1), P);

@@ -77,6 +77,10 @@ static_assert(sizeof(FeaRecHdr4) == 32, "FeaRecHdr4 must be 32 bytes");
 // v4 V row stride: even (16-byte DMMA epilogue stores) and == 2 (mod 8), so phase B's gathers of
 // many rows t of one element column spread over the banks (e_max == 8 mod 16)
 __host__ __device__ inline int32_t fea4_vstride(int32_t e_max) { return e_max + 2; }
+// Row stride of Lambda / p and of the gathered u (v) in kernels v4 / k_tensor4 (doubles): == 4 mod 16
+// for e_max a multiple of 8, so the DMMA B-fragment loads [(4 kk + c) ls + 8 et + g] are
+// conflict-free per half-warp (a stride == 8 mod 16 makes them 2-way).
+__host__ __device__ inline int32_t fea4_lstride(int32_t e_max) { return e_max + 4; }
 
 // v5 record: int4 class table {C, n_items, byte offset, item bytes} [ncls], then per class n_items
 // fixed-size item records {u16 block-local slot, u16 V offset [C]} of fea5_item_bytes(C) bytes
@@ -116,12 +120,13 @@ __host__ __device__ inline void fea_smem_layout(int32_t* L, int rstages, int rec
     const int nqp = 4 * fea_nk_kernel(p, nq);
     int32_t o = 0;
     for (int s = 0; s < 3; ++s) { L[FEA_L_REC + s] = o; o = fea_align(o + (s < rstages ? rec_max : 0), 128); }
+    const int ls = fea4_lstride(e_max);
     for (int s = 0; s < 2; ++s) {
-        L[FEA_L_GU + s] = o; o = fea_align(o + 8 * np * e_max, 16);
+        L[FEA_L_GU + s] = o; o = fea_align(o + 8 * np * ls, 16);
         L[FEA_L_GX + s] = o; o = fea_align(o + 16 * 3 * e_max, 16);
     }
-    L[FEA_L_LAMM] = o; o = fea_align(o + 8 * nqp * e_max, 16);
-    L[FEA_L_LAMC] = o; o = fea_align(o + 8 * nqp * e_max, 16);
+    L[FEA_L_LAMM] = o; o = fea_align(o + 8 * nqp * ls, 16);
+    L[FEA_L_LAMC] = o; o = fea_align(o + 8 * nqp * ls, 16);
     L[FEA_L_W] = o;    o = fea_align(o + 8 * 4 * e_max, 16);  // A00, A11, A01, |det B_e|
     o = fea_align(o, 128);
     L[FEA_L_VM] = o;   o = fea_align(o + (do_m ? 8 * T * fea4_vstride(e_max) : 0), 128);
@@ -174,8 +179,8 @@ struct FeaKParams {
 
 // ---- tensor contractions (NEXT-1 / NEXT-2; kernel fea_kernels_t.cu)
 // Plan: v5 record format with orientation bits (bit 15 of a contributor offset = local i > j).
-// Shared memory: V1 [T][vs] (M o2 v, symmetric), Vup / Vdn [T][vs] (C o2 v: entries (i, k) with
-// i <= k / i > k, indexed by the symmetric row of (min, max)), one record stage, reference tables
+// Shared memory: V1 [T][vs] (M o2 v, symmetric), Vup [T][vs] / Vdn [T - np][vs] (C o2 v: entries
+// (i, k) with i <= k / i > k), all at the row fea_trow(min, max), one record stage, reference tables
 // (Phi [np][16], J [2][np][16], w [16]), mbarrier.
 enum { FEA_LT_V1 = 0, FEA_LT_VUP = 1, FEA_LT_VDN = 2, FEA_LT_REC = 3, FEA_LT_TAB = 4, FEA_LT_BAR = 5,
        FEA_LT_TOTAL = 6, FEA_LT_N = 20 };
@@ -185,7 +190,7 @@ __host__ __device__ inline void fea_t_smem_layout(int32_t* L, int rec_max, int e
     int32_t o = 0;
     L[FEA_LT_V1] = o; o = (o + 8 * T * vs + 127) / 128 * 128;
     L[FEA_LT_VUP] = o; o = (o + 8 * T * vs + 127) / 128 * 128;
-    L[FEA_LT_VDN] = o; o = (o + 8 * T * vs + 127) / 128 * 128;
+    L[FEA_LT_VDN] = o; o = (o + 8 * (T - np) * vs + 127) / 128 * 128;  // strictly lower (i > k) rows
     o = (o + 127) / 128 * 128;
     L[FEA_LT_REC] = o; o += (rec_max + 127) / 128 * 128;
     L[FEA_LT_TAB] = o; o += 8 * (3 * np * 16 + 16);
@@ -201,7 +206,10 @@ __host__ __device__ inline void fea_t_smem_layout(int32_t* L, int rec_max, int e
 __host__ __device__ constexpr int fea_ntc(int p) { return (fea_np(p) * fea_np(p) + 7) / 8; }
 __host__ __device__ constexpr int fea_t4_ntm(int p, bool m) { return m ? fea_ntt(p) : 0; }
 __host__ __device__ constexpr int fea_t4_ntcm(int p, bool c) { return c ? fea_ntc(p) : 0; }
-__host__ __device__ constexpr int fea_t4_wmax(int p) { return p == 4 ? 8 : p == 3 ? 13 : 16; }
+#ifndef FEA_T4_W4
+#define FEA_T4_W4 10
+#endif
+__host__ __device__ constexpr int fea_t4_wmax(int p) { return p == 4 ? FEA_T4_W4 : p == 3 ? 13 : 16; }
 __host__ __device__ constexpr int fea_t4_ng(int p, bool m, bool c) {
     return fea_t4_ntm(p, m) > fea_t4_ntcm(p, c) ? (fea_t4_ntm(p, m) < fea_t4_wmax(p) ? fea_t4_ntm(p, m) : fea_t4_wmax(p))
                                                 : (fea_t4_ntcm(p, c) < fea_t4_wmax(p) ? fea_t4_ntcm(p, c) : fea_t4_wmax(p));
@@ -221,20 +229,27 @@ __host__ __device__ inline void fea_t4_smem_layout(int32_t* L, int rec_max, int 
     for (int i = 0; i < FEA_LT_N; ++i) L[i] = 0;
     int32_t o = 0;
     for (int s = 0; s < 2; ++s) { L[FEA_LT4_REC + s] = o; o = fea_align(o + rec_max, 128); }
+    const int ls = fea4_lstride(e_max);
     for (int s = 0; s < 2; ++s) {
-        L[FEA_LT4_GU + s] = o; o = fea_align(o + 8 * np * e_max, 16);
-        L[FEA_LT4_GV + s] = o; o = fea_align(o + 8 * np * e_max, 16);
+        L[FEA_LT4_GU + s] = o; o = fea_align(o + 8 * np * ls, 16);
+        L[FEA_LT4_GV + s] = o; o = fea_align(o + 8 * np * ls, 16);
         L[FEA_LT4_GX + s] = o; o = fea_align(o + 16 * 3 * e_max, 16);
     }
-    L[FEA_LT4_LM] = o; o = fea_align(o + 8 * nqp * e_max, 16);
-    L[FEA_LT4_P0] = o; o = fea_align(o + 8 * nqp * e_max, 16);
-    L[FEA_LT4_P1] = o; o = fea_align(o + 8 * nqp * e_max, 16);
+    L[FEA_LT4_LM] = o; o = fea_align(o + 8 * nqp * ls, 16);
+    L[FEA_LT4_P0] = o; o = fea_align(o + 8 * nqp * ls, 16);
+    L[FEA_LT4_P1] = o; o = fea_align(o + 8 * nqp * ls, 16);
     L[FEA_LT4_TAB] = o; o = fea_align(o + 8 * (3 * np * 16 + 16), 128);
     L[FEA_LT4_V1] = o; o = fea_align(o + 8 * T * vs, 128);
     L[FEA_LT4_VUP] = o; o = fea_align(o + 8 * T * vs, 128);
-    L[FEA_LT4_VDN] = o; o = fea_align(o + 8 * T * vs, 128);
+    L[FEA_LT4_VDN] = o; o = fea_align(o + 8 * (T - np) * vs, 128);  // strictly lower (i > k) rows
     L[FEA_LT4_BARS] = o; o += 8 * 8;
     L[FEA_LT4_TOTAL] = o;
+}
+// V row of the entry pair (lo, hi), lo <= hi, in the tensor kernels: the np (np - 1) / 2 off-diagonal
+// pairs first (row-major), the np diagonal ones last, so the strictly-lower V (i > k) needs only the
+// first T - np rows and both channels address a pair with the same row
+__host__ __device__ constexpr int fea_trow(int np, int lo, int hi) {
+    return lo < hi ? lo * np - lo * (lo - 1) / 2 + (hi - lo) - lo - 1 : np * (np - 1) / 2 + lo;
 }
 struct FeaTParams {
     const FeaBlock* blocks;

@@ -41,7 +41,7 @@ __global__ void __launch_bounds__(fea_threads(P), fea_ctas(P)) k_reassemble(cons
     constexpr int NK = NQ_T > 0 ? fea_nk(NQ_T) : fea_nk(FEA_MAX_NQ);  // k-steps (generic rule: 4, zero padded)
     constexpr int NQP = 4 * NK;                                       // padded quadrature count
     const int nq = NQ_T > 0 ? NQ_T : prm.nq;
-    const int e_max = prm.e_max;
+    const int e_max = prm.e_max, ls = fea4_lstride(e_max);  // ls: Lambda / gathered-u row stride
     const int tid = threadIdx.x;
     constexpr int RT = fea_rt(P), NGRP = fea_ngrp(P);
     constexpr int NCT = NGRP * S * 32;  // consumer threads
@@ -100,7 +100,7 @@ __global__ void __launch_bounds__(fea_threads(P), fea_ctas(P)) k_reassemble(cons
             double2* gx = gXb(gs);
             for (int le = lane; le < blk.nE; le += 32) {
 #pragma unroll
-                for (int i = 0; i < NP; ++i) cp_async8(gu + i * e_max + le, prm.u + gd[i * nEp + le]);
+                for (int i = 0; i < NP; ++i) cp_async8(gu + i * ls + le, prm.u + gd[i * nEp + le]);
 #pragma unroll
                 for (int v = 0; v < 3; ++v) cp_async16(gx + v * e_max + le, prm.xy + gd[v * nEp + le]);
             }
@@ -172,7 +172,7 @@ __global__ void __launch_bounds__(fea_threads(P), fea_ctas(P)) k_reassemble(cons
                     sW[2 * e_max + le] = A01;
                     double ue[NP];
 #pragma unroll
-                    for (int i = 0; i < NP; ++i) ue[i] = gU[i * e_max + le];
+                    for (int i = 0; i < NP; ++i) ue[i] = gU[i * ls + le];
 #pragma unroll
                     for (int q = 0; q < NQP; ++q) {
                         double lm = 0.0, lc = 0.0;
@@ -184,14 +184,14 @@ __global__ void __launch_bounds__(fea_threads(P), fea_ctas(P)) k_reassemble(cons
                             lm = wb * keval(DO_M ? prm.coef_m : prm.coef_c, uq);
                             lc = two_lam ? wb * keval(prm.coef_c, uq) : lm;
                         }
-                        sLm[q * e_max + le] = lm;
-                        if (two_lam) sLc[q * e_max + le] = lc;
+                        sLm[q * ls + le] = lm;
+                        if (two_lam) sLc[q * ls + le] = lc;
                     }
                 } else {  // padding columns of the last element tile
 #pragma unroll
                     for (int q = 0; q < NQP; ++q) {
-                        sLm[q * e_max + le] = 0.0;
-                        if (two_lam) sLc[q * e_max + le] = 0.0;
+                        sLm[q * ls + le] = 0.0;
+                        if (two_lam) sLc[q * ls + le] = 0.0;
                     }
                     sW[le] = sW[e_max + le] = sW[2 * e_max + le] = 0.0;
                 }
@@ -206,7 +206,7 @@ __global__ void __launch_bounds__(fea_threads(P), fea_ctas(P)) k_reassemble(cons
 #pragma unroll
                 for (int kt = 0; kt < KT; ++kt) {
                     const int i = kt * 4 + cq;
-                    const double b = i < NP ? gU[i * e_max + et * 8 + g] : 0.0;
+                    const double b = i < NP ? gU[i * ls + et * 8 + g] : 0.0;
                     double a = pfr[0][kt];  // select the m-tile without dynamic register indexing
 #pragma unroll
                     for (int m2 = 1; m2 < MT; ++m2) a = mt == m2 ? pfr[m2][kt] : a;
@@ -233,8 +233,8 @@ __global__ void __launch_bounds__(fea_threads(P), fea_ctas(P)) k_reassemble(cons
                             if (le0 + 1 < nE) lc1 = w * d1 * keval(prm.coef_c, u1);
                         }
                     }
-                    *reinterpret_cast<double2*>(sLm + q * e_max + le0) = make_double2(lm0, lm1);
-                    if (two_lam) *reinterpret_cast<double2*>(sLc + q * e_max + le0) = make_double2(lc0, lc1);
+                    *reinterpret_cast<double2*>(sLm + q * ls + le0) = make_double2(lm0, lm1);
+                    if (two_lam) *reinterpret_cast<double2*>(sLc + q * ls + le0) = make_double2(lc0, lc1);
                 }
             }
         }
@@ -265,8 +265,8 @@ __global__ void __launch_bounds__(fea_threads(P), fea_ctas(P)) k_reassemble(cons
                 double bm[NK], bc[NK];
 #pragma unroll
                 for (int kk = 0; kk < NK; ++kk) {
-                    bm[kk] = sLm[(kk * 4 + cq) * e_max + col];
-                    bc[kk] = Lc[(kk * 4 + cq) * e_max + col];
+                    bm[kk] = sLm[(kk * 4 + cq) * ls + col];
+                    bc[kk] = Lc[(kk * 4 + cq) * ls + col];
                 }
                 double2 w0, w1, w2;
                 if (DO_C) {

@@ -124,7 +124,7 @@ __global__ void __launch_bounds__(FEA_T_WARPS * 32, 1) k_tensor(const __grid_con
                         double s = 0.0;
 #pragma unroll
                         for (int q = 0; q < NQ; ++q) s = fma(Phi[i * 16 + q], y[q], s);
-                        sV1[(i * NP - i * (i - 1) / 2 + (k - i)) * vs + le] = s;
+                        sV1[fea_trow(NP, i, k) * vs + le] = s;
                     }
                 }
             }
@@ -140,8 +140,7 @@ __global__ void __launch_bounds__(FEA_T_WARPS * 32, 1) k_tensor(const __grid_con
                         double s = 0.0;
 #pragma unroll
                         for (int q = 0; q < NQ; ++q) s = fma(r[q], Phi[k * 16 + q], s);
-                        const int lo = min(i, k), hi = max(i, k);
-                        const int t = lo * NP - lo * (lo - 1) / 2 + (hi - lo);
+                        const int t = fea_trow(NP, min(i, k), max(i, k));
                         (i <= k ? sVu : sVd)[t * vs + le] = s;
                     }
                 }
@@ -161,9 +160,10 @@ __global__ void __launch_bounds__(FEA_T_WARPS * 32, 1) k_tensor(const __grid_con
 // coordinates), then per block
 //   A1  u_q, v_q = Phi^T (u_e, v_e), g_q = J_q^T v_e on DMMA, then per (q, e):
 //       lambda_q = w_q |det B_e| m'(u_q) v_q, p_q = w_q |det B_e| c'(u_q) A_e g_q
-//   A2  V1[t, e] = sum_q Q_m[t, q] lambda_qe                 (t = (i <= k); Q_m = Phi (.) Phi)
+//   A2  V1[t, e] = sum_q Q_m[t, q] lambda_qe                 (t = (i <= k); Q_m = Phi (.) Phi;
+//                                                             stored at row fea_trow(i, k))
 //       N[(i, k), e] = sum_d sum_q J_d,i(q) phi_k(q) p_dqe   (all (i, k); stored to Vup (i <= k) or
-//                                                             Vdn (i > k) at the symmetric row of (min, max))
+//                                                             Vdn (i > k) at row fea_trow(min, max))
 //   B   phase_b5 with orientation (the plan's bit 15 picks Vup / Vdn).
 // Software pipeline, two CTA barriers per block: A1(0) | for j: A2(j) | B(j) and A1(j + 1) |.
 template <int P, int NQ_T, bool DO_M, bool DO_C>
@@ -176,7 +176,7 @@ __global__ void __launch_bounds__(fea_t4_threads(P, DO_M, DO_C), 1) k_tensor4(co
     constexpr int RM = fea_t4_rm(P, DO_M, DO_C), RC = fea_t4_rc(P, DO_M, DO_C);
     constexpr int NCT = NG * S * 32;  // consumer threads
     const int nq = NQ_T > 0 ? NQ_T : prm.nq;
-    const int e_max = prm.e_max, vs = fea4_vstride(e_max);
+    const int e_max = prm.e_max, vs = fea4_vstride(e_max), ls = fea4_lstride(e_max);
     const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
     const bool producer = tid >= NCT;
 
@@ -200,6 +200,11 @@ __global__ void __launch_bounds__(fea_t4_threads(P, DO_M, DO_C), 1) k_tensor4(co
     const int ncta_blocks = prm.nblocks > (int)blockIdx.x ? (prm.nblocks - 1 - (int)blockIdx.x) / (int)gridDim.x + 1 : 0;
 
     for (int i = tid; i < 3 * NP * 16 + 16; i += blockDim.x) sTab[i] = prm.tab[i];
+    // V1 row of the Q_m fragment row t (tri order i <= k) -> fea_trow
+    __shared__ int sTrow[T];
+    for (int lo = 0; lo < NP; ++lo)
+        for (int hi = lo; hi < NP; ++hi)
+            if (tid == 0) sTrow[lo * NP - lo * (lo - 1) / 2 + (hi - lo)] = fea_trow(NP, lo, hi);
     if (tid == 0) {
         for (int s = 0; s < 2; ++s) {
             mbar_init(&full_rec[s], 1);
@@ -234,8 +239,8 @@ __global__ void __launch_bounds__(fea_t4_threads(P, DO_M, DO_C), 1) k_tensor4(co
 #pragma unroll
                 for (int i = 0; i < NP; ++i) {
                     const int d = gd[i * nEp + le];
-                    cp_async8(gu + i * e_max + le, prm.u + d);
-                    cp_async8(gv + i * e_max + le, prm.v + d);
+                    cp_async8(gu + i * ls + le, prm.u + d);
+                    cp_async8(gv + i * ls + le, prm.v + d);
                 }
 #pragma unroll
                 for (int v = 0; v < 3; ++v) cp_async16(gx + v * e_max + le, prm.xy + gd[v * nEp + le]);
@@ -298,8 +303,8 @@ __global__ void __launch_bounds__(fea_t4_threads(P, DO_M, DO_C), 1) k_tensor4(co
             for (int kt = 0; kt < KT; ++kt) {
                 const int i = kt * 4 + cq, qa = mt * 8 + g;
                 const bool ok = i < NP;
-                const double bu = ok ? gU[i * e_max + et * 8 + g] : 0.0;
-                const double bv = ok ? gV[i * e_max + et * 8 + g] : 0.0;
+                const double bu = ok ? gU[i * ls + et * 8 + g] : 0.0;
+                const double bv = ok ? gV[i * ls + et * 8 + g] : 0.0;
                 const double aphi = ok ? Phi[i * 16 + qa] : 0.0;
                 dmma(u0, u1, aphi, bu);
                 if (DO_M) dmma(v0, v1, aphi, bv);
@@ -328,10 +333,10 @@ __global__ void __launch_bounds__(fea_t4_threads(P, DO_M, DO_C), 1) k_tensor4(co
                         }
                     }
                 }
-                if (DO_M) *reinterpret_cast<double2*>(sLm + q * e_max + le0) = make_double2(lm[0], lm[1]);
+                if (DO_M) *reinterpret_cast<double2*>(sLm + q * ls + le0) = make_double2(lm[0], lm[1]);
                 if (DO_C) {
-                    *reinterpret_cast<double2*>(sP0 + q * e_max + le0) = make_double2(p0[0], p0[1]);
-                    *reinterpret_cast<double2*>(sP1 + q * e_max + le0) = make_double2(p1[0], p1[1]);
+                    *reinterpret_cast<double2*>(sP0 + q * ls + le0) = make_double2(p0[0], p0[1]);
+                    *reinterpret_cast<double2*>(sP1 + q * ls + le0) = make_double2(p1[0], p1[1]);
                 }
             }
         }
@@ -354,7 +359,7 @@ __global__ void __launch_bounds__(fea_t4_threads(P, DO_M, DO_C), 1) k_tensor4(co
             double bm[NK], b0[NK], b1[NK];
 #pragma unroll
             for (int kk = 0; kk < NK; ++kk) {
-                const int o = (kk * 4 + cq) * e_max + col;
+                const int o = (kk * 4 + cq) * ls + col;
                 bm[kk] = DO_M ? sLm[o] : 0.0;
                 b0[kk] = DO_C ? sP0[o] : 0.0;
                 b1[kk] = DO_C ? sP1[o] : 0.0;
@@ -366,7 +371,7 @@ __global__ void __launch_bounds__(fea_t4_threads(P, DO_M, DO_C), 1) k_tensor4(co
                 double x0 = 0.0, x1 = 0.0;
 #pragma unroll
                 for (int kk = 0; kk < NK; ++kk) dmma(x0, x1, am[r][kk], bm[kk]);
-                if (t < T) *reinterpret_cast<double2*>(sV1 + t * vs + le0) = make_double2(x0, x1);
+                if (t < T) *reinterpret_cast<double2*>(sV1 + sTrow[t] * vs + le0) = make_double2(x0, x1);
             }
 #pragma unroll
             for (int r = 0; r < RC; ++r) {
@@ -380,8 +385,7 @@ __global__ void __launch_bounds__(fea_t4_threads(P, DO_M, DO_C), 1) k_tensor4(co
                 }
                 if (rr < NP * NP) {
                     const int i = rr / NP, k = rr - i * NP;
-                    const int lo = min(i, k), hi = max(i, k);
-                    const int t = lo * NP - lo * (lo - 1) / 2 + (hi - lo);
+                    const int t = fea_trow(NP, min(i, k), max(i, k));
                     *reinterpret_cast<double2*>((i <= k ? sVu : sVd) + t * vs + le0) = make_double2(x0, x1);
                 }
             }

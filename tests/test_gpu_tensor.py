@@ -112,3 +112,37 @@ def test_tensor_config_shapes(name, N, tker):
     coef = (cfg.k_kind, tuple(cfg.k_par))
     err = _run(wl.mesh, wl.q_xy, wl.q_w, us[0], us[1] - us[0], cfg.p, coef, coef, tker=tker)
     assert err["M"] <= TOL and err["C"] <= TOL, err
+
+
+@pytest.mark.parametrize("p", [2, 3, 4])
+def test_tensor4_deterministic_across_tilings(p):
+    """k_tensor4: bit-identical values across runs and element caps per block (FEA_TUNE_EMAX):
+    per-element DMMA arithmetic does not depend on the element's tile position, and phase B sums
+    every slot in ascending library element order (reading 11)."""
+    import torch
+    from paper_2204_03893_b200.fea import FEA_MASS, FEA_STIFF, FEA_TUNE_EMAX, FEA_TUNE_TENSOR_KERNEL, Context
+    m = random_mesh_from_structured(10, p, seed=330 + p)
+    xy, w = triangle_rule(2 * p)
+    rng = np.random.default_rng(30 + p)
+    u = rng.uniform(-1, 1, m.n_dof)
+    v = rng.normal(size=m.n_dof)
+    outs = []
+    for cap in (0, 0, 24, 40):
+        ctx = Context(device=0)
+        ctx.set_element(p, xy, w)
+        ctx.mesh_upload(m.vert_xy, m.elem_vert, m.n_dof, m.elem_dof)
+        ctx.set_tuning(FEA_TUNE_TENSOR_KERNEL, 4)
+        ctx.set_tuning(FEA_TUNE_EMAX, cap)
+        ctx.build_pattern()
+        ctx.set_coefficient(FEA_MASS, K_EXP, (1.3, 0.5))
+        ctx.set_coefficient(FEA_STIFF, K_POLY, (1.0, 0.0, 1.0))
+        perm = ctx.get_dof_perm()
+        mt = torch.empty(ctx.nnz, dtype=torch.float64, device="cuda:0")
+        ct = torch.empty(ctx.nnz, dtype=torch.float64, device="cuda:0")
+        ctx.assemble_tensor(torch.tensor(u[perm], device="cuda:0"), torch.tensor(v[perm], device="cuda:0"), mt, ct)
+        ctx.sync()
+        outs.append((ctx.stat(16), mt.cpu().numpy(), ct.cpu().numpy()))
+        ctx.close()
+    assert outs[2][0] > outs[0][0]  # a finer tiling
+    for nb, mt, ct in outs[1:]:
+        assert np.array_equal(outs[0][1], mt) and np.array_equal(outs[0][2], ct)
