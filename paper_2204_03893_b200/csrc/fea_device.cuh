@@ -160,7 +160,7 @@ __device__ __forceinline__ int u16_of(const W& w, int k) { return (word_of(w, k 
 
 // ORIENT (tensor contractions): bit 15 of an offset selects sVd (entry (i, k) with local i > k)
 // over sVc for the nonsymmetric channel; the symmetric channel ignores it.
-// `first` is this thread's first item of the class (the classes continue one round-robin over
+// `first` is this thread's first item of the class (the classes continue one warp-aligned round-robin over
 // the threads, so no warp takes every class's tail)
 // IL: V_m and V_c interleaved ({m, c} double2 at sVm[2 off]): one 16-byte load per contributor
 template <int C, bool DO_M, bool DO_C, int ILP, bool ORIENT = false, bool IL = false>
@@ -236,7 +236,7 @@ __device__ __forceinline__ void phase_b5(const uint8_t* __restrict__ rec, int nc
                                          const double* __restrict__ sVc, double* om, double* oc, int tid, int nthr,
                                          const double* __restrict__ sVd = nullptr) {
     const int4* cls = reinterpret_cast<const int4*>(rec);
-    int start = 0;  // items of the previous classes (mod nthr): one round-robin over all classes
+    int start = 0;  // items of the previous classes, rounded up to warps (mod nthr): one round-robin
     for (int k = 0; k < ncls; ++k) {
         const int4 c = cls[k];  // {C, n_items, byte offset, item bytes}
         const uint8_t* base = rec + c.z;
@@ -249,7 +249,7 @@ __device__ __forceinline__ void phase_b5(const uint8_t* __restrict__ rec, int nc
             case 6: items5<6, DO_M, DO_C, 2, ORIENT, IL>(base, c.y, sVm, sVc, om, oc, first, nthr, sVd); break;
             default: items5_generic<DO_M, DO_C, ORIENT, IL>(base, c.x, c.y, c.w, sVm, sVc, om, oc, first, nthr, sVd);
         }
-        start = (start + c.y) % nthr;
+        start = (start + ((c.y + 31) & ~31)) % nthr;  // next class warp-aligned (the planner's 32-item groups)
     }
 }
 

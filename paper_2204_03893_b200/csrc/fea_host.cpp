@@ -708,31 +708,44 @@ fea_status fea_set_tuning(fea_ctx c, int key, int64_t value) {
 // in its aligned group of 32 and assigns each group's items to the two half-warps (16 + 16)
 // greedily, minimising repeated 8-byte banks (offset mod 16, orientation bit masked) per
 // contributor index within a half.  Phase B's sums do not depend on the item order.
-static std::vector<int32_t> half_split_order(const uint16_t* off, int n, int C) {
+// Item order within each aligned group of 32 items (one warp instruction of phase B: the classes
+// start warp-aligned, fea_device.cuh phase_b5): the group is split into the lane subsets that the
+// shared-memory V reads are served in -- half-warps for 8-byte reads (bank key: offset mod 16),
+// quarter-warps for the 16-byte {m, c} reads of interleaved V (key: offset mod 8) -- greedily
+// so each subset's keys are distinct where possible.  The group still covers the same 32 slots.
+static std::vector<int32_t> bank_split_order(const uint16_t* off, int n, int C, bool quarter) {
+    const int NSUB = quarter ? 4 : 2, SUB = 32 / NSUB, KEYS = quarter ? 8 : 16;
     std::vector<int32_t> ord(n);
     for (int g = 0; g < n; g += 32) {
         const int gn = std::min(32, n - g);
-        if (gn <= 16) {
+        if (gn <= SUB) {
             for (int l = 0; l < gn; ++l) ord[g + l] = g + l;
             continue;
         }
-        std::vector<int32_t> half[2];
-        int cnt[2][16][8] = {};  // [half][bank][q] (C <= 8 tracked; more is rare)
+        std::vector<int32_t> sub[4];
+        int cnt[4][16][8] = {};  // [subset][key][q] (C <= 8 tracked; more is rare)
         const int Cq = std::min(C, 8);
+        // capacity of each subset: lanes of the group that exist (the last group may be partial)
+        int cap[4];
+        for (int h = 0; h < NSUB; ++h) cap[h] = std::max(0, std::min(SUB, gn - h * SUB));
         for (int l = 0; l < gn; ++l) {
             const int i = g + l;
-            int cost[2] = {0, 0};
-            for (int h = 0; h < 2; ++h)
-                for (int q = 0; q < Cq; ++q) cost[h] += cnt[h][(off[(size_t)i * C + q] & 0x7fff) & 15][q];
-            int h = cost[0] <= cost[1] ? 0 : 1;
-            if ((int)half[h].size() >= 16) h ^= 1;
-            if (h == 1 && (int)half[1].size() >= gn - 16) h = 0;  // the first half is always full
-            half[h].push_back(i);
-            for (int q = 0; q < Cq; ++q) cnt[h][(off[(size_t)i * C + q] & 0x7fff) & 15][q]++;
+            int best = -1, bcost = 1 << 30;
+            for (int h = 0; h < NSUB; ++h) {
+                if ((int)sub[h].size() >= cap[h]) continue;
+                int cost = 0;
+                for (int q = 0; q < Cq; ++q) cost += cnt[h][(off[(size_t)i * C + q] & 0x7fff) % KEYS][q];
+                if (cost < bcost) {
+                    bcost = cost;
+                    best = h;
+                }
+            }
+            sub[best].push_back(i);
+            for (int q = 0; q < Cq; ++q) cnt[best][(off[(size_t)i * C + q] & 0x7fff) % KEYS][q]++;
         }
         int l = 0;
-        for (int h = 0; h < 2; ++h)
-            for (int32_t i : half[h]) ord[g + l++] = i;
+        for (int h = 0; h < NSUB; ++h)
+            for (int32_t i : sub[h]) ord[g + l++] = i;
     }
     return ord;
 }
@@ -752,7 +765,7 @@ struct PlanData {
 };
 
 static fea_status build_blocks(fea_ctx c, bool v5, bool orient, int64_t e_max, int64_t rec_budget, int64_t EM,
-                               PlanData& P) {
+                               PlanData& P, bool il = false) {
     const int np = c->np, T = c->T;
     const int64_t n_e = c->n_e;
     const int64_t R0 = c->row_begin, nr = c->n_rows;
@@ -927,11 +940,9 @@ static fea_status build_blocks(fea_ctx c, bool v5, bool orient, int64_t e_max, i
             tab[4 * k2 + 1] = n;
             tab[4 * k2 + 2] = coff[k2];
             tab[4 * k2 + 3] = R;
-            // items in slot order within the class, except that each aligned group of 32 items (one
-            // warp instruction of phase B) is split into its two half-warps so that the 8-byte V
-            // reads of each half hit distinct banks where possible (64-bit shared accesses only
-            // conflict within a half-warp); the group still stores the same 32 slots
-            const std::vector<int32_t> ord = half_split_order(&contrib[cls[3 * k2 + 2]], n, C);
+            // items in slot order within the class, each aligned group of 32 items (one warp
+            // instruction of phase B) ordered by bank_split_order
+            const std::vector<int32_t> ord = bank_split_order(&contrib[cls[3 * k2 + 2]], n, C, il);
             for (int it = 0; it < n; ++it) {
                 const int src = ord[it];
                 uint16_t* w = reinterpret_cast<uint16_t*>(o.rec.data() + base + coff[k2] + (size_t)it * R);
@@ -1068,7 +1079,8 @@ fea_status fea_build_pattern(fea_ctx c, int64_t* row_begin, int64_t* n_rows_loca
     const int64_t EM = v5 ? (e_max | 1) : fea4_vstride((int32_t)e_max);  // V row strides (fea_internal.h)
     PlanData P;
     {
-        const fea_status st = build_blocks(c, v5, false, e_max, rec_budget, EM, P);
+        // v5 with both matrices: V_m, V_c interleaved, phase B reads 16-byte {m, c} pairs
+        const fea_status st = build_blocks(c, v5, false, e_max, rec_budget, EM, P, v5 && nmat == 2);
         if (st != FEA_OK) return st;
     }
     const int64_t nb = (int64_t)P.blocks.size();
