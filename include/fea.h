@@ -77,6 +77,9 @@ enum {
     FEA_TUNE_PLAN_WHICH = 4,    /* FEA_MASS | FEA_STIFF: matrices the plan's shared memory is sized
                                    for (default both); assembling more than planned runs one pass
                                    per matrix                                                        */
+    FEA_TUNE_PAD1 = 10,         /* kernel v5 phase B: 1 = slots with one contributor join the two-
+                                   contributor class with a read of a zero cell where the block's
+                                   record still fits (denser stores; bit-identical; default), 0 = off */
     FEA_TUNE_TENSOR_KERNEL = 8  /* fea_assemble_tensor kernel: 0 = automatic (DMMA k_tensor4 for p >= 2
                                    or a non-native rule, k_tensor otherwise), 1 = k_tensor (one
                                    thread per element), 4 = k_tensor4 (FP64 tensor cores)            */

@@ -19,6 +19,7 @@
 #include <numeric>
 #include <string>
 #include <thread>
+#include <map>
 #include <vector>
 
 #include "../../include/fea.h"
@@ -129,6 +130,7 @@ struct fea_ctx_s {
     // tuning
     int64_t tune_smem = 0;
     int tune_kver = 0;     // 0 = automatic, 4 = force kernel v4
+    int tune_pad1 = 1;     // v5: single-contributor slots padded into the two-contributor class
     int tune_tker = 0;     // tensor kernel: 0 = automatic, 1 = k_tensor, 4 = k_tensor4 (FEA_TUNE_TENSOR_KERNEL)
     int tune_overlap = 1;  // world > 1: interior blocks assemble while u is exchanged (FEA_TUNE_OVERLAP)
     int n_int = 0;         // interior blocks (first n_int of the plan when world > 1)
@@ -689,6 +691,10 @@ fea_status fea_set_tuning(fea_ctx c, int key, int64_t value) {
             if (value != 0 && value != 1) return c->fail(FEA_E_ARG, "exchange must be 0 or 1");
             c->exchange = (int)value;
             break;
+        case 10:  // v5 phase B: pad single-contributor slots into the two-contributor class (1) or not (0)
+            if (value != 0 && value != 1) return c->fail(FEA_E_ARG, "pad flag must be 0 or 1");
+            c->tune_pad1 = (int)value;
+            break;
         case 8:  // tensor kernel: 0 = automatic, 1 = lane per element (k_tensor), 4 = DMMA (k_tensor4)
             if (value != 0 && value != 1 && value != 4) return c->fail(FEA_E_ARG, "tensor kernel must be 0, 1 or 4");
             c->tune_tker = (int)value;
@@ -885,14 +891,27 @@ static fea_status build_blocks(fea_ctx c, bool v5, bool orient, int64_t e_max, i
         // items: slots sorted by (count, slot); classes of equal count
         std::vector<int32_t> order(nslot);
         std::iota(order.begin(), order.end(), 0);
-        std::stable_sort(order.begin(), order.end(), [&](int32_t x, int32_t y) { return scount[x] < scount[y]; });
+        // v5: single-contributor slots join the two-contributor class with a second read of a
+        // zero cell (V row 0, column e_max: never written by the kernel, zeroed at its start), so
+        // each warp's stores of that class cover denser slot ranges (C2: ~16 -> ~9 sectors per
+        // store instruction); the sum is unchanged (x + 0.0).
+        bool pad1 = v5 && !orient && c->tune_pad1 && EM > e_max;
+        if (pad1) {  // only where the padded record still fits the block's record budget
+            std::map<int32_t, int32_t> n_by;
+            for (int32_t sl = 0; sl < nslot; ++sl) n_by[scount[sl] == 1 ? 2 : scount[sl]]++;
+            int64_t sz = 16 * (int64_t)n_by.size();
+            for (const auto& kv : n_by) sz += fea_pad16(kv.second * fea5_item_bytes(kv.first));
+            pad1 = sz <= rec_budget;
+        }
+        auto ecount = [&](int32_t sl) { return pad1 && scount[sl] == 1 ? 2 : scount[sl]; };
+        std::stable_sort(order.begin(), order.end(), [&](int32_t x, int32_t y) { return ecount(x) < ecount(y); });
         std::vector<int32_t> cls;
         std::vector<uint16_t> items(nslot), contrib;
         contrib.reserve(recs.size());
         for (int32_t it = 0; it < nslot; ++it) {
             const int32_t sl = order[it];
-            if (it == 0 || scount[sl] != scount[order[it - 1]]) {
-                cls.push_back(scount[sl]);
+            if (it == 0 || ecount(sl) != ecount(order[it - 1])) {
+                cls.push_back(ecount(sl));
                 cls.push_back(it);
                 cls.push_back((int32_t)contrib.size());
             }
@@ -903,6 +922,7 @@ static fea_status build_blocks(fea_ctx c, bool v5, bool orient, int64_t e_max, i
             items[it] = (uint16_t)sl;
             for (int32_t m = sstart[sl]; m < sstart[sl] + scount[sl]; ++m)
                 contrib.push_back((uint16_t)(((recs[m].t & 0xffff) * EM + recs[m].le) | ((recs[m].t >> 16) << 15)));
+            if (ecount(sl) != scount[sl]) contrib.push_back((uint16_t)e_max);  // the zero cell
         }
         FeaBlock& F = o.fb;
         F.nslots = nslot;

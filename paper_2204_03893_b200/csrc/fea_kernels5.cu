@@ -122,6 +122,15 @@ __global__ void __launch_bounds__(fea5_threads(P), 1) k_reassemble5(const __grid
         fence_mbar_init();
     }
     if (tid < 6 && tid < nb) sBlk[tid] = prm.blocks[b0 + tid * G];
+    // the zero cell of phase B's padded items (V row 0, column e_max; vs = e_max | 1 > e_max)
+    if (tid < 2) {
+        if (DO_M && DO_C) {
+            reinterpret_cast<double2*>(sVm0 + tid * 2 * vbuf)[prm.e_max] = make_double2(0.0, 0.0);
+        } else {
+            if (DO_M) sVm0[tid * vbuf + prm.e_max] = 0.0;
+            if (DO_C) sVc0[tid * vbuf + prm.e_max] = 0.0;
+        }
+    }
     __syncthreads();
     if (tid == 0)
         for (int k = 0; k < PF && k < nb; ++k) prefetch_blk(k);

@@ -91,7 +91,8 @@ def test_deterministic_across_runs_and_tilings(p):
     again = library_assemble(m, xy, w, u, p, coef, coef)
     assert np.array_equal(base["M"], again["M"]) and np.array_equal(base["K"], again["K"])
     # smem budgets (v4 and v5) and element caps per block (v5, FEA_TUNE_EMAX = 3)
-    tunings = {1: [{1: 24000}, {3: 64}, {3: 120}], 2: [{1: 40000}, {3: 48}, {3: 120}],
+    # ... and v5 without the zero-padded single-contributor items (FEA_TUNE_PAD1 = 10)
+    tunings = {1: [{1: 24000}, {3: 64}, {3: 120}, {10: 0}], 2: [{1: 40000}, {3: 48}, {3: 120}, {10: 0}],
                3: [{1: 100000}, {1: 150000}], 4: [{1: 150000}, {1: 190000}]}[p]
     for tu in tunings:
         r = library_assemble(m, xy, w, u, p, coef, coef, tuning=tu)
