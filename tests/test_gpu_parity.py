@@ -96,7 +96,8 @@ def test_deterministic_across_runs_and_tilings(p):
                3: [{1: 100000}, {1: 150000}], 4: [{1: 150000}, {1: 190000}]}[p]
     for tu in tunings:
         r = library_assemble(m, xy, w, u, p, coef, coef, tuning=tu)
-        assert r["ctx"].stat(1) > max(1, base["ctx"].stat(1) // 2)  # a different, finer tiling
+        if 1 in tu or 3 in tu:
+            assert r["ctx"].stat(1) > max(1, base["ctx"].stat(1) // 2)  # a different, finer tiling
         assert np.array_equal(base["M"], r["M"]) and np.array_equal(base["K"], r["K"])
 
 
