@@ -138,3 +138,31 @@ def test_pattern_rows_window_matches_full_pattern():
         assert np.array_equal(wrp, rp[r0:r1 + 1])
         assert np.array_equal(wci, ci[rp[r0]:rp[r1]])
     ctx.close()
+
+
+def test_tuning_keys_validated_and_plan_invariant():
+    """fea_set_tuning rejects unknown keys and out-of-range values (FEA_E_ARG) and leaves the
+    context usable; tuning keys that only change the kernel-side plan (v5 padding, tensor kernel)
+    keep the CSR pattern bit-identical."""
+    m = random_mesh_from_structured(6, 2, seed=520)
+    base = _plan(m, 2)
+    rp0, ci0 = base.get_pattern()
+    for key, bad in ((2, 3), (3, -1), (4, 0), (5, 2), (7, 2), (8, 2), (10, 2), (99, 0)):
+        ctx = fea.Context(device=-1)
+        xy, w = triangle_rule(4)
+        ctx.set_element(2, xy, w)
+        ctx.mesh_upload(m.vert_xy, m.elem_vert, m.n_dof, m.elem_dof)
+        with pytest.raises(fea.FeaError):
+            ctx.set_tuning(key, bad)
+        ctx.build_pattern()  # still usable after the rejected value
+        rp, ci = ctx.get_pattern()
+        assert np.array_equal(rp, rp0) and np.array_equal(ci, ci0)
+    for key, val in ((10, 0), (8, 1), (8, 4), (2, 4)):
+        ctx = fea.Context(device=-1)
+        xy, w = triangle_rule(4)
+        ctx.set_element(2, xy, w)
+        ctx.mesh_upload(m.vert_xy, m.elem_vert, m.n_dof, m.elem_dof)
+        ctx.set_tuning(key, val)
+        ctx.build_pattern()
+        rp, ci = ctx.get_pattern()
+        assert np.array_equal(rp, rp0) and np.array_equal(ci, ci0)
