@@ -67,7 +67,7 @@ enum {
                                    smaller row blocks (more, finer CTA tiles)                        */
     FEA_TUNE_KERNEL = 2,        /* kernel generation: 0 = automatic (v5 for p <= 2 with the native
                                    3/6-point rules, v4 otherwise), 4 = force v4                      */
-    FEA_TUNE_EMAX = 3,          /* v5 and k_tensor4: cap on elements per row block (0 = from the
+    FEA_TUNE_EMAX = 3,          /* cap on elements per row block (all kernels; 0 = from the
                                    shared-memory budget)                                             */
     FEA_TUNE_EXCHANGE = 5,      /* world > 1: 0 = interface-only exchange of u (default), 1 = full-
                                    vector allgather                                                 */

@@ -1080,6 +1080,7 @@ fea_status fea_build_pattern(fea_ctx c, int64_t* row_begin, int64_t* n_rows_loca
             e_max = (int64_t)((budget - 256 - 3 * 128 - 16LL * T * nmat - 32LL * (np + 2 * nqp) - rstages * r0) /
                               (per_el_smem + rstages * rec_el));
             e_max = std::min<int64_t>(e_max, 65535 / T);
+            if (c->tune_emax) e_max = std::min(e_max, c->tune_emax);
             e_max = e_max >= 8 ? ((e_max - 8) / 16) * 16 + 8 : 0;  // multiple of 8, == 8 mod 16
             rec_budget = ((int64_t)(rec_el * e_max) + r0 + 15) & ~int64_t(15);
             if (pass == 1 || e_max < 8) break;
