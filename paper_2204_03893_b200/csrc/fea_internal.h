@@ -28,6 +28,9 @@ __host__ __device__ constexpr int fea_S(int p) { return p == 1 ? 8 : p == 2 ? 3 
 __host__ __device__ constexpr int fea_ctas(int p) { return p <= 2 ? 2 : 1; }
 __host__ __device__ constexpr int fea_rstages(int p) { return p <= 2 ? 3 : 2; }
 // row tiles per consumer warp (B-fragment loads shared by RT tiles); warp groups = ceil(NTT / RT)
+#ifndef FEA5_PF
+#define FEA5_PF 3  // kernel v5: L2 prefetch distance (blocks); at most 5 (the descriptor ring)
+#endif
 #ifndef FEA4_RT4
 #define FEA4_RT4 1
 #endif

@@ -61,7 +61,7 @@ __global__ void __launch_bounds__(fea5_threads(P), 1) k_reassemble5(const __grid
     constexpr int NS = fea5_nsplit(P);           // units per 32-element tile
     constexpr int NJ = NS == 1 ? NP : NP / 2;    // columns per unit
     constexpr int oW = (NP * NQ + 1) & ~1;       // w_q in ctab
-    constexpr int PF = 3;                        // L2 prefetch distance (blocks)
+    constexpr int PF = FEA5_PF;                  // L2 prefetch distance (blocks)
     constexpr int DR = 8;                        // descriptor ring
     static_assert(2 * NP * NQ <= FEA_JTAB_MAX, "J tables exceed the parameter bank");
     static_assert(NS == 1 || NP == 6, "column halves are defined for P2");
