@@ -31,6 +31,9 @@ __host__ __device__ constexpr int fea_rstages(int p) { return p <= 2 ? 3 : 2; }
 #ifndef FEA5_PF
 #define FEA5_PF 3  // kernel v5: L2 prefetch distance (blocks); at most 5 (the descriptor ring)
 #endif
+#ifndef FEA4_A1FIRST
+#define FEA4_A1FIRST 1  // kernel v4: warps running A1(j+1) before B(j): 0 none, 1 odd warps, 2 all
+#endif
 #ifndef FEA4_RT4
 #define FEA4_RT4 1
 #endif

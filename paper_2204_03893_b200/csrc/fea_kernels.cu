@@ -303,7 +303,7 @@ __global__ void __launch_bounds__(fea_threads(P), fea_ctas(P)) k_reassemble(cons
 
         // ---------------- Phase B of block j (fixed-order segmented reduction into the CSR slots)
         // and A1 of block j + 1, in alternating order across warps so the two overlap.
-        const bool a1_first = (warp & 1) && j + 1 < ncta_blocks;
+        const bool a1_first = (FEA4_A1FIRST == 2 || (FEA4_A1FIRST == 1 && (warp & 1))) && j + 1 < ncta_blocks;
         if (a1_first) phase_a1(j + 1);
         phase_b5<DO_M, DO_C>(rec + 32, blk.ncls, sVm, sVc, DO_M ? prm.out_m + blk.slot0 : nullptr,
                              DO_C ? prm.out_c + blk.slot0 : nullptr, tid, NCT);
