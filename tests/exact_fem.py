@@ -104,7 +104,43 @@ def k_exact(kind: int, par, u):
         return r
     if kind == 1:
         return mpmath.mpf(par[0]) * mpmath.exp(mpmath.mpf(par[1]) * mpmath.mpf(u.numerator) / u.denominator)
+    if kind == 2:
+        return pwl_exact(par, u)
     raise ValueError(kind)
+
+
+def _pwl_pairs(par):
+    pts = [(Fraction(par[2 * i]), Fraction(par[2 * i + 1])) for i in range(len(par) // 2)]
+    assert all(pts[i][0] < pts[i + 1][0] for i in range(len(pts) - 1))
+    return pts
+
+
+def _pwl_segment(pts, T):
+    """Segment index s of T: the first case is T_1 <= T <= T_2 (T_2 belongs to
+    it), the following ones T_s < T <= T_{s+1}.  Outside [T_1, T_m] (where the paper is silent)
+    reading R26: the end segments continue (linear extrapolation)."""
+    for s in range(len(pts) - 1):
+        if T <= pts[s + 1][0]:
+            return s
+    return len(pts) - 2
+
+
+def pwl_exact(par, T):
+    """k(T) = k_s + (k_{s+1} - k_s) / (T_{s+1} - T_s) (T - T_s) in exact rationals."""
+    pts = _pwl_pairs(par)
+    T = Fraction(T)
+    s = _pwl_segment(pts, T)
+    (T0, k0), (T1, k1) = pts[s], pts[s + 1]
+    return k0 + (k1 - k0) / (T1 - T0) * (T - T0)
+
+
+def pwl_slope_exact(par, T):
+    """k'(T) of the piecewise-linear k: the slope of the segment that owns T (breakpoints belong to
+    the segment on their left, as in the paper's closed first case), exact."""
+    pts = _pwl_pairs(par)
+    s = _pwl_segment(pts, Fraction(T))
+    (T0, k0), (T1, k1) = pts[s], pts[s + 1]
+    return (k1 - k0) / (T1 - T0)
 
 
 def brute_force_assemble(mesh, q_xy, q_w, u, m_coef, c_coef):
