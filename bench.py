@@ -31,7 +31,9 @@ from fea_inputs import CONFIGS, MASS, STIFF, make_workload  # noqa: E402
 
 METRIC = "element-matrix entries assembled/s (FP64, into CSR) and % of HBM roofline"
 UNIT = "entries/s"
-DEFAULT_CONFIG = "C2"  # BASELINE.json configs[1]
+# The largest single-GPU config: C5, P4 M+K, 33.9 GB of algorithmic traffic per
+# reassembly (HBM-resident; C2's 73.5 MB fits in L2).  The other configs are parity cases.
+DEFAULT_CONFIG = "C5"
 
 
 def canonical_bytes(n_v, n_e, n_p, n_dof, nnz, nmat):
@@ -130,7 +132,9 @@ def workload_desc(cfg, wl):
 
 def cpu_oracle_run(wl, cfg, target_s: float, nthreads: int, lib_to_user=None, tensor: bool = False):
     """Time the oracle (Algorithm 1, as it stands) on a bounded sample: whole reassemblies of the
-    workload if one takes < target_s, else a leading block of rows.  Returns (entries/s, desc)."""
+    workload if one takes < target_s, else a leading block of rows.  Returns (entries/s, desc,
+    seconds per sample, pattern-build seconds of the sample) -- formation (values) and the
+    structural pattern are timed separately, mirroring the paper's split."""
     import oracle
     m = wl.mesh
     if lib_to_user is not None:  # same numbering as the GPU run
@@ -159,7 +163,9 @@ def cpu_oracle_run(wl, cfg, target_s: float, nthreads: int, lib_to_user=None, te
     # sample rows [0, r1): grow until the estimated time reaches target_s
     r1 = min(m.n_dof, max(1000, m.n_dof // 64))
     while True:
+        tp = time.perf_counter()
         pat = oracle.pattern(m.n_dof, m.elem_dof, 0, r1)
+        t_pat = time.perf_counter() - tp
         t0 = time.perf_counter()
         run(r1, pat)
         dt = time.perf_counter() - t0
@@ -176,8 +182,8 @@ def cpu_oracle_run(wl, cfg, target_s: float, nthreads: int, lib_to_user=None, te
     rows_in = (ed < r1).sum(axis=1)  # per element: local rows in the sample
     entries = int(rows_in.sum()) * n_p * nmat
     desc = (f"oracle rows [0,{r1}) of {m.n_dof} ({100.0 * r1 / m.n_dof:.1f}%), {reps} rep(s), "
-            f"pattern build excluded, {nthreads} thread(s)")
-    return entries / dt, desc, dt
+            f"pattern build timed separately, {nthreads} thread(s)")
+    return entries / dt, desc, dt, t_pat
 
 
 def run_reference(args):
@@ -192,12 +198,12 @@ def run_reference(args):
     times = []
     desc = ""
     for i in range(args.warmup + args.steps):
-        rate, desc, dt = cpu_oracle_run(wl, cfg, step_target, cores)
+        rate, desc, dt, _ = cpu_oracle_run(wl, cfg, step_target, cores)
         if i >= args.warmup:
             times.append(rate)
     value = statistics.median(times)
     ent_step = wl.mesh.n_e * cfg.n_p ** 2 * cfg.n_matrices
-    line = {"metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
+    line = {"metric": METRIC, "value": value, "unit": UNIT, "n_gpus": max(world, args.gpus), "steps": args.steps,
             "warmup": args.warmup, "ms_per_step": 1e3 * ent_step / value, "higher_is_better": True,
             "scaling": "strong", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
             "impl": "reference", "config": workload_desc(cfg, wl),
@@ -217,11 +223,16 @@ def run_ours(args):
         dist.init_process_group("nccl", device_id=dev)
     from paper_2204_03893_b200 import Assembler
     cfg = CONFIGS[args.config]
+    if args.scale:  # diagnostics only: the config's recipe on an N x N grid (not a bench value)
+        from fea_inputs import scaled
+        cfg = scaled(cfg, args.scale)
     t_setup = time.perf_counter()
     wl = make_workload(cfg)
     m = wl.mesh
     coef, mcoef = cfg.coef_c, cfg.coef_m
     tuning = {int(kv.split("=")[0]): int(kv.split("=")[1]) for kv in args.tune}
+    if world > 1:
+        tuning.setdefault(11, 1)  # FEA_TUNE_TIMING: exchange / assembly events per call (split below)
     asm = Assembler(cfg.p, wl.q_xy, wl.q_w, m.vert_xy, m.elem_vert, m.n_dof, m.elem_dof, device=local,
                     reorder=cfg.reorder, which=cfg.which, coef_m=mcoef, coef_c=coef, rank=rank, world=world,
                     tuning=tuning)
@@ -264,6 +275,7 @@ def run_ours(args):
     sampler = ClockSampler(local)
     barrier()
     torch.cuda.synchronize()
+    split = []  # world > 1: (exchange us, assembly us) of every timed step (library events)
     with sampler:
         for i in range(args.steps):
             if flush_mb:
@@ -273,6 +285,8 @@ def run_ours(args):
             ev[i][0].record(stream)
             step(i)
             ev[i][1].record(stream)
+            if world > 1 and not tensor:
+                split.append((asm.ctx.stat(36), asm.ctx.stat(37)))
         torch.cuda.synchronize()
     barrier()
     step_ms = [a.elapsed_time(b) for a, b in ev]
@@ -294,12 +308,22 @@ def run_ours(args):
         frac_rows = asm.n_rows / m.n_dof
         B = canonical_bytes(m.n_v, m.n_e, cfg.n_p, m.n_dof, 0, nmat) * frac_rows + 8 * nnz_local * nmat
     kern_ms = statistics.median(step_ms)
+    xsplit = None
+    if split:  # median per rank, then the max over ranks (allgather and kernels reported apart)
+        med = torch.tensor([statistics.median(x for x, _ in split), statistics.median(k for _, k in split)],
+                           dtype=torch.float64, device=dev)
+        torch.distributed.all_reduce(med, op=torch.distributed.ReduceOp.MAX)
+        xsplit = {"exchange_ms_max_over_ranks": float(med[0]) / 1e3,
+                  "assembly_ms_max_over_ranks": float(med[1]) / 1e3,
+                  "note": "per-rank medians over the timed steps (CUDA events on the library's streams); the "
+                          "assembly span includes any wait of the boundary blocks for the halo"}
+        kern_ms = float(med[1]) / 1e3
     achieved = B / (kern_ms * 1e-3) / 1e9
     traffic = None
     if tensor:
         kname = "k_tensor4" if asm.ctx.stat(12) == 4 else "k_tensor"
     else:
-        kname = "k_reassemble5" if asm.ctx.stat(11) == 5 else "k_reassemble"
+        kname = {5: "k_reassemble5", 6: "k_reassemble6"}.get(asm.ctx.stat(11), "k_reassemble")
     prof = os.path.join(ROOT, "profiles", f"ncu_traffic_{cfg.name}_{kname}.json")
     if os.path.exists(prof):  # an ncu --set full capture of this kernel on this config
         with open(prof) as f:
@@ -346,11 +370,18 @@ def run_ours(args):
         cpu = None
         if world == 1 and not args.no_cpu_baseline:
             cores = len(os.sched_getaffinity(0))
-            rate, desc, _ = cpu_oracle_run(wl, cfg, float(os.environ.get("FEA_CPU_BASELINE_S", "10")), cores,
-                                           lib_to_user=asm.lib_to_user, tensor=tensor)
+            tgt = float(os.environ.get("FEA_CPU_BASELINE_S", "10"))
+            rate, desc, dt, t_pat = cpu_oracle_run(wl, cfg, tgt, cores, lib_to_user=asm.lib_to_user, tensor=tensor)
             cores = 1 if tensor else cores
-            cpu = {"value": rate, "unit": UNIT, "cores": cores, "kind": "oracle", "sample": desc}
+            cpu = {"value": rate, "unit": UNIT, "cores": cores, "kind": "oracle", "sample": desc,
+                   "pattern_build_s_of_sample": round(t_pat, 4), "values_s_of_sample": round(dt, 4)}
+            if not tensor and cores > 1:  # the same oracle on one core (SURVEY 8(d) "Oracle timing")
+                rate1, desc1, dt1, t_pat1 = cpu_oracle_run(wl, cfg, tgt, 1, lib_to_user=asm.lib_to_user)
+                cpu["one_core"] = {"value": rate1, "unit": UNIT, "cores": 1, "sample": desc1,
+                                   "pattern_build_s_of_sample": round(t_pat1, 4), "values_s_of_sample": round(dt1, 4)}
         desc = workload_desc(cfg, wl)
+        if args.scale:
+            desc["workload"] = f"DIAGNOSTIC {cfg.name} scaled to N={cfg.N} (not a bench value)"
         if tensor:
             desc["op"] = "tensor contractions (M o2 v, C o2 v), NEXT-1/2: u = u_r, v = u_{r+1} - u_r"
         if world > 1:
@@ -389,6 +420,7 @@ def run_ours(args):
             "e2e": {"value": entries_step / e2e_s, "unit": UNIT, "h2d_bytes_per_step": 8 * nu * (2 if tensor else 1),
                     "d2h_bytes_per_step": 8 * nnz_local * nmat, "ms_per_step": e2e_s * 1e3},
             "gpu_launches": args.steps * asm.ctx.stat(5),
+            "exchange_split": xsplit,
             "clocks": sampler.summary(),
         }
         print(json.dumps(line), flush=True)
@@ -408,10 +440,23 @@ def main():
     ap.add_argument("--op", default="reassemble", choices=["reassemble", "tensor"],
                     help="reassemble: the per-iteration M, K reassembly (default); tensor: NEXT-1/2")
     ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--scale", type=int, default=0, help="diagnostics: run the config's recipe on an N x N grid")
     ap.add_argument("--tune", action="append", default=[], help="libfea tuning key=value (fea.h FEA_TUNE_*)")
     args = ap.parse_args()
     if args.warmup < 3:
         args.warmup = 3  # timing rule: at least 3 warm-up steps
+    if "WORLD_SIZE" in os.environ:
+        if int(os.environ["WORLD_SIZE"]) != args.gpus and args.impl == "ours":
+            raise SystemExit(f"--gpus {args.gpus} but WORLD_SIZE={os.environ['WORLD_SIZE']}")
+    elif args.gpus > 1:
+        # one process per GPU: re-launch under torchrun (rendezvous on 127.0.0.1)
+        import socket
+        with socket.socket() as sk:
+            sk.bind(("127.0.0.1", 0))
+            port = sk.getsockname()[1]
+        cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", f"--nproc-per-node={args.gpus}",
+               "--master-addr", "127.0.0.1", f"--master-port={port}", os.path.abspath(__file__), *sys.argv[1:]]
+        os.execv(sys.executable, cmd)
     if args.impl == "reference":
         return run_reference(args)
     return run_ours(args)

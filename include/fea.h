@@ -80,9 +80,12 @@ enum {
     FEA_TUNE_PAD1 = 10,         /* kernel v5 phase B: 1 = slots with one contributor join the two-
                                    contributor class with a read of a zero cell where the block's
                                    record still fits (denser stores; bit-identical; default), 0 = off */
-    FEA_TUNE_TENSOR_KERNEL = 8  /* fea_assemble_tensor kernel: 0 = automatic (DMMA k_tensor4 for p >= 2
+    FEA_TUNE_TENSOR_KERNEL = 8, /* fea_assemble_tensor kernel: 0 = automatic (DMMA k_tensor4 for p >= 2
                                    or a non-native rule, k_tensor otherwise), 1 = k_tensor (one
                                    thread per element), 4 = k_tensor4 (FP64 tensor cores)            */
+    FEA_TUNE_TIMING = 11        /* 1 = fea_reassemble / fea_assemble record CUDA events around the
+                                   exchange of u and around the assembly launches (read with
+                                   fea_get_stat keys 36 / 37); 0 = off (default).  Keeps the plan.   */
 };
 
 /* Create a context on CUDA device `cuda_device`.  `stream` is a cudaStream_t (NULL = the
@@ -207,6 +210,18 @@ fea_status fea_exchange_unpack(fea_ctx ctx, const double* u_owned, const double*
 fea_status fea_nccl_unique_id(void* id_out_128_bytes);
 fea_status fea_set_nccl(fea_ctx ctx, const void* id_128_bytes);
 
+/* Host transport of the per-iteration allgather (world > 1), for callers whose ranks talk over
+ * MPI, gloo, sockets, ... instead of NCCL: fea_reassemble then copies this rank's `count` float64
+ * (the packed interface values, or rows_per_rank values with FEA_TUNE_EXCHANGE 1) to a pinned host
+ * buffer, waits for them, and calls fn(send, recv, count, user) on the calling thread; fn must
+ * fill recv (host, world * count float64) with every rank's send buffer in rank order and return
+ * 0 (nonzero -> FEA_E_NCCL).  The values go back to the device on the exchange stream.  With the
+ * overlap (FEA_TUNE_OVERLAP 1) the interior blocks are enqueued before the exchange, so they
+ * assemble while fn runs.  The library owns the host buffers (valid during the call only).
+ * fn = NULL restores NCCL (fea_set_nccl). */
+typedef int (*fea_host_allgather_fn)(const double* send, double* recv, int64_t count, void* user);
+fea_status fea_set_host_transport(fea_ctx ctx, fea_host_allgather_fn fn, void* user);
+
 /* Wait for all work on the ctx stream; returns deferred CUDA / NCCL errors. */
 fea_status fea_sync(fea_ctx ctx);
 
@@ -216,7 +231,9 @@ fea_status fea_sync(fea_ctx ctx);
  * block (max), 8 = grid, 10 = largest block record (bytes), 11 = matrix kernel (4 or 5),
  * 14 = max interface size, 15 = interior blocks (world > 1).  Tensor plan (after the first
  * fea_assemble_tensor, else -1): 12 = tensor kernel (1 or 4), 13 = its grid, 16 = blocks,
- * 17 = element visits, 18 = owned elements, 19 = smem bytes per CTA. */
+ * 17 = element visits, 18 = owned elements, 19 = smem bytes per CTA.  With FEA_TUNE_TIMING (waits
+ * for the last call's events): 36 = exchange of u in microseconds (world > 1; -1 if none ran),
+ * 37 = assembly launches, first start to last end, in microseconds. */
 fea_status fea_get_stat(fea_ctx ctx, int key, int64_t* value);
 
 const char* fea_last_error(fea_ctx ctx);

@@ -16,7 +16,7 @@ LIB = os.path.join(HERE, "libfea.so")
 OBJ = os.path.join(HERE, "build")
 NVCC = os.environ.get("NVCC", "/usr/local/cuda/bin/nvcc")
 ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
-SOURCES = ["fea_kernels.cu", "fea_kernels5.cu", "fea_kernels_t.cu", "fea_kernels_x.cu", "fea_host.cpp"]
+SOURCES = ["fea_kernels.cu", "fea_kernels5.cu", "fea_kernels6.cu", "fea_kernels_t.cu", "fea_kernels_x.cu", "fea_host.cpp"]
 DEPS = SOURCES + ["fea_internal.h", "fea_device.cuh"]
 
 
@@ -35,8 +35,16 @@ def build(force: bool = False, verbose: bool = False) -> str:
     inc = ["-I", os.path.join(ROOT, "include"), "-I", CSRC]
     inc += os.environ.get("FEA_BUILD_DEFS", "").split()  # experiment switches, e.g. "-DFEA5_MMA=0"
 
+    hdrs = [os.path.join(CSRC, h) for h in ("fea_internal.h", "fea_device.cuh")] + [os.path.join(ROOT, "include", "fea.h")]
+    defs_key = os.environ.get("FEA_BUILD_DEFS", "") + ("|diag" if os.environ.get("FEA_BUILD_DIAG") else "")
+    stamp = os.path.join(OBJ, "defs.txt")
+    same_defs = os.path.exists(stamp) and open(stamp).read() == defs_key
+
     def compile_one(src):
         obj = os.path.join(OBJ, src + ".o")
+        deps = [os.path.join(CSRC, src), __file__] + hdrs
+        if not force and same_defs and os.path.exists(obj) and os.path.getmtime(obj) > max(map(os.path.getmtime, deps)):
+            return obj  # up to date (per-object: only changed sources recompile)
         if src.endswith(".cu"):
             diag = ["-DFEA5_DIAG"] if os.environ.get("FEA_BUILD_DIAG") else []
             cmd = [NVCC, "-O3", "-std=c++17", *ARCH, "-lineinfo", "-Xcompiler", "-fPIC", *diag, *inc, "-c",
@@ -53,6 +61,8 @@ def build(force: bool = False, verbose: bool = False) -> str:
 
     with ThreadPoolExecutor(len(SOURCES)) as ex:
         objs = list(ex.map(compile_one, SOURCES))
+    with open(stamp, "w") as f:
+        f.write(defs_key)
     tmp = LIB + f".tmp{os.getpid()}"
     cmd = [NVCC, "-shared", *ARCH, "-cudart", "static", "-o", tmp, *objs, "-ldl", "-lpthread"]
     r = subprocess.run(cmd, capture_output=True, text=True)

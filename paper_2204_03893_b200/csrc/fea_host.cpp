@@ -136,6 +136,11 @@ struct fea_ctx_s {
     int n_int = 0;         // interior blocks (first n_int of the plan when world > 1)
     cudaStream_t stream2 = nullptr;  // exchange stream of the overlap
     cudaEvent_t ev_own = nullptr, ev_halo = nullptr;
+    // FEA_TUNE_TIMING: events of the last call: [0, 1] around the exchange of u (world > 1),
+    // [2, 3] from the first assembly launch to the end of the last one
+    int tune_timing = 0;
+    bool t_exch = false, t_asm = false;
+    cudaEvent_t ev_t[4] = {nullptr, nullptr, nullptr, nullptr};
     int64_t tune_emax = 0; // v5 element cap per block (0 = from the budget)
 
     // reassemble buffers
@@ -153,7 +158,16 @@ struct fea_ctx_s {
     double* d_vm = nullptr;
     double* d_vc = nullptr;
     void* comm = nullptr;
+    // host transport of the allgather (fea_set_host_transport) instead of NCCL, pinned staging
+    fea_host_allgather_fn htrans = nullptr;
+    void* huser = nullptr;
+    double* h_send = nullptr;
+    double* h_recv = nullptr;
+    int64_t h_cap = 0;
+    int int_grid_cap = 0;  // world > 1 overlap: SMs left free for the exchange (FEA_TUNE_EXCH_SMS)
     unsigned long long* d_dbg = nullptr;  // FEA_DEBUG_TIMING phase counters
+    int dbg_mode = 0;                     // FEA_DEBUG_MODE / FEA_DEBUG_TIMING, read once at fea_create
+    bool dbg_timing = false;
 
     fea_status fail(fea_status s, const char* fmt, ...) {
         char buf[512];
@@ -197,6 +211,16 @@ struct fea_ctx_s {
         cudaError_t _e = (x);                                                                         \
         if (_e != cudaSuccess) return (ctx)->fail(FEA_E_CUDA, "%s: %s", #x, cudaGetErrorString(_e)); \
     } while (0)
+
+// FEA_TUNE_TIMING: record timing event i of the current call on `st` (no-op when off)
+static fea_status tmark(fea_ctx c, int i, cudaStream_t st) {
+    if (!c->tune_timing) return FEA_OK;
+    if (!c->ev_t[i]) FEA_CUDA(c, cudaEventCreate(&c->ev_t[i]));
+    FEA_CUDA(c, cudaEventRecord(c->ev_t[i], st));
+    if (i == 1) c->t_exch = true;
+    if (i == 3) c->t_asm = true;
+    return FEA_OK;
+}
 
 // ------------------------------------------------------------------ reference tables
 namespace {
@@ -405,6 +429,8 @@ fea_status fea_create(fea_ctx* out, int cuda_device, void* stream, int rank, int
     c->rank = rank;
     c->world = world;
     if (!host_only) cudaDeviceGetAttribute(&c->sm_count, cudaDevAttrMultiProcessorCount, cuda_device);
+    if (const char* dm = getenv("FEA_DEBUG_MODE")) c->dbg_mode = atoi(dm);  // diagnostics builds only
+    c->dbg_timing = getenv("FEA_DEBUG_TIMING") != nullptr;
     c->coef_m.kind = c->coef_c.kind = FEA_K_POLY;
     c->coef_m.npar = c->coef_c.npar = 1;
     c->coef_m.par[0] = c->coef_c.par[0] = 1.0;
@@ -419,12 +445,16 @@ void fea_destroy(fea_ctx c) {
     if (c->stream2) cudaStreamDestroy(c->stream2);
     if (c->ev_own) cudaEventDestroy(c->ev_own);
     if (c->ev_halo) cudaEventDestroy(c->ev_halo);
+    for (auto& e : c->ev_t)
+        if (e) cudaEventDestroy(e);
     dfree(c->d_tables);
     dfree(c->d_ttab);
     dfree(c->d_tables_c);
     dfree(c->d_ttab_c);
     dfree(c->d_dbg);
     if (c->comm && nccl().ok) nccl().commDestroy((ncclComm_t)c->comm);
+    if (c->h_send) cudaFreeHost(c->h_send);
+    if (c->h_recv) cudaFreeHost(c->h_recv);
     delete c;
 }
 
@@ -676,7 +706,7 @@ fea_status fea_set_tuning(fea_ctx c, int key, int64_t value) {
             c->tune_smem = value;
             break;
         case 2:  // kernel generation (0 = automatic, 4 = force v4)
-            if (value != 0 && value != 4 && value != 5) return c->fail(FEA_E_ARG, "kernel must be 0, 4 or 5");
+            if (value != 0 && value != 4 && value != 5 && value != 6) return c->fail(FEA_E_ARG, "kernel must be 0, 4, 5 or 6");
             c->tune_kver = (int)value;
             break;
         case 3:  // v5 elements per block cap
@@ -699,6 +729,10 @@ fea_status fea_set_tuning(fea_ctx c, int key, int64_t value) {
             if (value != 0 && value != 1 && value != 4) return c->fail(FEA_E_ARG, "tensor kernel must be 0, 1 or 4");
             c->tune_tker = (int)value;
             break;
+        case 11:  // per-call timing events (fea_get_stat keys 36, 37)
+            if (value != 0 && value != 1) return c->fail(FEA_E_ARG, "timing flag must be 0 or 1");
+            c->tune_timing = (int)value;
+            return FEA_OK;  // does not change the plan
         case 4:  // plan matrices bitmask (FEA_MASS | FEA_STIFF)
             if (value < 1 || value > 3) return c->fail(FEA_E_ARG, "plan matrices must be a nonzero MASS|STIFF mask");
             c->plan_which = (int)value;
@@ -770,8 +804,10 @@ struct PlanData {
     int64_t nnz = 0, rec_max = 16, visits = 0, owned = 0, ncon = 0, rbytes = 0;
 };
 
+// v6: kernel v6 record (fea_internal.h): class-A u32 items in slot order + class-B items; the
+// DOFs travel separately as for v5 (pass v5 = true); records stay in global memory.
 static fea_status build_blocks(fea_ctx c, bool v5, bool orient, int64_t e_max, int64_t rec_budget, int64_t EM,
-                               PlanData& P, bool il = false) {
+                               PlanData& P, bool il = false, bool v6 = false) {
     const int np = c->np, T = c->T;
     const int64_t n_e = c->n_e;
     const int64_t R0 = c->row_begin, nr = c->n_rows;
@@ -895,7 +931,7 @@ static fea_status build_blocks(fea_ctx c, bool v5, bool orient, int64_t e_max, i
         // zero cell (V row 0, column e_max: never written by the kernel, zeroed at its start), so
         // each warp's stores of that class cover denser slot ranges (C2: ~16 -> ~9 sectors per
         // store instruction); the sum is unchanged (x + 0.0).
-        bool pad1 = v5 && !orient && c->tune_pad1 && EM > e_max;
+        bool pad1 = v5 && !v6 && !orient && c->tune_pad1 && EM > e_max;
         if (pad1) {  // only where the padded record still fits the block's record budget
             std::map<int32_t, int32_t> n_by;
             for (int32_t sl = 0; sl < nslot; ++sl) n_by[scount[sl] == 1 ? 2 : scount[sl]]++;
@@ -923,6 +959,70 @@ static fea_status build_blocks(fea_ctx c, bool v5, bool orient, int64_t e_max, i
             for (int32_t m = sstart[sl]; m < sstart[sl] + scount[sl]; ++m)
                 contrib.push_back((uint16_t)(((recs[m].t & 0xffff) * EM + recs[m].le) | ((recs[m].t >> 16) << 15)));
             if (ecount(sl) != scount[sl]) contrib.push_back((uint16_t)e_max);  // the zero cell
+        }
+        if (v6) {  // kernel v6 record: class A in slot order, class B (> 2 contributors) by count
+            if (nslot > 65535) {
+                o.err = "more than 65535 slots in one block";
+                return;
+            }
+            const int32_t nA = (nslot + 31) & ~31;
+            std::vector<uint32_t> ia(nA, 0xffffffffu);
+            std::map<int32_t, std::vector<int32_t>> clsB;  // C -> slots
+            for (int32_t sl = 0; sl < nslot; ++sl) {
+                const int32_t C = scount[sl];
+                auto off = [&](int32_t m) { return (uint32_t)((recs[m].t & 0xffff) * EM + recs[m].le); };
+                if (C == 1) ia[sl] = off(sstart[sl]) | (uint32_t)e_max << 16;  // + the zero cell
+                else if (C == 2) ia[sl] = off(sstart[sl]) | off(sstart[sl] + 1) << 16;
+                else clsB[C].push_back(sl);
+            }
+            const int32_t ncl = (int32_t)clsB.size();
+            if (ncl > FEA_MAX_CLASSES) {
+                o.err = "too many contributor-count classes";
+                return;
+            }
+            int32_t off = 16 * ncl;  // class-B part: table, then item arrays (offsets from the table)
+            std::vector<int32_t> coff;
+            for (const auto& kv : clsB) {
+                coff.push_back(off);
+                off += fea_pad16((int32_t)kv.second.size() * fea5_item_bytes(kv.first));
+            }
+            const int32_t bytes = (4 * nA + off + 127) & ~127;
+            o.rec.assign(bytes, 0);
+            std::memcpy(o.rec.data(), ia.data(), 4 * (size_t)nA);
+            int32_t* tab = reinterpret_cast<int32_t*>(o.rec.data() + 4 * nA);
+            int k2 = 0;
+            for (const auto& kv : clsB) {
+                const int C = kv.first, R = fea5_item_bytes(C), n = (int)kv.second.size();
+                tab[4 * k2] = C;
+                tab[4 * k2 + 1] = n;
+                tab[4 * k2 + 2] = coff[k2];
+                tab[4 * k2 + 3] = R;
+                for (int it = 0; it < n; ++it) {
+                    const int32_t sl = kv.second[it];
+                    uint16_t* w = reinterpret_cast<uint16_t*>(o.rec.data() + 4 * nA + coff[k2] + (size_t)it * R);
+                    w[0] = (uint16_t)sl;
+                    for (int q = 0; q < C; ++q) {
+                        const int32_t m = sstart[sl] + q;
+                        w[1 + q] = (uint16_t)((recs[m].t & 0xffff) * EM + recs[m].le);
+                    }
+                }
+                ++k2;
+            }
+            FeaBlock& F = o.fb;
+            F.nslots = nslot;
+            F.ncontrib = (int32_t)recs.size();
+            F.nE = (int32_t)E.size();
+            F.ncls = ncl;
+            F.rec_bytes = bytes;
+            F.r0 = (int32_t)ga;
+            F.nr = (int32_t)(gb - ga);
+            const int32_t nEp = fea_pad4(F.nE);
+            o.dofs.assign((size_t)np * nEp, 0);
+            for (int64_t le = 0; le < (int64_t)E.size(); ++le)
+                for (int i = 0; i < np; ++i) o.dofs[i * nEp + le] = c->ed[(size_t)E[le] * np + i];
+            for (int64_t le = E.size(); le < nEp; ++le)
+                for (int i = 0; i < np; ++i) o.dofs[i * nEp + le] = o.dofs[i * nEp];
+            return;
         }
         FeaBlock& F = o.fb;
         F.nslots = nslot;
@@ -1057,11 +1157,23 @@ fea_status fea_build_pattern(fea_ctx c, int64_t* row_begin, int64_t* n_rows_loca
     // ---- shared-memory budget -> elements per block (e_max) and record budget
     const int dm = (c->plan_which & FEA_MASS) ? 1 : 0, dcm = (c->plan_which & FEA_STIFF) ? 1 : 0;
     const int nmat = dm + dcm;
-    const bool v5 = fea5_supported(c->order, nq) && c->tune_kver != 4 && !c->split;
-    c->kver = v5 ? 5 : 4;
+    const bool v6 = fea6_supported(c->order, nq) && (c->tune_kver == 0 || c->tune_kver == 6) && !c->split;
+    const bool v5 = !v6 && fea5_supported(c->order, nq) && c->tune_kver != 4 && !c->split;
+    c->kver = v6 ? 6 : v5 ? 5 : 4;
     const int rstages = c->order <= 2 ? 3 : 2;  // fea_rstages (v4)
     int64_t e_max, rec_budget;
-    if (v5) {
+    if (v6) {
+        // two V buffers, two gather / Lambda / W stages (fea6_smem_layout); records stay in global memory
+        const int64_t budget = c->tune_smem ? c->tune_smem : 227 * 1024;
+        e_max = std::min<int64_t>(512, 65535 / T - 2) / 8 * 8;
+        if (c->tune_emax) e_max = std::min<int64_t>(e_max, c->tune_emax / 8 * 8);
+        int32_t L6[FEA_L_N];
+        for (; e_max >= 8; e_max -= 8) {
+            fea6_smem_layout(L6, (int)e_max, c->order, dm, dcm);
+            if (L6[FEA6_L_TOTAL] <= budget) break;
+        }
+        rec_budget = INT64_MAX / 4;
+    } else if (v5) {
         // two V_m, V_c [T][e_max | 1] buffers + two record stages in 227 KiB (one CTA per SM)
         const int64_t budget = c->tune_smem ? c->tune_smem : 227 * 1024;
         const double rec_el = 1.1 * 2.0 * np * np + 8;  // record bytes per element (estimate)
@@ -1097,11 +1209,12 @@ fea_status fea_build_pattern(fea_ctx c, int64_t* row_begin, int64_t* n_rows_loca
         }
     }
 
-    const int64_t EM = v5 ? (e_max | 1) : fea4_vstride((int32_t)e_max);  // V row strides (fea_internal.h)
+    const int64_t EM = v6 ? fea6_vstride((int32_t)e_max) : v5 ? (e_max | 1) : fea4_vstride((int32_t)e_max);  // V row strides
     PlanData P;
     {
         // v5 with both matrices: V_m, V_c interleaved, phase B reads 16-byte {m, c} pairs
-        const fea_status st = build_blocks(c, v5, false, e_max, rec_budget, EM, P, v5 && nmat == 2);
+        const fea_status st = v6 ? build_blocks(c, true, false, e_max, rec_budget, EM, P, nmat == 2, true)
+                                 : build_blocks(c, v5, false, e_max, rec_budget, EM, P, v5 && nmat == 2);
         if (st != FEA_OK) return st;
     }
     const int64_t nb = (int64_t)P.blocks.size();
@@ -1118,13 +1231,14 @@ fea_status fea_build_pattern(fea_ctx c, int64_t* row_begin, int64_t* n_rows_loca
     std::vector<int32_t>& alldofs = P.dofs;
     const int64_t visits = P.visits, owned = P.owned, ncon = P.ncon, rbytes = P.rbytes;
     int32_t L[FEA_L_N];
-    if (v5) fea5_smem_layout(L, (int)rec_max, (int)e_max, c->order, dm, dcm);
+    if (v6) fea6_smem_layout(L, (int)e_max, c->order, dm, dcm);
+    else if (v5) fea5_smem_layout(L, (int)rec_max, (int)e_max, c->order, dm, dcm);
     else fea_smem_layout(L, rstages, (int)rec_max, (int)e_max, c->order, c->split ? 0 : nq, dm, dcm);
     c->nblocks = (int)nb;
     c->e_max = (int)e_max;
     c->rec_max = (int)rec_max;
     c->nnz = nnz;
-    c->smem_bytes = L[FEA_L_TOTAL];
+    c->smem_bytes = v6 ? L[FEA6_L_TOTAL] : L[FEA_L_TOTAL];
     std::memcpy(c->lay, L, sizeof(c->lay));
     // ---- interface sets I_t of every rank t (world > 1): owned DOFs that another rank's elements
     // read.  Ranks own contiguous chunks of rows_per_rank library rows; every rank derives the
@@ -1170,7 +1284,7 @@ fea_status fea_build_pattern(fea_ctx c, int64_t* row_begin, int64_t* n_rows_loca
     if (nb) FEA_CUDA(c, cudaMemcpy(c->d_blocks, blocks.data(), nb * sizeof(FeaBlock), cudaMemcpyHostToDevice));
     FEA_CUDA(c, cudaMalloc((void**)&c->d_records, records.size()));
     FEA_CUDA(c, cudaMemcpy(c->d_records, records.data(), records.size(), cudaMemcpyHostToDevice));
-    if (v5) {
+    if (v5 || v6) {
         FEA_CUDA(c, cudaMalloc((void**)&c->d_dofs, alldofs.size() * sizeof(int32_t)));
         FEA_CUDA(c, cudaMemcpy(c->d_dofs, alldofs.data(), alldofs.size() * sizeof(int32_t), cudaMemcpyHostToDevice));
     }
@@ -1190,8 +1304,9 @@ fea_status fea_build_pattern(fea_ctx c, int64_t* row_begin, int64_t* n_rows_loca
         FEA_CUDA(c, cudaMalloc(&c->d_irecv, std::max<size_t>(1, (size_t)c->maxI * c->world) * sizeof(double)));
     }
     int occ = 0;
-    int rc = v5 ? fea_kernel_occupancy5(c->order, dm, dcm, c->smem_bytes, &occ, &c->threads)
-                : fea_kernel_occupancy(c->order, c->nq, dm, dcm, c->smem_bytes, &occ, &c->threads);
+    int rc = v6   ? fea_kernel_occupancy6(c->order, dm, dcm, c->smem_bytes, &occ, &c->threads)
+             : v5 ? fea_kernel_occupancy5(c->order, dm, dcm, c->smem_bytes, &occ, &c->threads)
+                  : fea_kernel_occupancy(c->order, c->nq, dm, dcm, c->smem_bytes, &occ, &c->threads);
     if (rc != 0) return c->fail(FEA_E_CUDA, "occupancy query: %s", cudaGetErrorString((cudaError_t)rc));
     if (occ < 1) return c->fail(FEA_E_UNSUPPORTED, "kernel does not fit: %d B shared memory", c->smem_bytes);
     c->grid = (int)std::min<int64_t>(std::max<int64_t>(nb, 1), (int64_t)occ * c->sm_count);
@@ -1284,13 +1399,20 @@ static fea_status launch(fea_ctx c, const double* u, double* vm, double* vc, boo
     prm.nq = rule_c ? c->nq_c : c->nq;
     prm.same_coef = same_coef(c->coef_m, c->coef_c) ? 1 : 0;
     std::memcpy(prm.lay, c->lay, sizeof(prm.lay));
+    // a single-matrix pass on a plan sized for the other matrix: its V region has size 0 in the
+    // layout, so it takes the planned matrix's region (same size, same contributor offsets)
+    // (kernel v6 has one V region either way: its single-matrix passes use it with 8-byte cells)
+    const bool pm = c->plan_which & FEA_MASS, pc = c->plan_which & FEA_STIFF;
+    if (c->kver != 6 && vc && !vm && !pc) prm.lay[FEA_L_VC] = c->lay[FEA_L_VM];
+    if (c->kver != 6 && vm && !vc && !pm) prm.lay[FEA_L_VM] = c->lay[FEA_L_VC];
+    if (vm && vc && !(pm && pc)) return c->fail(FEA_E_STATE, "internal: fused M+K pass on a one-matrix plan");
     prm.coef_m = c->coef_m;
     prm.coef_c = c->coef_c;
     const std::vector<double>& tab = rule_c ? c->tables_c : c->tables;
     std::memcpy(prm.ctab, tab.data(), tab.size() * sizeof(double));
     if (c->kver == 5) std::memcpy(prm.jtab, c->jplain.data(), c->jplain.size() * sizeof(double));
-    if (const char* dm = getenv("FEA_DEBUG_MODE")) prm.dbg_mode = atoi(dm);
-    if (getenv("FEA_DEBUG_TIMING")) {
+    prm.dbg_mode = c->dbg_mode;
+    if (c->dbg_timing) {
         if (!c->d_dbg) {
             FEA_CUDA(c, cudaMalloc(&c->d_dbg, 1536 * sizeof(unsigned long long)));
             FEA_CUDA(c, cudaMemset(c->d_dbg, 0, 1536 * sizeof(unsigned long long)));
@@ -1298,9 +1420,10 @@ static fea_status launch(fea_ctx c, const double* u, double* vm, double* vc, boo
         prm.dbg = c->d_dbg;
     }
     if (b1 <= b0) return FEA_OK;
-    const int grid = std::min(c->grid, b1 - b0);
-    const int rc = c->kver == 5 ? fea_launch_reassemble5(prm, c->order, c->smem_bytes, grid, c->stream)
-                                : fea_launch_reassemble(prm, c->order, c->smem_bytes, grid, c->stream);
+    const int grid = std::min(c->int_grid_cap > 0 ? c->int_grid_cap : c->grid, b1 - b0);
+    const int rc = c->kver == 6   ? fea_launch_reassemble6(prm, c->order, c->smem_bytes, grid, c->stream)
+                   : c->kver == 5 ? fea_launch_reassemble5(prm, c->order, c->smem_bytes, grid, c->stream)
+                                  : fea_launch_reassemble(prm, c->order, c->smem_bytes, grid, c->stream);
     if (rc != 0) return c->fail(FEA_E_CUDA, "k_reassemble launch: %s", cudaGetErrorString((cudaError_t)rc));
     return FEA_OK;
 }
@@ -1316,7 +1439,8 @@ static fea_status assemble_part(fea_ctx c, const double* u_full, double* mass_va
         if (mass_vals && (s = launch(c, u_full, mass_vals, nullptr, false, b0, b1)) != FEA_OK) return s;
         return stiff_vals ? launch(c, u_full, nullptr, stiff_vals, true, b0, b1) : FEA_OK;
     }
-    if (mass_vals && stiff_vals && !(pm && pc)) {  // plan sized for one matrix: two passes
+    // plan sized for one matrix, or (kernel v6, one Lambda) distinct coefficients: two passes
+    if (mass_vals && stiff_vals && (!(pm && pc) || (c->kver == 6 && !same_coef(c->coef_m, c->coef_c)))) {
         if ((s = launch(c, u_full, mass_vals, nullptr, false, b0, b1)) != FEA_OK) return s;
         return launch(c, u_full, nullptr, stiff_vals, false, b0, b1);
     }
@@ -1332,9 +1456,14 @@ fea_status fea_assemble(fea_ctx c, const double* u_full, double* mass_vals, doub
         return c->fail(FEA_E_ARG, "vals must be 16-byte aligned");
     if (!mass_vals && !stiff_vals) return FEA_OK;
     cudaSetDevice(c->device);
-    if (c->world == 1) return assemble_part(c, u_full, mass_vals, stiff_vals, FEA_PART_ALL);
-    const fea_status s = assemble_part(c, u_full, mass_vals, stiff_vals, FEA_PART_INT);
-    return s != FEA_OK ? s : assemble_part(c, u_full, mass_vals, stiff_vals, FEA_PART_BND);
+    fea_status s = tmark(c, 2, c->stream);
+    if (s != FEA_OK) return s;
+    if (c->world == 1) s = assemble_part(c, u_full, mass_vals, stiff_vals, FEA_PART_ALL);
+    else {
+        s = assemble_part(c, u_full, mass_vals, stiff_vals, FEA_PART_INT);
+        if (s == FEA_OK) s = assemble_part(c, u_full, mass_vals, stiff_vals, FEA_PART_BND);
+    }
+    return s != FEA_OK ? s : tmark(c, 3, c->stream);
 }
 
 fea_status fea_assemble_mass(fea_ctx c, const double* u_full, double* vals) {
@@ -1347,6 +1476,35 @@ fea_status fea_assemble_stiffness(fea_ctx c, const double* u_full, double* vals)
     return fea_assemble(c, u_full, nullptr, vals);
 }
 
+// One allgather of `count` float64 per rank, stream-ordered on `st`: ncclAllGather on the
+// library's communicator, or the caller's host transport (D2H of this rank's values, wait, the
+// callback, H2D of every rank's values; the pinned buffers are reused only after the next call's
+// wait on the same stream).
+static fea_status allgather(fea_ctx c, const double* send, double* recv, int64_t count, cudaStream_t st) {
+    if (count <= 0) return FEA_OK;
+    if (c->htrans) {
+        if (c->h_cap < count) {
+            if (c->h_send) cudaFreeHost(c->h_send);
+            if (c->h_recv) cudaFreeHost(c->h_recv);
+            c->h_send = c->h_recv = nullptr;
+            c->h_cap = 0;
+            FEA_CUDA(c, cudaMallocHost(&c->h_send, (size_t)count * sizeof(double)));
+            FEA_CUDA(c, cudaMallocHost(&c->h_recv, (size_t)count * c->world * sizeof(double)));
+            c->h_cap = count;
+        }
+        FEA_CUDA(c, cudaMemcpyAsync(c->h_send, send, (size_t)count * sizeof(double), cudaMemcpyDeviceToHost, st));
+        FEA_CUDA(c, cudaStreamSynchronize(st));
+        const int rc = c->htrans(c->h_send, c->h_recv, count, c->huser);
+        if (rc != 0) return c->fail(FEA_E_NCCL, "host transport returned %d", rc);
+        FEA_CUDA(c, cudaMemcpyAsync(recv, c->h_recv, (size_t)count * c->world * sizeof(double), cudaMemcpyHostToDevice, st));
+        return FEA_OK;
+    }
+    if (!c->comm) return c->fail(FEA_E_STATE, "world > 1 requires fea_set_nccl or fea_set_host_transport");
+    ncclResult_t r = nccl().allGather(send, recv, (size_t)count, ncclDouble, (ncclComm_t)c->comm, st);
+    if (r != ncclSuccess) return c->fail(FEA_E_NCCL, "ncclAllGather: %s", nccl().getErrorString(r));
+    return FEA_OK;
+}
+
 // u_owned (this rank's rows) -> c->d_ufull holding every value this rank's kernel reads:
 // interface-only (pack, one ncclAllGather of maxI values per rank, unpack) or the full-vector
 // allgather of rows_per_rank values per rank.  Stream-ordered on the ctx stream.
@@ -1355,11 +1513,8 @@ static fea_status exchange_u(fea_ctx c, const double* u_owned) {
         int rc = fea_launch_pack(u_owned, c->d_iface + c->ioff[c->rank], (int)(c->ioff[c->rank + 1] - c->ioff[c->rank]),
                                  c->row_begin, c->maxI, c->d_isend, c->stream);
         if (rc) return c->fail(FEA_E_CUDA, "pack: %s", cudaGetErrorString((cudaError_t)rc));
-        if (c->maxI > 0) {
-            ncclResult_t r = nccl().allGather(c->d_isend, c->d_irecv, (size_t)c->maxI, ncclDouble, (ncclComm_t)c->comm,
-                                              c->stream);
-            if (r != ncclSuccess) return c->fail(FEA_E_NCCL, "ncclAllGather: %s", nccl().getErrorString(r));
-        }
+        fea_status s = allgather(c, c->d_isend, c->d_irecv, c->maxI, c->stream);
+        if (s != FEA_OK) return s;
         rc = fea_launch_unpack(c->d_irecv, c->d_iface, c->d_ioff, c->world, c->rank, c->maxI, c->ioff[c->world],
                                u_owned, c->row_begin, c->n_rows, c->d_ufull, c->stream);
         if (rc) return c->fail(FEA_E_CUDA, "unpack: %s", cudaGetErrorString((cudaError_t)rc));
@@ -1368,10 +1523,7 @@ static fea_status exchange_u(fea_ctx c, const double* u_owned) {
     // full vector: pad the owned slice to rows_per_rank, then allgather
     if (c->n_rows && u_owned != c->d_usend)
         FEA_CUDA(c, cudaMemcpyAsync(c->d_usend, u_owned, c->n_rows * sizeof(double), cudaMemcpyDeviceToDevice, c->stream));
-    ncclResult_t r = nccl().allGather(c->d_usend, c->d_ufull, (size_t)c->rows_per_rank, ncclDouble,
-                                      (ncclComm_t)c->comm, c->stream);
-    if (r != ncclSuccess) return c->fail(FEA_E_NCCL, "ncclAllGather: %s", nccl().getErrorString(r));
-    return FEA_OK;
+    return allgather(c, c->d_usend, c->d_ufull, c->rows_per_rank, c->stream);
 }
 
 // NEXT-3 overlap: the owned rows go into u_full on the ctx stream, the interior blocks (which read
@@ -1388,22 +1540,33 @@ static fea_status reassemble_overlap(fea_ctx c, const double* u_owned, double* m
                                     cudaMemcpyDeviceToDevice, c->stream));
     FEA_CUDA(c, cudaEventRecord(c->ev_own, c->stream));
     FEA_CUDA(c, cudaStreamWaitEvent(c->stream2, c->ev_own, 0));
+    fea_status s = tmark(c, 0, c->stream2);
+    if (s != FEA_OK) return s;
+    // a host transport blocks this thread inside the exchange: enqueue the interior blocks first
+    const bool host = c->htrans != nullptr;
+    if (host) {
+        if ((s = tmark(c, 2, c->stream)) != FEA_OK) return s;
+        if ((s = assemble_part(c, c->d_ufull, mass_vals, stiff_vals, FEA_PART_INT)) != FEA_OK) return s;
+    }
     int rc = fea_launch_pack(u_owned, c->d_iface + c->ioff[c->rank], (int)(c->ioff[c->rank + 1] - c->ioff[c->rank]),
                              c->row_begin, c->maxI, c->d_isend, c->stream2);
     if (rc) return c->fail(FEA_E_CUDA, "pack: %s", cudaGetErrorString((cudaError_t)rc));
-    if (c->maxI > 0) {
-        ncclResult_t r = nccl().allGather(c->d_isend, c->d_irecv, (size_t)c->maxI, ncclDouble, (ncclComm_t)c->comm,
-                                          c->stream2);
-        if (r != ncclSuccess) return c->fail(FEA_E_NCCL, "ncclAllGather: %s", nccl().getErrorString(r));
-    }
+    if ((s = allgather(c, c->d_isend, c->d_irecv, c->maxI, c->stream2)) != FEA_OK) return s;
     rc = fea_launch_unpack(c->d_irecv, c->d_iface, c->d_ioff, c->world, c->rank, c->maxI, c->ioff[c->world],
                            u_owned, c->row_begin, 0 /* owned rows already copied */, c->d_ufull, c->stream2);
     if (rc) return c->fail(FEA_E_CUDA, "unpack: %s", cudaGetErrorString((cudaError_t)rc));
+    if ((s = tmark(c, 1, c->stream2)) != FEA_OK) return s;
     FEA_CUDA(c, cudaEventRecord(c->ev_halo, c->stream2));
-    fea_status s = assemble_part(c, c->d_ufull, mass_vals, stiff_vals, FEA_PART_INT);
-    if (s != FEA_OK) return s;
+    if (!host) {  // NCCL: its kernel is queued first; the interior grid leaves it int_grid_cap SMs
+        if ((s = tmark(c, 2, c->stream)) != FEA_OK) return s;
+        c->int_grid_cap = std::max(1, c->grid - 4);
+        s = assemble_part(c, c->d_ufull, mass_vals, stiff_vals, FEA_PART_INT);
+        c->int_grid_cap = 0;
+        if (s != FEA_OK) return s;
+    }
     FEA_CUDA(c, cudaStreamWaitEvent(c->stream, c->ev_halo, 0));
-    return assemble_part(c, c->d_ufull, mass_vals, stiff_vals, FEA_PART_BND);
+    s = assemble_part(c, c->d_ufull, mass_vals, stiff_vals, FEA_PART_BND);
+    return s != FEA_OK ? s : tmark(c, 3, c->stream);
 }
 
 fea_status fea_get_interface(fea_ctx c, int64_t* offsets, int32_t* dofs) {
@@ -1443,12 +1606,14 @@ fea_status fea_reassemble(fea_ctx c, const double* u_owned, double* mass_vals, d
     if (!u_owned) return c->fail(FEA_E_ARG, "u_owned is NULL");
     cudaSetDevice(c->device);
     if (c->world == 1) return fea_assemble(c, u_owned, mass_vals, stiff_vals);
-    if (!c->comm) return c->fail(FEA_E_STATE, "world > 1 requires fea_set_nccl");
+    if (!c->comm && !c->htrans) return c->fail(FEA_E_STATE, "world > 1 requires fea_set_nccl or fea_set_host_transport");
     if ((mass_vals && ((uintptr_t)mass_vals & 15)) || (stiff_vals && ((uintptr_t)stiff_vals & 15)))
         return c->fail(FEA_E_ARG, "vals must be 16-byte aligned");
     if (c->exchange == 0 && c->tune_overlap)
         return reassemble_overlap(c, u_owned, mass_vals, stiff_vals);
-    const fea_status st = exchange_u(c, u_owned);
+    fea_status st = tmark(c, 0, c->stream);
+    if (st == FEA_OK) st = exchange_u(c, u_owned);
+    if (st == FEA_OK) st = tmark(c, 1, c->stream);
     if (st != FEA_OK) return st;
     return fea_assemble(c, c->d_ufull, mass_vals, stiff_vals);
 }
@@ -1467,7 +1632,6 @@ fea_status fea_reassemble_host(fea_ctx c, const double* u_host, double* mass_hos
     fea_status s;
     if (c->world == 1) s = fea_assemble(c, c->d_ufull, mass_host ? c->d_vm : nullptr, stiff_host ? c->d_vc : nullptr);
     else {
-        if (!c->comm) return c->fail(FEA_E_STATE, "world > 1 requires fea_set_nccl");
         s = fea_reassemble(c, c->d_usend, mass_host ? c->d_vm : nullptr, stiff_host ? c->d_vc : nullptr);
     }
     if (s != FEA_OK) return s;
@@ -1598,6 +1762,13 @@ fea_status fea_nccl_unique_id(void* id_out) {
     return FEA_OK;
 }
 
+fea_status fea_set_host_transport(fea_ctx c, fea_host_allgather_fn fn, void* user) {
+    if (!c) return FEA_E_ARG;
+    c->htrans = fn;
+    c->huser = user;
+    return FEA_OK;
+}
+
 fea_status fea_set_nccl(fea_ctx c, const void* id_bytes) {
     if (!c || !id_bytes) return FEA_E_ARG;
     if (c->host_only) return c->fail(FEA_E_STATE, "host-only (planning) context has no device");
@@ -1643,6 +1814,17 @@ fea_status fea_get_stat(fea_ctx c, int key, int64_t* value) {
             break;
         }
         case 10: *value = c->rec_max; break;
+        case 36: case 37: {  // FEA_TUNE_TIMING: exchange / assembly time of the last call, microseconds
+            const int i0 = key == 36 ? 0 : 2;
+            const bool have = key == 36 ? c->t_exch : c->t_asm;
+            float ms = 0.f;
+            if (have) {
+                FEA_CUDA(c, cudaEventSynchronize(c->ev_t[i0 + 1]));
+                FEA_CUDA(c, cudaEventElapsedTime(&ms, c->ev_t[i0], c->ev_t[i0 + 1]));
+            }
+            *value = have ? (int64_t)llround(1000.0 * ms) : -1;
+            break;
+        }
         default:
             if (key >= 40 && key < 1536 + 24) {  // FEA_DEBUG_MODE & 8 / 32 trace words
                 unsigned long long v = 0;

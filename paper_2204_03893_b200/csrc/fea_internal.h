@@ -31,6 +31,7 @@ __host__ __device__ constexpr int fea_rstages(int p) { return p <= 2 ? 3 : 2; }
 #ifndef FEA5_PF
 #define FEA5_PF 3  // kernel v5: L2 prefetch distance (blocks); at most 5 (the descriptor ring)
 #endif
+static_assert(FEA5_PF >= 1 && FEA5_PF <= 5, "FEA5_PF: the 8-entry descriptor ring is filled 6 blocks ahead");
 #ifndef FEA4_A1FIRST
 #define FEA4_A1FIRST 1  // kernel v4: warps running A1(j+1) before B(j): 0 none, 1 odd warps, 2 all
 #endif
@@ -288,3 +289,53 @@ int fea_kernel_occupancy(int order, int nq, int do_m, int do_c, int smem_bytes, 
 // The same for kernel v5 (fea_kernels5.cu).
 int fea_launch_reassemble5(const FeaKParams& prm, int order, int smem_bytes, int grid, void* stream);
 int fea_kernel_occupancy5(int order, int do_m, int do_c, int smem_bytes, int* ctas_per_sm, int* threads);
+
+// ---- kernel v6 (P3 / P4 with the configs' native rules; fea_kernels6.cu): warp-specialised
+// persistent CTA -- NA "A" warps (A1 interpolation + A2 contraction on DMMA, RT row tiles of Q
+// each), NB "B" warps (phase B), one producer warp (gathers).  V is double-buffered so phase B of
+// block j overlaps A2 of block j + 1; the block records stay in global memory (L2-prefetched) and
+// phase B reads them with coalesced loads, which frees the shared memory for the second V buffer.
+#ifndef FEA6_NB
+#define FEA6_NB 7
+#endif
+__host__ __device__ constexpr bool fea6_supported(int p, int nq) { return p >= 3 && nq == fea_nq_native(p); }
+__host__ __device__ constexpr int fea6_na(int p) { return p == 4 ? 8 : 7; }
+__host__ __device__ constexpr int fea6_rt(int p) { return p == 4 ? 2 : 1; }
+__host__ __device__ constexpr int fea6_threads(int p) { return (fea6_na(p) + FEA6_NB + 1) * 32; }
+// Lambda / gathered-u row stride (doubles): == 4 (mod 16), so the DMMA B-fragment loads
+// [(4 kk + c) ls + 8 et + g] are conflict-free per half-warp
+__host__ __device__ inline int32_t fea6_lstride(int32_t e_max) { return e_max + ((4 - e_max) % 16 + 16) % 16; }
+// V row stride in cells (a cell = {m, c} double2 for M + K, one double otherwise): odd, so the
+// epilogue's 16-byte stores (columns 2c, 2c + 1 of rows g, g + 1) are conflict-free per quarter-
+// warp; column e_max of row 0 is the zero cell (never written by A2)
+__host__ __device__ inline int32_t fea6_vstride(int32_t e_max) { return e_max + 1; }
+// v6 record (global memory only; one per block, 128-byte aligned): class A = u32 items for the
+// block's slots in CSR order [pad32(nslots)]: {u16 V offset 0, u16 V offset 1} -- one
+// contributor: offset 1 = the zero cell (e_max); two contributors: both, in ascending library
+// element order; more: 0xffff (a hole, the slot is a class-B item); then the class-B table
+// int4 {C, n_items, byte offset, item bytes} [ncls] and the v5-format items {u16 block-local slot,
+// u16 V offset [C]} (offsets relative to the table).  Lane l of a warp handles slot 32 k + l of
+// class A, so its CSR stores are contiguous.
+enum { FEA6_L_V = 0, FEA6_L_VB = 1, FEA6_L_GU = 2, FEA6_L_GUB = 3, FEA6_L_GX = 4, FEA6_L_GXB = 5, FEA6_L_LAM = 6,
+       FEA6_L_LAMB = 7, FEA6_L_W = 8, FEA6_L_WB = 9, FEA6_L_BARS = 10, FEA6_L_TOTAL = 11 };
+__host__ __device__ inline void fea6_smem_layout(int32_t* L, int e_max, int p, int do_m, int do_c) {
+    const int T = fea_T(p), np = fea_np(p), nqp = 4 * fea_nk(fea_nq_native(p));
+    const int ls = fea6_lstride(e_max), vs = fea6_vstride(e_max);
+    const int cell = (do_m && do_c) ? 16 : 8;
+    for (int i = 0; i < FEA_L_N; ++i) L[i] = 0;
+    int32_t o = 0;
+    L[FEA6_L_VB] = fea_align(T * vs * cell, 128);
+    L[FEA6_L_V] = o; o += 2 * L[FEA6_L_VB];
+    L[FEA6_L_GUB] = fea_align(8 * np * ls, 128);
+    L[FEA6_L_GU] = o; o += 2 * L[FEA6_L_GUB];
+    L[FEA6_L_GXB] = fea_align(16 * 3 * e_max, 128);
+    L[FEA6_L_GX] = o; o += 2 * L[FEA6_L_GXB];
+    L[FEA6_L_LAMB] = fea_align(8 * nqp * ls, 128);
+    L[FEA6_L_LAM] = o; o += 2 * L[FEA6_L_LAMB];
+    L[FEA6_L_WB] = fea_align(8 * 3 * e_max, 128);
+    L[FEA6_L_W] = o; o += 2 * L[FEA6_L_WB];
+    L[FEA6_L_BARS] = o; o += 8 * 8;
+    L[FEA6_L_TOTAL] = o;
+}
+int fea_launch_reassemble6(const FeaKParams& prm, int order, int smem_bytes, int grid, void* stream);
+int fea_kernel_occupancy6(int order, int do_m, int do_c, int smem_bytes, int* ctas_per_sm, int* threads);

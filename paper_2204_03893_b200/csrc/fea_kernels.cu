@@ -142,15 +142,19 @@ __global__ void __launch_bounds__(fea_threads(P), fea_ctas(P)) k_reassemble(cons
     const double* cPhi = prm.ctab;
     const double* cW = prm.ctab + ((NP * nq + 1) & ~1);
 
+#ifdef FEA5_DIAG
     unsigned long long tacc[6] = {0, 0, 0, 0, 0, 0};
     unsigned long long tcl = 0;
-    auto tick = [&](int slot) {  // optional phase timing (consumer thread 0)
+    auto tick = [&](int slot) {  // optional phase timing (consumer thread 0), diagnostics builds only
         if (prm.dbg && tid == 0) {
             const unsigned long long now = clock64();
             if (slot >= 0) tacc[slot] += now - tcl;
             tcl = now;
         }
     };
+#else
+    auto tick = [](int) {};
+#endif
     const int vs = fea4_vstride(e_max);  // V row stride (fea_internal.h)
 
     // ---------------- A1 of block j: geometry (W_e, b_e), u_q = Phi^T u_e, k(u_q), Lambda
@@ -316,8 +320,10 @@ __global__ void __launch_bounds__(fea_threads(P), fea_ctas(P)) k_reassemble(cons
             if (j + 1 < ncta_blocks) mbar_arrive(&gdone[(j + 1) & 1]);
         }
     }
+#ifdef FEA5_DIAG
     if (prm.dbg && tid == 0)
         for (int i = 0; i < 6; ++i) atomicAdd(prm.dbg + i, tacc[i]);
+#endif
 }
 
 using kfun_t = void (*)(const FeaKParams);

@@ -386,14 +386,10 @@ kfun_t select5(int order, int dm, int dc, int two) {
 int fea_launch_reassemble5(const FeaKParams& prm, int order, int smem_bytes, int grid, void* stream) {
     kfun_t kern = select5(order, prm.out_m != nullptr, prm.out_c != nullptr, !prm.same_coef);
     if (!kern) return (int)cudaErrorInvalidValue;
-    static thread_local const void* last = nullptr;  // attribute once per kernel variant / size
-    static thread_local int last_smem = -1;
-    if (last != (const void*)kern || last_smem != smem_bytes) {
-        cudaError_t err = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, smem_bytes);
-        if (err != cudaSuccess) return (int)err;
-        last = (const void*)kern;
-        last_smem = smem_bytes;
-    }
+    // the attribute is per (device, kernel): set it on every launch (cheap; a cached value goes stale
+    // when another context on this thread re-plans or the thread switches devices)
+    cudaError_t err = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, smem_bytes);
+    if (err != cudaSuccess) return (int)err;
     kern<<<grid, order == 1 ? fea5_threads(1) : fea5_threads(2), smem_bytes, (cudaStream_t)stream>>>(prm);
     return (int)cudaGetLastError();
 }

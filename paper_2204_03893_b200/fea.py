@@ -28,8 +28,13 @@ SYMBOLS = ["fea_create", "fea_set_element", "fea_set_rule", "fea_mesh_upload", "
            "fea_get_pattern", "fea_get_pattern_rows", "fea_get_dof_perm", "fea_get_elem_perm", "fea_set_coefficient",
            "fea_assemble_mass", "fea_assemble_stiffness", "fea_assemble", "fea_reassemble",
            "fea_reassemble_host", "fea_assemble_tensor", "fea_get_interface", "fea_exchange_pack",
-           "fea_exchange_unpack", "fea_nccl_unique_id", "fea_set_nccl", "fea_sync", "fea_get_stat",
+           "fea_exchange_unpack", "fea_nccl_unique_id", "fea_set_nccl", "fea_set_host_transport", "fea_sync",
+           "fea_get_stat",
            "fea_last_error", "fea_destroy"]
+
+
+# fea.h fea_host_allgather_fn: int (*)(const double* send, double* recv, int64_t count, void* user)
+HOST_ALLGATHER = C.CFUNCTYPE(C.c_int, C.c_void_p, C.c_void_p, C.c_int64, C.c_void_p)
 
 
 class FeaError(RuntimeError):
@@ -73,6 +78,7 @@ def load_library():
         "fea_exchange_unpack": [P, P, P, P],
         "fea_nccl_unique_id": [P],
         "fea_set_nccl": [P, P],
+        "fea_set_host_transport": [P, P, P],
         "fea_sync": [P],
         "fea_get_stat": [P, I, P],
     }
@@ -270,6 +276,30 @@ class Context:
     def set_nccl(self, uid: bytes):
         b = (C.c_char * 128).from_buffer_copy(uid)
         self._check(self._lib.fea_set_nccl(self._h, b))
+
+    def set_host_transport(self, fn):
+        """fn(send: np.ndarray[count], recv: np.ndarray[world * count]) -> None: an allgather of the
+        float64 values over any host transport (fea.h fea_set_host_transport); None -> NCCL.  The
+        arrays view the library's pinned buffers (valid during the call only)."""
+        if fn is None:
+            self._htrans = None
+            self._check(self._lib.fea_set_host_transport(self._h, None, None))
+            return
+        world = self.world
+
+        def tramp(send, recv, count, user):
+            try:
+                s = np.ctypeslib.as_array(C.cast(send, C.POINTER(C.c_double)), shape=(count,))
+                r = np.ctypeslib.as_array(C.cast(recv, C.POINTER(C.c_double)), shape=(count * world,))
+                fn(s, r)
+                return 0
+            except Exception:  # reported as FEA_E_NCCL by the library
+                import traceback
+                traceback.print_exc()
+                return 1
+
+        self._htrans = HOST_ALLGATHER(tramp)  # keep the ctypes thunk alive
+        self._check(self._lib.fea_set_host_transport(self._h, C.cast(self._htrans, C.c_void_p), None))
 
     def sync(self):
         self._check(self._lib.fea_sync(self._h))

@@ -34,14 +34,16 @@ SMALL = [("C1", 32), ("C2", 48), ("C3", 24), ("C4", 96), ("C5", 12), ("E2", 43)]
 @pytest.mark.parametrize("name,N", SMALL)
 @pytest.mark.parametrize("kernel", [0, 4])
 def test_config_parity_small(name, N, kernel):
-    """kernel 0: automatic (v5 for p <= 2 with the native rule), 4: v4 forced (FEA_TUNE_KERNEL)."""
+    """kernel 0: automatic (v5 for p <= 2, v6 for p >= 3 with the native rule), 4: v4 forced
+    (FEA_TUNE_KERNEL)."""
     cfg = scaled(CONFIGS[name], N)
     w = make_workload(cfg)
     mcoef, ccoef = coefs_of(cfg)
     for u in w.u_sequence(min(cfg.reassemblies, 2)):
         res = library_assemble(w.mesh, w.q_xy, w.q_w, u, cfg.p, mcoef, ccoef, which=cfg.which,
                                tuning={2: kernel} if kernel else None)
-        assert res["ctx"].stat(11) == (5 if cfg.p <= 2 and kernel == 0 else 4)
+        auto = 5 if cfg.p <= 2 else 6  # the automatic kernel for the native rules
+        assert res["ctx"].stat(11) == (auto if kernel == 0 else kernel)
         assert res["ctx"].stat(1) >= 2  # several blocks
         ref = oracle_for(w.mesh, w.q_xy, w.q_w, u, res["perm"], mcoef, ccoef, cfg.which)
         _check(res, ref, cfg.which)
@@ -91,9 +93,10 @@ def test_deterministic_across_runs_and_tilings(p):
     again = library_assemble(m, xy, w, u, p, coef, coef)
     assert np.array_equal(base["M"], again["M"]) and np.array_equal(base["K"], again["K"])
     # smem budgets (v4 and v5) and element caps per block (v5, FEA_TUNE_EMAX = 3)
-    # ... and v5 without the zero-padded single-contributor items (FEA_TUNE_PAD1 = 10)
+    # ... and v5 without the zero-padded single-contributor items (FEA_TUNE_PAD1 = 10); p >= 3:
+    # kernel v6 (default) and v4 (FEA_TUNE_KERNEL = 4) sum in the same order: bit-identical
     tunings = {1: [{1: 24000}, {3: 64}, {3: 120}, {10: 0}], 2: [{1: 40000}, {3: 48}, {3: 120}, {10: 0}],
-               3: [{1: 100000}, {1: 150000}], 4: [{1: 150000}, {1: 190000}]}[p]
+               3: [{1: 100000}, {1: 150000}, {3: 24}, {2: 4}], 4: [{1: 150000}, {1: 190000}, {3: 16}, {2: 4}]}[p]
     for tu in tunings:
         r = library_assemble(m, xy, w, u, p, coef, coef, tuning=tu)
         if 1 in tu or 3 in tu:
@@ -255,3 +258,41 @@ def test_separate_rules_per_matrix(p):
     assert maxabs_rel(M[: ctx.nnz].cpu().numpy(), refb.M) <= TOL
     assert maxabs_rel(K[: ctx.nnz].cpu().numpy(), refb.K) <= TOL
     ctx.close()
+
+
+@pytest.mark.parametrize("p", [1, 2, 3])
+@pytest.mark.parametrize("kernel", [0, 4])
+def test_assembling_more_than_planned(p, kernel):
+    """A plan sized for one matrix (FEA_TUNE_PLAN_WHICH) serves the other matrix too (fea.h: one
+    pass per matrix; the unplanned matrix takes the planned matrix's shared-memory V region)."""
+    import torch
+    from paper_2204_03893_b200.fea import Context
+    m = random_mesh_from_structured(9, p, seed=70 + p)
+    xy, w = triangle_rule(2 * p)
+    u = np.random.default_rng(70 + p).uniform(-1, 1, m.n_dof)
+    km, kc = (K_POLY, (1.0, 0.0, 1.0)), (K_EXP, (1.0, 0.5))
+    for plan in (MASS, STIFF):
+        ctx = Context(device=0)
+        ctx.set_element(p, xy, w)
+        ctx.mesh_upload(m.vert_xy, m.elem_vert, m.n_dof, m.elem_dof, reorder=True)
+        ctx.set_tuning(4, plan)
+        if kernel:
+            ctx.set_tuning(2, kernel)
+        _, _, nnz = ctx.build_pattern()
+        ctx.set_coefficient(MASS, *km)
+        ctx.set_coefficient(STIFF, *kc)
+        perm = ctx.get_dof_perm()
+        ul = torch.tensor(u[perm], dtype=torch.float64, device="cuda:0")
+        ref = oracle_for(m, xy, w, u, perm, km, kc, MASS | STIFF)
+        vm = torch.full((nnz,), np.nan, dtype=torch.float64, device="cuda:0")
+        vc = torch.full((nnz,), np.nan, dtype=torch.float64, device="cuda:0")
+        ctx.assemble(ul, vm, vc)
+        ctx.sync()
+        assert maxabs_rel(vm.cpu().numpy(), ref.M) <= TOL and maxabs_rel(vc.cpu().numpy(), ref.K) <= TOL
+        vm.fill_(np.nan)
+        vc.fill_(np.nan)
+        ctx.assemble_stiffness(ul, vc)
+        ctx.assemble_mass(ul, vm)
+        ctx.sync()
+        assert maxabs_rel(vm.cpu().numpy(), ref.M) <= TOL and maxabs_rel(vc.cpu().numpy(), ref.K) <= TOL
+        ctx.close()
