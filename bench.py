@@ -401,11 +401,18 @@ def run_ours(args):
         if os.environ.get("FEA_DEBUG_TIMING"):
             if asm.ctx.stat(11) == 5:  # per-warp timeline of k_reassemble5 (lane 0 of every warp)
                 names = ["compute", "move_refill", "full_wait", "rec_wait", "phaseB", "free_wait", "prologue"]
+            elif asm.ctx.stat(11) == 6:  # k_reassemble6: summed over the warps of each role
+                names = ["A_gather_wait", "A_A1", "A_barrier", "A_vfree_wait", "A_A2", "A_loop", "A6", "A7",
+                         "B_setup", "B_vfull_wait", "B_classA", "B_classB", "B4", "B5", "B6", "B7"]
+                ph = [asm.ctx.stat(20 + i) for i in range(16)] + [asm.ctx.stat(40 + i) for i in range(2)]
+                desc["phase_cycles"] = dict(zip(names + ["P_free_wait", "P_gather"], ph))
+                names = []
             else:
                 names = ["unused0", "unused1", "A2_dmma", "B_and_next_A1", "unused4", "barrier_wait"]
-            ph = [asm.ctx.stat(20 + i) for i in range(len(names))]
-            tot = sum(ph) or 1
-            desc["phase_cycles_pct"] = dict(zip(names, [round(100.0 * x / tot, 1) for x in ph]))
+            if names:
+                ph = [asm.ctx.stat(20 + i) for i in range(len(names))]
+                tot = sum(ph) or 1
+                desc["phase_cycles_pct"] = dict(zip(names, [round(100.0 * x / tot, 1) for x in ph]))
         line = {
             "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
             "warmup": args.warmup, "ms_per_step": ms_per_step, "higher_is_better": True,

@@ -960,59 +960,52 @@ static fea_status build_blocks(fea_ctx c, bool v5, bool orient, int64_t e_max, i
                 contrib.push_back((uint16_t)(((recs[m].t & 0xffff) * EM + recs[m].le) | ((recs[m].t >> 16) << 15)));
             if (ecount(sl) != scount[sl]) contrib.push_back((uint16_t)e_max);  // the zero cell
         }
-        if (v6) {  // kernel v6 record: class A in slot order, class B (> 2 contributors) by count
+        if (v6) {  // kernel v6 record: class A in slot order, class B (> 2 contributors) as flat items
             if (nslot > 65535) {
                 o.err = "more than 65535 slots in one block";
                 return;
             }
             const int32_t nA = (nslot + 31) & ~31;
             std::vector<uint32_t> ia(nA, 0xffffffffu);
-            std::map<int32_t, std::vector<int32_t>> clsB;  // C -> slots
+            std::vector<int32_t> clsB;  // slots with more than two contributors
+            int32_t cmax = 0;
             for (int32_t sl = 0; sl < nslot; ++sl) {
                 const int32_t C = scount[sl];
                 auto off = [&](int32_t m) { return (uint32_t)((recs[m].t & 0xffff) * EM + recs[m].le); };
                 if (C == 1) ia[sl] = off(sstart[sl]) | (uint32_t)e_max << 16;  // + the zero cell
                 else if (C == 2) ia[sl] = off(sstart[sl]) | off(sstart[sl] + 1) << 16;
-                else clsB[C].push_back(sl);
+                else {
+                    clsB.push_back(sl);
+                    cmax = std::max(cmax, C);
+                }
             }
-            const int32_t ncl = (int32_t)clsB.size();
-            if (ncl > FEA_MAX_CLASSES) {
-                o.err = "too many contributor-count classes";
+            // class B item: {u16 block-local slot, u16 C, u16 V offset [C]}, all items of the block
+            // padded to one size R (16, 32, 48 or 64 bytes: C <= 30)
+            const int32_t R = clsB.empty() ? 0 : fea_pad16(2 * (cmax + 2));
+            if (R > 64) {
+                o.err = "a slot with more than 30 contributors (kernel v6)";
                 return;
             }
-            int32_t off = 16 * ncl;  // class-B part: table, then item arrays (offsets from the table)
-            std::vector<int32_t> coff;
-            for (const auto& kv : clsB) {
-                coff.push_back(off);
-                off += fea_pad16((int32_t)kv.second.size() * fea5_item_bytes(kv.first));
-            }
-            const int32_t bytes = (4 * nA + off + 127) & ~127;
+            const int32_t bytes = (4 * nA + (int32_t)clsB.size() * R + 127) & ~127;
             o.rec.assign(bytes, 0);
             std::memcpy(o.rec.data(), ia.data(), 4 * (size_t)nA);
-            int32_t* tab = reinterpret_cast<int32_t*>(o.rec.data() + 4 * nA);
-            int k2 = 0;
-            for (const auto& kv : clsB) {
-                const int C = kv.first, R = fea5_item_bytes(C), n = (int)kv.second.size();
-                tab[4 * k2] = C;
-                tab[4 * k2 + 1] = n;
-                tab[4 * k2 + 2] = coff[k2];
-                tab[4 * k2 + 3] = R;
-                for (int it = 0; it < n; ++it) {
-                    const int32_t sl = kv.second[it];
-                    uint16_t* w = reinterpret_cast<uint16_t*>(o.rec.data() + 4 * nA + coff[k2] + (size_t)it * R);
-                    w[0] = (uint16_t)sl;
-                    for (int q = 0; q < C; ++q) {
-                        const int32_t m = sstart[sl] + q;
-                        w[1 + q] = (uint16_t)((recs[m].t & 0xffff) * EM + recs[m].le);
-                    }
+            for (size_t it = 0; it < clsB.size(); ++it) {
+                const int32_t sl = clsB[it];
+                uint16_t* w = reinterpret_cast<uint16_t*>(o.rec.data() + 4 * nA + it * R);
+                w[0] = (uint16_t)sl;
+                w[1] = (uint16_t)scount[sl];
+                for (int q = 0; q < scount[sl]; ++q) {
+                    const int32_t m = sstart[sl] + q;
+                    w[2 + q] = (uint16_t)((recs[m].t & 0xffff) * EM + recs[m].le);
                 }
-                ++k2;
             }
+            const int32_t ncl = (int32_t)clsB.size();
             FeaBlock& F = o.fb;
             F.nslots = nslot;
             F.ncontrib = (int32_t)recs.size();
             F.nE = (int32_t)E.size();
-            F.ncls = ncl;
+            F.ncls = ncl;  // v6: class-B items
+            F.pad_ = R;    // v6: class-B item bytes
             F.rec_bytes = bytes;
             F.r0 = (int32_t)ga;
             F.nr = (int32_t)(gb - ga);

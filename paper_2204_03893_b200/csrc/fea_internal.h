@@ -291,10 +291,11 @@ int fea_launch_reassemble5(const FeaKParams& prm, int order, int smem_bytes, int
 int fea_kernel_occupancy5(int order, int do_m, int do_c, int smem_bytes, int* ctas_per_sm, int* threads);
 
 // ---- kernel v6 (P3 / P4 with the configs' native rules; fea_kernels6.cu): warp-specialised
-// persistent CTA -- NA "A" warps (A1 interpolation + A2 contraction on DMMA, RT row tiles of Q
-// each), NB "B" warps (phase B), one producer warp (gathers).  V is double-buffered so phase B of
-// block j overlaps A2 of block j + 1; the block records stay in global memory (L2-prefetched) and
-// phase B reads them with coalesced loads, which frees the shared memory for the second V buffer.
+// persistent CTA -- NA "A" warps (the A2 contraction on DMMA, RT row tiles of Q each), NB "B" warps
+// (A1 of block j + 1, then phase B of block j), one producer warp (gathers u, element geometry).
+// V is double-buffered so phase B of block j overlaps A2 of block j + 1; the block records stay in
+// global memory (L2-prefetched) and phase B reads them with coalesced loads, which frees the
+// shared memory for the second V buffer.
 #ifndef FEA6_NB
 #define FEA6_NB 7
 #endif
@@ -312,12 +313,15 @@ __host__ __device__ inline int32_t fea6_vstride(int32_t e_max) { return e_max + 
 // v6 record (global memory only; one per block, 128-byte aligned): class A = u32 items for the
 // block's slots in CSR order [pad32(nslots)]: {u16 V offset 0, u16 V offset 1} -- one
 // contributor: offset 1 = the zero cell (e_max); two contributors: both, in ascending library
-// element order; more: 0xffff (a hole, the slot is a class-B item); then the class-B table
-// int4 {C, n_items, byte offset, item bytes} [ncls] and the v5-format items {u16 block-local slot,
-// u16 V offset [C]} (offsets relative to the table).  Lane l of a warp handles slot 32 k + l of
-// class A, so its CSR stores are contiguous.
-enum { FEA6_L_V = 0, FEA6_L_VB = 1, FEA6_L_GU = 2, FEA6_L_GUB = 3, FEA6_L_GX = 4, FEA6_L_GXB = 5, FEA6_L_LAM = 6,
-       FEA6_L_LAMB = 7, FEA6_L_W = 8, FEA6_L_WB = 9, FEA6_L_BARS = 10, FEA6_L_TOTAL = 11 };
+// element order; more: 0xffff (a hole, the slot is a class-B item); then FeaBlock::ncls class-B
+// items of FeaBlock::pad_ (R) bytes each: {u16 block-local slot, u16 C, u16 V offset [C]} (R = 16,
+// 32, 48 or 64: C <= 30).  Lane l of a warp handles slot 32 k + l of class A, so its CSR stores
+// are contiguous.
+// Shared memory (byte offsets / per-buffer bytes): V [2][T][vs] cells; GU [2][np][ls] gathered u;
+// GW [2][4][e_max] (|det B_e|, A00, A11, A01 from the producer); LW [3] Lambda [nqp][ls] then
+// W [3][e_max] (A1's copy for A2); mbarriers.
+enum { FEA6_L_V = 0, FEA6_L_VB = 1, FEA6_L_GU = 2, FEA6_L_GUB = 3, FEA6_L_GW = 4, FEA6_L_GWB = 5, FEA6_L_LW = 6,
+       FEA6_L_LWB = 7, FEA6_L_BARS = 10, FEA6_L_TOTAL = 11 };
 __host__ __device__ inline void fea6_smem_layout(int32_t* L, int e_max, int p, int do_m, int do_c) {
     const int T = fea_T(p), np = fea_np(p), nqp = 4 * fea_nk(fea_nq_native(p));
     const int ls = fea6_lstride(e_max), vs = fea6_vstride(e_max);
@@ -328,13 +332,11 @@ __host__ __device__ inline void fea6_smem_layout(int32_t* L, int e_max, int p, i
     L[FEA6_L_V] = o; o += 2 * L[FEA6_L_VB];
     L[FEA6_L_GUB] = fea_align(8 * np * ls, 128);
     L[FEA6_L_GU] = o; o += 2 * L[FEA6_L_GUB];
-    L[FEA6_L_GXB] = fea_align(16 * 3 * e_max, 128);
-    L[FEA6_L_GX] = o; o += 2 * L[FEA6_L_GXB];
-    L[FEA6_L_LAMB] = fea_align(8 * nqp * ls, 128);
-    L[FEA6_L_LAM] = o; o += 2 * L[FEA6_L_LAMB];
-    L[FEA6_L_WB] = fea_align(8 * 3 * e_max, 128);
-    L[FEA6_L_W] = o; o += 2 * L[FEA6_L_WB];
-    L[FEA6_L_BARS] = o; o += 8 * 8;
+    L[FEA6_L_GWB] = fea_align(8 * 4 * e_max, 128);
+    L[FEA6_L_GW] = o; o += 2 * L[FEA6_L_GWB];
+    L[FEA6_L_LWB] = fea_align(8 * (nqp * ls + 3 * e_max), 128);
+    L[FEA6_L_LW] = o; o += 3 * L[FEA6_L_LWB];  // three Lambda / W buffers (A1 runs two blocks ahead)
+    L[FEA6_L_BARS] = o; o += 14 * 8;
     L[FEA6_L_TOTAL] = o;
 }
 int fea_launch_reassemble6(const FeaKParams& prm, int order, int smem_bytes, int grid, void* stream);

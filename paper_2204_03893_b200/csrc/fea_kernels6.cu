@@ -39,8 +39,21 @@ __device__ __forceinline__ uint32_t ldg_u32(const uint32_t* p) {
     return v;
 }
 __device__ __forceinline__ void named_sync(int id, int n) { asm volatile("bar.sync %0, %1;" ::"r"(id), "r"(n) : "memory"); }
+// one arrival per warp: __syncwarp orders the warp's shared-memory writes before lane 0's
+// (release) arrive, so a waiter (acquire) sees all of them
+__device__ __forceinline__ void warp_arrive(uint64_t* bar, int lane) {
+    __syncwarp();
+    if (lane == 0) mbar_arrive(bar);
+}
 
-template <int P, bool DO_M, bool DO_C>
+// per-role cycle split (FEA_DEBUG_TIMING): a separate DIAG instantiation of the kernel, launched
+// only when diagnostics are requested; lane 0 of every warp adds its cycles per phase to
+// prm.dbg[base + k].  The production instantiation (DIAG = false) contains none of it.
+#define T6_DECL unsigned long long t6acc[8] = {0, 0, 0, 0, 0, 0, 0, 0}, t6c = DIAG ? clock64() : 0;
+#define T6_TICK(k) if constexpr (DIAG) { const unsigned long long n_ = clock64(); t6acc[k] += n_ - t6c; t6c = n_; }
+#define T6_FLUSH(base) if constexpr (DIAG) { if (prm.dbg && lane == 0) for (int k_ = 0; k_ < 8; ++k_) atomicAdd(prm.dbg + (base) + k_, t6acc[k_]); }
+
+template <int P, bool DO_M, bool DO_C, bool DIAG>
 __global__ void __launch_bounds__(fea6_threads(P), 1) k_reassemble6(const __grid_constant__ FeaKParams prm) {
     constexpr int NP = fea_np(P), T = fea_T(P), NTT = fea_ntt(P);
     constexpr int NQ = fea_nq_native(P), NK = fea_nk(NQ), NQP = 4 * NK;
@@ -57,21 +70,26 @@ __global__ void __launch_bounds__(fea6_threads(P), 1) k_reassemble6(const __grid
     extern __shared__ __align__(128) uint8_t smem[];
     auto sV = [&](int b) { return smem + prm.lay[FEA6_L_V] + b * prm.lay[FEA6_L_VB]; };
     auto sGU = [&](int b) { return reinterpret_cast<double*>(smem + prm.lay[FEA6_L_GU] + b * prm.lay[FEA6_L_GUB]); };
-    auto sGX = [&](int b) { return reinterpret_cast<double2*>(smem + prm.lay[FEA6_L_GX] + b * prm.lay[FEA6_L_GXB]); };
-    auto sLam = [&](int b) { return reinterpret_cast<double*>(smem + prm.lay[FEA6_L_LAM] + b * prm.lay[FEA6_L_LAMB]); };
-    auto sW = [&](int b) { return reinterpret_cast<double*>(smem + prm.lay[FEA6_L_W] + b * prm.lay[FEA6_L_WB]); };
+    auto sGW = [&](int b) { return reinterpret_cast<double*>(smem + prm.lay[FEA6_L_GW] + b * prm.lay[FEA6_L_GWB]); };
+    auto sLW = [&](int b) { return reinterpret_cast<double*>(smem + prm.lay[FEA6_L_LW] + b * prm.lay[FEA6_L_LWB]); };
     uint64_t* bars = reinterpret_cast<uint64_t*>(smem + prm.lay[FEA6_L_BARS]);
-    uint64_t* gat_full = bars;      // [2] 32 producer lanes (cp.async completion)
-    uint64_t* gat_free = bars + 2;  // [2] 1 arrival: the A warps are done with the gather stage
-    uint64_t* v_full = bars + 4;    // [2] NA * 32 arrivals: V of the buffer's block stored
-    uint64_t* v_free = bars + 6;    // [2] NB * 32 arrivals: phase B of the buffer's block done
+    uint64_t* gat_full = bars;       // [2] producer: 32 cp.async completions + 32 arrivals (geometry)
+    uint64_t* gat_free = bars + 2;   // [2] NB * 32: A1 of the stage's block done
+    uint64_t* v_full = bars + 4;     // [2] NA * 32: V of the buffer's block stored
+    uint64_t* v_free = bars + 6;     // [2] NB * 32: phase B of the buffer's block done
+    uint64_t* lam_full = bars + 8;   // [3] NB * 32: Lambda / W of the buffer's block stored
+    uint64_t* lam_free = bars + 11;  // [3] NA * 32: A2 of the buffer's block done reading it
 
     if (tid == 0) {
         for (int b = 0; b < 2; ++b) {
-            mbar_init(&gat_full[b], 32);
-            mbar_init(&gat_free[b], 1);
-            mbar_init(&v_full[b], NA * 32);
-            mbar_init(&v_free[b], NB * 32);
+            mbar_init(&gat_full[b], 33);  // 32 lanes' cp.async completions + the geometry stores
+            mbar_init(&gat_free[b], NB);
+            mbar_init(&v_full[b], NA);
+            mbar_init(&v_free[b], NB);
+        }
+        for (int b = 0; b < 3; ++b) {
+            mbar_init(&lam_full[b], NB);
+            mbar_init(&lam_free[b], NA);
         }
         fence_mbar_init();
     }
@@ -97,32 +115,50 @@ __global__ void __launch_bounds__(fea6_threads(P), 1) k_reassemble6(const __grid
         };
         if (lane == 0)
             for (int k = 0; k < 2 && k < nb; ++k) prefetch_blk(k);
+        T6_DECL
         for (int j = 0; j < nb; ++j) {
             const int g = j & 1;
             if (lane == 0 && j + 2 < nb) prefetch_blk(j + 2);
+            T6_TICK(1)
             if (j >= 2) mbar_wait(&gat_free[g], (uint32_t)(((j >> 1) - 1) & 1));
+            const int l3 = j % 3;
+            if (j >= 3) mbar_wait(&lam_free[l3], (uint32_t)(((j / 3) - 1) & 1));  // W goes to LW[j % 3]
+            T6_TICK(0)
             const FeaBlock* B = prm.blocks + b0 + j * G;
             const int nE = __ldg(&B->nE), nEp = fea_pad4(nE);
             const int32_t* gd = prm.dofs + __ldg(&B->dof_off);
             double* gu = sGU(g);
-            double2* gx = sGX(g);
+            double* gw = sGW(g);
+            double* W = sLW(l3) + NQP * ls;
             for (int le = lane; le < nE; le += 32) {
                 int32_t d[NP];
 #pragma unroll
                 for (int i = 0; i < NP; ++i) d[i] = ldg_s32(gd + i * nEp + le);
 #pragma unroll
                 for (int i = 0; i < NP; ++i) cp_async8(gu + i * ls + le, prm.u + d[i]);
-#pragma unroll
-                for (int v = 0; v < 3; ++v) cp_async16(gx + v * e_max + le, prm.xy + d[v]);
+                // element geometry once per element: b_e = |det B_e|, vec A_e
+                const double2 a = ldg_f64x2(prm.xy + d[0]), b = ldg_f64x2(prm.xy + d[1]), c = ldg_f64x2(prm.xy + d[2]);
+                const double B00 = b.x - a.x, B10 = b.y - a.y, B01 = c.x - a.x, B11 = c.y - a.y;
+                const double det = B00 * B11 - B01 * B10;
+                const double inv = 1.0 / (det * det);  // det(B^T B) = det(B)^2
+                gw[le] = fabs(det);
+                W[le] = (B01 * B01 + B11 * B11) * inv;
+                W[e_max + le] = (B00 * B00 + B10 * B10) * inv;
+                W[2 * e_max + le] = -(B00 * B01 + B10 * B11) * inv;
             }
-            cp_async_mbar_arrive(&gat_full[g]);
+            for (int le = nE + lane; le < ((nE + 7) & ~7); le += 32)  // padding columns of the last tile
+                W[le] = W[e_max + le] = W[2 * e_max + le] = 0.0;
+            cp_async_mbar_arrive(&gat_full[g]);  // (noinc) counts when this lane's gathers land
+            warp_arrive(&gat_full[g], lane);     // the geometry stores
+            T6_TICK(1)
         }
         asm volatile("cp.async.wait_all;" ::: "memory");
+        T6_FLUSH(16)
         return;
     }
 
     if (warp < NA) {
-        // ------------------------------------------------------------------ A warps
+        // ------------------------------------------------------------------ A warps: A2
         const int g8 = lane >> 2, cq = lane & 3;
         double afr[RT][4][NK];  // this warp's row tiles warp, warp + NA, ... of Q_f (f = m, A00, A11, A01)
 #pragma unroll
@@ -135,56 +171,21 @@ __global__ void __launch_bounds__(fea6_threads(P), 1) k_reassemble6(const __grid
                     afr[r][f][kk] = (f == 0 ? DO_M : DO_C) && tt < NTT
                                         ? __ldg(prm.qfrag + ((f * NTT + tt) * NK + kk) * 32 + lane) : 0.0;
                 }
-        const double* pfrag = prm.qfrag + 4 * NTT * NK * 32;  // Phi^T A-fragments [MT][KT][32]
-        const double* cPhi = prm.ctab;
-        const double* cW = prm.ctab + oW;
-        const FeaCoef& cf = DO_M ? prm.coef_m : prm.coef_c;  // one coefficient (distinct ones: two passes)
-        (void)cPhi;
-
+        T6_DECL
+        int nE_n = nb > 0 ? ldg_s32(&prm.blocks[b0].nE) : 0;  // one block ahead (L2 latency; asm volatile: issued here)
         for (int j = 0; j < nb; ++j) {
             const int g = j & 1;
-            const int nE = __ldg(&prm.blocks[b0 + j * G].nE);
+            const int nE = nE_n;
+            if (j + 1 < nb) nE_n = ldg_s32(&prm.blocks[b0 + (j + 1) * G].nE);
             const int net = (nE + 7) >> 3;
-            double* Lam = sLam(g);
-            double* W = sW(g);
-            // ---- A1: U = Phi^T U_e on DMMA, epilogue Lambda_qe = w_q b_e k(u_qe), W_e = vec A_e
-            mbar_wait(&gat_full[g], (uint32_t)((j >> 1) & 1));
-            {
-                const double* gU = sGU(g);
-                const double2* gX = sGX(g);
-                for (int un = warp; un < MT * net; un += NA) {
-                    const int mt = un % MT, et = un / MT;
-                    double u0 = 0.0, u1 = 0.0;
-#pragma unroll
-                    for (int kt = 0; kt < KT; ++kt) {
-                        const int i = kt * 4 + cq;
-                        const double b = i < NP ? gU[i * ls + et * 8 + g8] : 0.0;
-                        dmma(u0, u1, __ldg(pfrag + (mt * KT + kt) * 32 + lane), b);
-                    }
-                    const int q = mt * 8 + g8, le0 = et * 8 + 2 * cq;
-                    double d0 = 0.0, d1 = 0.0, w00 = 0.0, w01 = 0.0, w10 = 0.0, w11 = 0.0, w20 = 0.0, w21 = 0.0;
-                    if (le0 < nE) geometry(gX, e_max, le0, d0, w00, w10, w20);
-                    if (le0 + 1 < nE) geometry(gX, e_max, le0 + 1, d1, w01, w11, w21);
-                    if (mt == 0 && g8 == 0) {
-                        *reinterpret_cast<double2*>(W + le0) = make_double2(w00, w01);
-                        *reinterpret_cast<double2*>(W + e_max + le0) = make_double2(w10, w11);
-                        *reinterpret_cast<double2*>(W + 2 * e_max + le0) = make_double2(w20, w21);
-                    }
-                    if (q < NQP) {
-                        double l0 = 0.0, l1 = 0.0;
-                        if (q < NQ) {
-                            const double w = cW[q];
-                            if (le0 < nE) l0 = w * d0 * keval(cf, u0);
-                            if (le0 + 1 < nE) l1 = w * d1 * keval(cf, u1);
-                        }
-                        *reinterpret_cast<double2*>(Lam + q * ls + le0) = make_double2(l0, l1);
-                    }
-                }
-            }
-            named_sync(1, NA * 32);  // Lambda / W of block j complete; every A warp is past A2(j - 1)
-            if (tid == 0) mbar_arrive(&gat_free[g]);
-            // ---- A2: V = Q Lambda on DMMA into V buffer g
+            const int l3 = j % 3;
+            const double* Lam = sLW(l3);
+            const double* W = Lam + NQP * ls;
+            T6_TICK(5)
+            mbar_wait(&lam_full[l3], (uint32_t)((j / 3) & 1));
+            T6_TICK(0)
             if (j >= 2) mbar_wait(&v_free[g], (uint32_t)(((j >> 1) - 1) & 1));
+            T6_TICK(3)
             uint8_t* Vb = sV(g);
             for (int et = 0; et < net; ++et) {
                 const int col = et * 8 + g8, le0 = et * 8 + 2 * cq;
@@ -227,32 +228,116 @@ __global__ void __launch_bounds__(fea6_threads(P), 1) k_reassemble6(const __grid
                     }
                 }
             }
-            mbar_arrive(&v_full[g]);
+            T6_TICK(4)
+            __syncwarp();
+            if (lane == 0) {
+                mbar_arrive(&lam_free[l3]);
+                mbar_arrive(&v_full[g]);
+            }
         }
+        T6_FLUSH(0)
         return;
     }
 
-    // ------------------------------------------------------------------ B warps
+    // ------------------------------------------------------------------ B warps: A1(j), then B(j - 2)
+    // (A1 runs two blocks ahead of phase B and one to two ahead of A2: three Lambda buffers).  With
+    // nearly all shared memory in use the L1 holds ~1 KB, so every global read is an L2 round trip:
+    // the next phase B's descriptor and first items are loaded right after the current one.
     {
         const int bt = tid - NA * 32, bw = bt >> 5;
-        constexpr int U = 8;  // class-A chunks per round; two rounds of item loads in flight per lane
-        for (int j = 0; j < nb; ++j) {
-            const int g = j & 1;
-            const FeaBlock* B = prm.blocks + b0 + j * G;
-            const int nslots = __ldg(&B->nslots), ncls = __ldg(&B->ncls);
-            const int64_t slot0 = __ldg(&B->slot0);
-            const uint8_t* rec = prm.records + __ldg(&B->rec_off);
+        const int g8 = lane >> 2, cq = lane & 3;
+        const double* cW = prm.ctab + oW;
+        const FeaCoef& cf = DO_M ? prm.coef_m : prm.coef_c;  // one coefficient (distinct ones: two passes)
+        double pf[MT][KT];  // Phi^T A-fragments (A1 interpolation on DMMA)
+#pragma unroll
+        for (int mt = 0; mt < MT; ++mt)
+#pragma unroll
+            for (int kt = 0; kt < KT; ++kt) pf[mt][kt] = __ldg(prm.qfrag + 4 * NTT * NK * 32 + (mt * KT + kt) * 32 + lane);
+        // phase B: warp bw takes the 32-slot chunks bw, bw + NB, ... (U per round, two rounds of item
+        // loads in flight per lane)
+        constexpr int U = 8;
+        int nslots = 0, ncls = 0, rB = 0, nch = 0;
+        int64_t slot0 = 0;
+        const uint8_t* rec = nullptr;
+        uint32_t wa[U], wb[U];
+        uint4 ib = make_uint4(0, 0, 0, 0);
+        auto loadA = [&](uint32_t (&w)[U], int c0) {
             const uint32_t* ia = reinterpret_cast<const uint32_t*>(rec);
-            const int nch = (nslots + 31) >> 5;
+#pragma unroll
+            for (int u = 0; u < U; ++u) {
+                const int ch = c0 + u * NB;
+                w[u] = ch < nch ? ldg_u32(ia + ch * 32 + lane) : 0xffffffffu;
+            }
+        };
+        auto prefetchB = [&](int jb) {  // descriptor, first two rounds, this thread's first class-B item
+            const FeaBlock* B = prm.blocks + b0 + jb * G;
+            nslots = __ldg(&B->nslots);
+            ncls = __ldg(&B->ncls);
+            rB = __ldg(&B->pad_);
+            slot0 = __ldg(&B->slot0);
+            rec = prm.records + __ldg(&B->rec_off);
+            nch = (nslots + 31) >> 5;
+            loadA(wa, bw);
+            loadA(wb, bw + U * NB);
+            if (bt < ncls)
+                ib = __ldg(reinterpret_cast<const uint4*>(rec + 4 * ((nslots + 31) & ~31) + (size_t)bt * rB));
+        };
+        int nE_a = nb > 0 ? ldg_s32(&prm.blocks[b0].nE) : 0;  // A1's block size, one block ahead
+        if (nb > 0) prefetchB(0);
+        T6_DECL
+        for (int j = 0; j < nb + 2; ++j) {
+            if (j < nb) {
+                // ---- A1(j): U = Phi^T U_e on DMMA, epilogue Lambda_qe = w_q b_e k(u_qe)
+                const int g = j & 1;
+                const int nE = nE_a;
+                if (j + 1 < nb) nE_a = ldg_s32(&prm.blocks[b0 + (j + 1) * G].nE);
+                const int net = (nE + 7) >> 3;
+                const int l3 = j % 3;
+                double* Lam = sLW(l3);
+                if (j >= 3) mbar_wait(&lam_free[l3], (uint32_t)(((j / 3) - 1) & 1));
+                T6_TICK(4)
+                mbar_wait(&gat_full[g], (uint32_t)((j >> 1) & 1));
+                T6_TICK(5)
+                const double* gU = sGU(g);
+                const double* gw = sGW(g);
+                for (int et = bw; et < net; et += NB) {  // one element tile, all m-tiles (independent chains)
+                    double uq[MT][2];
+#pragma unroll
+                    for (int mt = 0; mt < MT; ++mt) uq[mt][0] = uq[mt][1] = 0.0;
+#pragma unroll
+                    for (int kt = 0; kt < KT; ++kt) {
+                        const int i = kt * 4 + cq;
+                        const double b = i < NP ? gU[i * ls + et * 8 + g8] : 0.0;
+#pragma unroll
+                        for (int mt = 0; mt < MT; ++mt) dmma(uq[mt][0], uq[mt][1], pf[mt][kt], b);
+                    }
+                    const int le0 = et * 8 + 2 * cq;
+                    const bool v0 = le0 < nE, v1 = le0 + 1 < nE;
+                    const double d0 = v0 ? gw[le0] : 0.0, d1 = v1 ? gw[le0 + 1] : 0.0;
+#pragma unroll
+                    for (int mt = 0; mt < MT; ++mt) {
+                        const int q = mt * 8 + g8;
+                        double l0 = 0.0, l1 = 0.0;
+                        if (q < NQ) {
+                            const double w = cW[q];
+                            l0 = w * d0 * keval(cf, uq[mt][0]);
+                            l1 = w * d1 * keval(cf, uq[mt][1]);
+                        }
+                        if (q < NQP) *reinterpret_cast<double2*>(Lam + q * ls + le0) = make_double2(l0, l1);
+                    }
+                }
+                __syncwarp();
+                if (lane == 0) {
+                    mbar_arrive(&gat_free[g]);
+                    mbar_arrive(&lam_full[l3]);
+                }
+                T6_TICK(6)
+            }
+            if (j < 2) continue;
+            // ---- B(j - 2): every CSR slot of the block = sum of its contributors
+            const int jb = j - 2, g = jb & 1;
             double* om = DO_M ? prm.out_m + slot0 : nullptr;
             double* oc = DO_C ? prm.out_c + slot0 : nullptr;
-            auto load = [&](uint32_t (&w)[U], int c0) {
-#pragma unroll
-                for (int u = 0; u < U; ++u) {
-                    const int ch = c0 + u * NB;
-                    w[u] = ch < nch ? ldg_u32(ia + ch * 32 + lane) : 0xffffffffu;
-                }
-            };
             const uint8_t* Vb = sV(g);
             auto run = [&](const uint32_t (&w)[U], int c0) {
 #pragma unroll
@@ -262,50 +347,77 @@ __global__ void __launch_bounds__(fea6_threads(P), 1) k_reassemble6(const __grid
                     if (o0 != 0xffff) {
                         const int p = (c0 + u * NB) * 32 + lane;
                         if (IL) {
-                            const double2 v0 = reinterpret_cast<const double2*>(Vb)[o0];
-                            const double2 v1 = reinterpret_cast<const double2*>(Vb)[o1];
-                            om[p] = v0.x + v1.x;
-                            oc[p] = v0.y + v1.y;
+                            const double2 x0 = reinterpret_cast<const double2*>(Vb)[o0];
+                            const double2 x1 = reinterpret_cast<const double2*>(Vb)[o1];
+                            om[p] = x0.x + x1.x;
+                            oc[p] = x0.y + x1.y;
                         } else {
-                            const double s = reinterpret_cast<const double*>(Vb)[o0] + reinterpret_cast<const double*>(Vb)[o1];
-                            if (DO_M) om[p] = s;
-                            else oc[p] = s;
+                            const double sum = reinterpret_cast<const double*>(Vb)[o0] + reinterpret_cast<const double*>(Vb)[o1];
+                            if (DO_M) om[p] = sum;
+                            else oc[p] = sum;
                         }
                     }
                 }
             };
-            uint32_t wa[U], wb[U];
-            load(wa, bw);  // the first two rounds load before the wait on V
-            load(wb, bw + U * NB);
-            mbar_wait(&v_full[g], (uint32_t)((j >> 1) & 1));
+            T6_TICK(0)
+            mbar_wait(&v_full[g], (uint32_t)((jb >> 1) & 1));
+            T6_TICK(1)
             for (int c0 = bw; c0 < nch; c0 += 2 * U * NB) {
                 run(wa, c0);
-                load(wa, c0 + 2 * U * NB);
+                loadA(wa, c0 + 2 * U * NB);
                 run(wb, c0 + U * NB);
-                load(wb, c0 + 3 * U * NB);
+                loadA(wb, c0 + 3 * U * NB);
             }
-            if (ncls > 0) {  // class B: slots with more than two contributors
-                const double* V1 = reinterpret_cast<const double*>(Vb);
-                phase_b5<DO_M, DO_C, false, IL>(rec + 4 * ((nslots + 31) & ~31), ncls, V1, V1, om, oc, bt, NB * 32);
+            T6_TICK(2)
+            // class B (more than two contributors: vertex diagonals), one item per thread, summed in
+            // ascending library element order
+            for (int it = bt; it < ncls; it += NB * 32) {
+                const uint16_t* wrd = reinterpret_cast<const uint16_t*>(rec + 4 * ((nslots + 31) & ~31) + (size_t)it * rB);
+                const uint4 h = it == bt ? ib : __ldg(reinterpret_cast<const uint4*>(wrd));
+                const int sl = h.x & 0xffff, C = h.x >> 16;
+                double am = 0.0, ac = 0.0;
+                for (int q = 0; q < C; ++q) {
+                    const uint32_t hw = q < 2 ? h.y : q < 4 ? h.z : h.w;  // no local-memory indexing
+                    const int o = q < 6 ? (int)((hw >> (16 * (q & 1))) & 0xffff) : (int)__ldg(wrd + 2 + q);
+                    if (IL) {
+                        const double2 x = reinterpret_cast<const double2*>(Vb)[o];
+                        am += x.x;
+                        ac += x.y;
+                    } else {
+                        am += reinterpret_cast<const double*>(Vb)[o];
+                    }
+                }
+                if (IL) {
+                    om[sl] = am;
+                    oc[sl] = ac;
+                } else if (DO_M) {
+                    om[sl] = am;
+                } else {
+                    oc[sl] = am;
+                }
             }
-            mbar_arrive(&v_free[g]);
+            T6_TICK(3)
+            warp_arrive(&v_free[g], lane);
+            if (jb + 1 < nb) prefetchB(jb + 1);
+            T6_TICK(7)
         }
+        T6_FLUSH(8)
     }
 }
 
 using kfun_t = void (*)(const FeaKParams);
 
-template <int P>
+template <int P, bool DIAG>
 kfun_t pick6(int dm, int dc) {
-    if (dm && dc) return k_reassemble6<P, true, true>;
-    if (dm) return k_reassemble6<P, true, false>;
-    return k_reassemble6<P, false, true>;
+    if (dm && dc) return k_reassemble6<P, true, true, DIAG>;
+    if (dm) return k_reassemble6<P, true, false, DIAG>;
+    return k_reassemble6<P, false, true, DIAG>;
 }
 
-kfun_t select6(int order, int dm, int dc) {
+kfun_t select6(int order, int dm, int dc, bool diag) {
     switch (order) {
-        case 3: return pick6<3>(dm, dc);
-        case 4: return pick6<4>(dm, dc);
+        case 3: return diag ? pick6<3, true>(dm, dc) : pick6<3, false>(dm, dc);
+        case 4: return diag ? pick6<4, true>(dm, dc) : pick6<4, false>(dm, dc);
         default: return nullptr;
     }
 }
@@ -313,7 +425,7 @@ kfun_t select6(int order, int dm, int dc) {
 }  // namespace
 
 int fea_launch_reassemble6(const FeaKParams& prm, int order, int smem_bytes, int grid, void* stream) {
-    kfun_t kern = select6(order, prm.out_m != nullptr, prm.out_c != nullptr);
+    kfun_t kern = select6(order, prm.out_m != nullptr, prm.out_c != nullptr, prm.dbg != nullptr);
     if (!kern) return (int)cudaErrorInvalidValue;
     cudaError_t err = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, smem_bytes);
     if (err != cudaSuccess) return (int)err;
@@ -322,7 +434,7 @@ int fea_launch_reassemble6(const FeaKParams& prm, int order, int smem_bytes, int
 }
 
 int fea_kernel_occupancy6(int order, int dm, int dc, int smem_bytes, int* n, int* threads) {
-    kfun_t kern = select6(order, dm, dc);
+    kfun_t kern = select6(order, dm, dc, false);
     if (!kern) return (int)cudaErrorInvalidValue;
     *threads = fea6_threads(order);
     cudaError_t err = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, smem_bytes);
