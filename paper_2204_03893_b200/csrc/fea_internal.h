@@ -296,6 +296,12 @@ int fea_kernel_occupancy5(int order, int do_m, int do_c, int smem_bytes, int* ct
 // V is double-buffered so phase B of block j overlaps A2 of block j + 1; the block records stay in
 // global memory (L2-prefetched) and phase B reads them with coalesced loads, which frees the
 // shared memory for the second V buffer.
+// where A1 runs: 2 = on the A warps, in the middle of A2 of the previous block (P4: the contraction
+// dominates and the A warps' DMMA work hides A1's latency); 0 = on the phase-B warps, two blocks
+// ahead of their phase B (P3: measured faster, C3 1.51 vs 1.61 ms)
+#ifndef FEA6_A1MODE
+#define FEA6_A1MODE(p) ((p) == 4 ? 2 : 0)
+#endif
 #ifndef FEA6_NB
 #define FEA6_NB 7
 #endif

@@ -38,7 +38,6 @@ __device__ __forceinline__ uint32_t ldg_u32(const uint32_t* p) {
     asm volatile("ld.global.nc.u32 %0, [%1];" : "=r"(v) : "l"(p));
     return v;
 }
-__device__ __forceinline__ void named_sync(int id, int n) { asm volatile("bar.sync %0, %1;" ::"r"(id), "r"(n) : "memory"); }
 // one arrival per warp: __syncwarp orders the warp's shared-memory writes before lane 0's
 // (release) arrive, so a waiter (acquire) sees all of them
 __device__ __forceinline__ void warp_arrive(uint64_t* bar, int lane) {
@@ -83,12 +82,12 @@ __global__ void __launch_bounds__(fea6_threads(P), 1) k_reassemble6(const __grid
     if (tid == 0) {
         for (int b = 0; b < 2; ++b) {
             mbar_init(&gat_full[b], 33);  // 32 lanes' cp.async completions + the geometry stores
-            mbar_init(&gat_free[b], NB);
+            mbar_init(&gat_free[b], FEA6_A1MODE(P) == 2 ? NA : NB);
             mbar_init(&v_full[b], NA);
             mbar_init(&v_free[b], NB);
         }
         for (int b = 0; b < 3; ++b) {
-            mbar_init(&lam_full[b], NB);
+            mbar_init(&lam_full[b], FEA6_A1MODE(P) == 2 ? NA : NB);
             mbar_init(&lam_free[b], NA);
         }
         fence_mbar_init();
@@ -99,7 +98,6 @@ __global__ void __launch_bounds__(fea6_threads(P), 1) k_reassemble6(const __grid
         reinterpret_cast<double*>(sV(tid / 3))[k == 0 ? e_max : 2 * e_max + k - 1] = 0.0;
     }
     __syncthreads();
-
     if (warp == NA + NB) {
         // ------------------------------------------------------------------ producer
         auto prefetch_range = [&](const void* p, size_t bytes) {
@@ -157,6 +155,62 @@ __global__ void __launch_bounds__(fea6_threads(P), 1) k_reassemble6(const __grid
         return;
     }
 
+    // ------------------------------------------------------------------ A1 (warp aw of naw)
+    // A1(j): U = Phi^T U_e on DMMA, epilogue Lambda_qe = w_q b_e k(u_qe), into the
+    // Lambda buffer j % 3 (W_e came from the producer).  FEA6_A1MODE 2: the A warps run A1(j + 1)
+    // in the middle of A2(j) (its latency hides behind the other warps' DMMA work); 0: the B warps
+    // run A1(j) two blocks ahead of their phase B.
+    constexpr int A1MODE = FEA6_A1MODE(P);
+    const double* cW = prm.ctab + oW;
+    const FeaCoef& cf = DO_M ? prm.coef_m : prm.coef_c;  // one coefficient (distinct ones: two passes)
+    auto do_a1 = [&](int j, int aw, int naw, int nE) {
+        const int g8 = lane >> 2, cq = lane & 3;
+        const int g = j & 1;
+        const int net = (nE + 7) >> 3;
+        const int l3 = j % 3;
+        double* Lam = sLW(l3);
+        if (j >= 3) mbar_wait(&lam_free[l3], (uint32_t)(((j / 3) - 1) & 1));
+        if (aw < net) mbar_wait(&gat_full[g], (uint32_t)((j >> 1) & 1));
+        const double* gU = sGU(g);
+        const double* gw = sGW(g);
+        for (int et = aw; et < net; et += naw) {  // one element tile, all m-tiles (independent chains)
+            double pf[MT][KT];  // Phi^T A-fragments (L1 / L2)
+#pragma unroll
+            for (int mt = 0; mt < MT; ++mt)
+#pragma unroll
+                for (int kt = 0; kt < KT; ++kt) pf[mt][kt] = __ldg(prm.qfrag + 4 * NTT * NK * 32 + (mt * KT + kt) * 32 + lane);
+            double uq[MT][2];
+#pragma unroll
+            for (int mt = 0; mt < MT; ++mt) uq[mt][0] = uq[mt][1] = 0.0;
+#pragma unroll
+            for (int kt = 0; kt < KT; ++kt) {
+                const int i = kt * 4 + cq;
+                const double b = i < NP ? gU[i * ls + et * 8 + g8] : 0.0;
+#pragma unroll
+                for (int mt = 0; mt < MT; ++mt) dmma(uq[mt][0], uq[mt][1], pf[mt][kt], b);
+            }
+            const int le0 = et * 8 + 2 * cq;
+            const bool v0 = le0 < nE, v1 = le0 + 1 < nE;
+            const double d0 = v0 ? gw[le0] : 0.0, d1 = v1 ? gw[le0 + 1] : 0.0;
+#pragma unroll
+            for (int mt = 0; mt < MT; ++mt) {
+                const int q = mt * 8 + g8;
+                double l0 = 0.0, l1 = 0.0;
+                if (q < NQ) {
+                    const double w = cW[q];
+                    l0 = w * d0 * keval(cf, uq[mt][0]);
+                    l1 = w * d1 * keval(cf, uq[mt][1]);
+                }
+                if (q < NQP) *reinterpret_cast<double2*>(Lam + q * ls + le0) = make_double2(l0, l1);
+            }
+        }
+        __syncwarp();
+        if (lane == 0) {
+            mbar_arrive(&gat_free[g]);
+            mbar_arrive(&lam_full[l3]);
+        }
+    };
+
     if (warp < NA) {
         // ------------------------------------------------------------------ A warps: A2
         const int g8 = lane >> 2, cq = lane & 3;
@@ -173,6 +227,7 @@ __global__ void __launch_bounds__(fea6_threads(P), 1) k_reassemble6(const __grid
                 }
         T6_DECL
         int nE_n = nb > 0 ? ldg_s32(&prm.blocks[b0].nE) : 0;  // one block ahead (L2 latency; asm volatile: issued here)
+        if (A1MODE == 2 && nb > 0) do_a1(0, NA - 1 - warp, NA, nE_n);
         for (int j = 0; j < nb; ++j) {
             const int g = j & 1;
             const int nE = nE_n;
@@ -188,12 +243,14 @@ __global__ void __launch_bounds__(fea6_threads(P), 1) k_reassemble6(const __grid
             T6_TICK(3)
             uint8_t* Vb = sV(g);
             for (int et = 0; et < net; ++et) {
+                // (units to the last warps first: warp NA - 1 holds one row tile less)
+                if (A1MODE == 2 && et == (net >> 1) && j + 1 < nb) do_a1(j + 1, NA - 1 - warp, NA, nE_n);
                 const int col = et * 8 + g8, le0 = et * 8 + 2 * cq;
                 double bl[NK];
 #pragma unroll
                 for (int kk = 0; kk < NK; ++kk) bl[kk] = Lam[(kk * 4 + cq) * ls + col];
 #pragma unroll
-                for (int r = 0; r < RT; ++r) {
+                for (int r = 0; r < RT; ++r) {  // row tiles one after the other (fused: measured slower)
                     const int tt = warp + r * NA;
                     if (RT > 1 && tt >= NTT) continue;
                     double m0 = 0.0, m1 = 0.0, a0 = 0.0, a1 = 0.0, p0 = 0.0, p1 = 0.0, c0 = 0.0, c1 = 0.0;
@@ -239,20 +296,14 @@ __global__ void __launch_bounds__(fea6_threads(P), 1) k_reassemble6(const __grid
         return;
     }
 
-    // ------------------------------------------------------------------ B warps: A1(j), then B(j - 2)
+    // ------------------------------------------------------------------ B warps: [A1(j)], then B(j - LAG)
     // (A1 runs two blocks ahead of phase B and one to two ahead of A2: three Lambda buffers).  With
     // nearly all shared memory in use the L1 holds ~1 KB, so every global read is an L2 round trip:
     // the next phase B's descriptor and first items are loaded right after the current one.
     {
         const int bt = tid - NA * 32, bw = bt >> 5;
-        const int g8 = lane >> 2, cq = lane & 3;
-        const double* cW = prm.ctab + oW;
-        const FeaCoef& cf = DO_M ? prm.coef_m : prm.coef_c;  // one coefficient (distinct ones: two passes)
-        double pf[MT][KT];  // Phi^T A-fragments (A1 interpolation on DMMA)
-#pragma unroll
-        for (int mt = 0; mt < MT; ++mt)
-#pragma unroll
-            for (int kt = 0; kt < KT; ++kt) pf[mt][kt] = __ldg(prm.qfrag + 4 * NTT * NK * 32 + (mt * KT + kt) * 32 + lane);
+        constexpr int LAG = A1MODE == 2 ? 0 : 2;  // phase B of block j - LAG after A1(j) (B warps running A1)
+        int nE_a = nb > 0 ? ldg_s32(&prm.blocks[b0].nE) : 0;  // A1's block size, one block ahead
         // phase B: warp bw takes the 32-slot chunks bw, bw + NB, ... (U per round, two rounds of item
         // loads in flight per lane)
         constexpr int U = 8;
@@ -282,60 +333,18 @@ __global__ void __launch_bounds__(fea6_threads(P), 1) k_reassemble6(const __grid
             if (bt < ncls)
                 ib = __ldg(reinterpret_cast<const uint4*>(rec + 4 * ((nslots + 31) & ~31) + (size_t)bt * rB));
         };
-        int nE_a = nb > 0 ? ldg_s32(&prm.blocks[b0].nE) : 0;  // A1's block size, one block ahead
         if (nb > 0) prefetchB(0);
         T6_DECL
-        for (int j = 0; j < nb + 2; ++j) {
-            if (j < nb) {
-                // ---- A1(j): U = Phi^T U_e on DMMA, epilogue Lambda_qe = w_q b_e k(u_qe)
-                const int g = j & 1;
+        for (int j = 0; j < nb + LAG; ++j) {
+            if (A1MODE == 0 && j < nb) {
                 const int nE = nE_a;
                 if (j + 1 < nb) nE_a = ldg_s32(&prm.blocks[b0 + (j + 1) * G].nE);
-                const int net = (nE + 7) >> 3;
-                const int l3 = j % 3;
-                double* Lam = sLW(l3);
-                if (j >= 3) mbar_wait(&lam_free[l3], (uint32_t)(((j / 3) - 1) & 1));
-                T6_TICK(4)
-                mbar_wait(&gat_full[g], (uint32_t)((j >> 1) & 1));
-                T6_TICK(5)
-                const double* gU = sGU(g);
-                const double* gw = sGW(g);
-                for (int et = bw; et < net; et += NB) {  // one element tile, all m-tiles (independent chains)
-                    double uq[MT][2];
-#pragma unroll
-                    for (int mt = 0; mt < MT; ++mt) uq[mt][0] = uq[mt][1] = 0.0;
-#pragma unroll
-                    for (int kt = 0; kt < KT; ++kt) {
-                        const int i = kt * 4 + cq;
-                        const double b = i < NP ? gU[i * ls + et * 8 + g8] : 0.0;
-#pragma unroll
-                        for (int mt = 0; mt < MT; ++mt) dmma(uq[mt][0], uq[mt][1], pf[mt][kt], b);
-                    }
-                    const int le0 = et * 8 + 2 * cq;
-                    const bool v0 = le0 < nE, v1 = le0 + 1 < nE;
-                    const double d0 = v0 ? gw[le0] : 0.0, d1 = v1 ? gw[le0 + 1] : 0.0;
-#pragma unroll
-                    for (int mt = 0; mt < MT; ++mt) {
-                        const int q = mt * 8 + g8;
-                        double l0 = 0.0, l1 = 0.0;
-                        if (q < NQ) {
-                            const double w = cW[q];
-                            l0 = w * d0 * keval(cf, uq[mt][0]);
-                            l1 = w * d1 * keval(cf, uq[mt][1]);
-                        }
-                        if (q < NQP) *reinterpret_cast<double2*>(Lam + q * ls + le0) = make_double2(l0, l1);
-                    }
-                }
-                __syncwarp();
-                if (lane == 0) {
-                    mbar_arrive(&gat_free[g]);
-                    mbar_arrive(&lam_full[l3]);
-                }
+                do_a1(j, bw, NB, nE);
                 T6_TICK(6)
             }
-            if (j < 2) continue;
-            // ---- B(j - 2): every CSR slot of the block = sum of its contributors
-            const int jb = j - 2, g = jb & 1;
+            if (j < LAG) continue;
+            // ---- B(j - LAG): every CSR slot of the block = sum of its contributors
+            const int jb = j - LAG, g = jb & 1;
             double* om = DO_M ? prm.out_m + slot0 : nullptr;
             double* oc = DO_C ? prm.out_c + slot0 : nullptr;
             const uint8_t* Vb = sV(g);
