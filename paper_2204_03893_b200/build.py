@@ -50,7 +50,7 @@ def build(force: bool = False, verbose: bool = False) -> str:
             cmd = [NVCC, "-O3", "-std=c++17", *ARCH, "-lineinfo", "-Xcompiler", "-fPIC", *diag, *inc, "-c",
                    os.path.join(CSRC, src), "-o", obj]
         else:
-            cmd = ["g++", "-O3", "-std=c++17", "-fPIC", "-Wall", "-Wno-unused-function", "-pthread",
+            cmd = ["g++", "-O3", "-std=c++17", "-fPIC", "-Wall", "-Wno-unused-function", "-pthread", "-fopenmp",
                    "-I", "/usr/local/cuda/include", *inc, "-c", os.path.join(CSRC, src), "-o", obj]
         r = subprocess.run(cmd, capture_output=True, text=True)
         if r.returncode != 0:
@@ -64,7 +64,7 @@ def build(force: bool = False, verbose: bool = False) -> str:
     with open(stamp, "w") as f:
         f.write(defs_key)
     tmp = LIB + f".tmp{os.getpid()}"
-    cmd = [NVCC, "-shared", *ARCH, "-cudart", "static", "-o", tmp, *objs, "-ldl", "-lpthread"]
+    cmd = [NVCC, "-shared", *ARCH, "-cudart", "static", "-o", tmp, *objs, "-ldl", "-lpthread", "-lgomp"]
     r = subprocess.run(cmd, capture_output=True, text=True)
     if r.returncode != 0:
         raise RuntimeError(f"link failed: {' '.join(cmd)}\n{r.stdout}\n{r.stderr}")

@@ -5,10 +5,30 @@
 #pragma once
 #include <cuda_runtime.h>
 #include <cstdint>
+#include <cstdio>
 
 #include "fea_internal.h"
 
 namespace fea_dev {
+
+// Device-side bounds checks of the FEA_BOUNDS_CHECK build (FEA_BUILD_DEFS=-DFEA_BOUNDS_CHECK):
+// compute-sanitizer is not available on this pool, so the kernels check their own shared- and
+// global-memory indices (tools/sanitize_cases.py runs every kernel so built); a failed check
+// prints its site and traps.  The production build compiles them out.
+#ifdef FEA_BOUNDS_CHECK
+#define FEA_CHECK(cond)                                                                               \
+    do {                                                                                              \
+        if (!(cond)) {                                                                                \
+            printf("FEA_CHECK failed %s:%d: %s (block %d thread %d)\n", __FILE__, __LINE__, #cond,    \
+                   (int)blockIdx.x, (int)threadIdx.x);                                                \
+            __trap();                                                                                 \
+        }                                                                                             \
+    } while (0)
+#else
+#define FEA_CHECK(cond) \
+    do {                \
+    } while (0)
+#endif
 
 // ------------------------------------------------------------------ PTX helpers
 __device__ __forceinline__ uint32_t smem_u32(const void* p) { return (uint32_t)__cvta_generic_to_shared(p); }
@@ -180,6 +200,7 @@ __device__ __forceinline__ void items5(const uint8_t* __restrict__ base, int n, 
             for (int q = 0; q < C; ++q) {
                 const int raw = u16_of(w[u], 1 + q);
                 const int off = ORIENT ? (raw & 0x7fff) : raw;
+                FEA_CHECK(off < 32768);
                 if (IL) {
                     const double2 v = reinterpret_cast<const double2*>(sVm)[off];
                     vm[u][q] = v.x;

@@ -11,6 +11,8 @@
 
 #include <algorithm>
 #include <atomic>
+#include <chrono>
+#include <parallel/algorithm>  // __gnu_parallel::sort (OpenMP): the mesh-size sorts of the setup
 #include <cmath>
 #include <cstdarg>
 #include <cstdio>
@@ -55,6 +57,18 @@ NcclApi& nccl() {
     }
     return api;
 }
+
+// allocator that default-initialises (no zero fill): for the mesh-size plan arrays, which are
+// written completely right after their allocation
+template <typename T>
+struct dinit_alloc : std::allocator<T> {
+    template <typename U> struct rebind { using other = dinit_alloc<U>; };
+    using std::allocator<T>::allocator;
+    template <typename U> void construct(U* p) noexcept { ::new ((void*)p) U; }
+    template <typename U, typename... A> void construct(U* p, A&&... a) { ::new ((void*)p) U(std::forward<A>(a)...); }
+};
+template <typename T>
+using dvec = std::vector<T, dinit_alloc<T>>;
 
 template <typename T>
 void dfree(T*& p) {
@@ -103,7 +117,7 @@ struct fea_ctx_s {
     int plan_which = FEA_MASS | FEA_STIFF;
     int64_t row_begin = 0, n_rows = 0, nnz = 0, rows_per_rank = 0;
     std::vector<int64_t> row_ptr;
-    std::vector<int32_t> col_idx;
+    dvec<int32_t> col_idx;
     FeaBlock* d_blocks = nullptr;
     uint8_t* d_records = nullptr;
     int32_t* d_dofs = nullptr;  // v5: per-block element DOFs
@@ -211,6 +225,16 @@ struct fea_ctx_s {
         cudaError_t _e = (x);                                                                         \
         if (_e != cudaSuccess) return (ctx)->fail(FEA_E_CUDA, "%s: %s", #x, cudaGetErrorString(_e)); \
     } while (0)
+
+// FEA_PLAN_TIMING=1: the setup phases' wall times on stderr (diagnostics)
+static void ptime(const char* what) {
+    static const bool on = getenv("FEA_PLAN_TIMING") != nullptr;
+    if (!on) return;
+    static auto t0 = std::chrono::steady_clock::now();
+    const auto t = std::chrono::steady_clock::now();
+    fprintf(stderr, "[fea plan] %-28s %8.3f s\n", what, std::chrono::duration<double>(t - t0).count());
+    t0 = t;
+}
 
 // FEA_TUNE_TIMING: record timing event i of the current call on `st` (no-op when off)
 static fea_status tmark(fea_ctx c, int i, cudaStream_t st) {
@@ -602,6 +626,7 @@ fea_status fea_mesh_upload(fea_ctx c, int64_t n_vert, const double* vert_xy, int
     if (!c->host_only) cudaSetDevice(c->device);
     c->free_mesh();
 
+    ptime("mesh_upload start");
     // validation + DOF coordinates (user numbering), element by element
     std::vector<double> uxy(2 * n_dof, 0.0);
     std::vector<int64_t> first(n_dof, -1);
@@ -639,6 +664,7 @@ fea_status fea_mesh_upload(fea_ctx c, int64_t n_vert, const double* vert_xy, int
     for (int64_t d = 0; d < n_dof; ++d)
         if (first[d] < 0) return c->fail(FEA_E_MESH, "DOF %lld is not referenced by any element", (long long)d);
 
+    ptime("validation");
     // library DOF numbering
     std::vector<int64_t> lib2user(n_dof), user2lib(n_dof);
     std::iota(lib2user.begin(), lib2user.end(), 0);
@@ -655,10 +681,18 @@ fea_status fea_mesh_upload(fea_ctx c, int64_t n_vert, const double* vert_xy, int
             const int64_t a = blk * 65536, b = std::min<int64_t>(n_dof, a + 65536);
             for (int64_t d = a; d < b; ++d) key[d] = morton(uxy[2 * d], uxy[2 * d + 1], x0, y0, x1 - x0, y1 - y0);
         });
-        std::stable_sort(lib2user.begin(), lib2user.end(), [&](int64_t a, int64_t b) { return key[a] < key[b]; });
+        // (key, user id) pairs, sorted in parallel: the same order as a stable sort by key
+        std::vector<std::pair<uint64_t, int64_t>> kp(n_dof);
+        parallel_for((n_dof + 65535) / 65536, [&](int64_t blk) {
+            const int64_t a = blk * 65536, b = std::min<int64_t>(n_dof, a + 65536);
+            for (int64_t d = a; d < b; ++d) kp[d] = {key[d], d};
+        });
+        __gnu_parallel::sort(kp.begin(), kp.end());
+        for (int64_t d = 0; d < n_dof; ++d) lib2user[d] = kp[d].second;
     }
     for (int64_t l = 0; l < n_dof; ++l) user2lib[lib2user[l]] = l;
 
+    ptime("Morton DOF order");
     // library element order: by minimum library DOF, then user id
     std::vector<int32_t> emin(n_elem);
     for (int64_t e = 0; e < n_elem; ++e) {
@@ -668,8 +702,14 @@ fea_status fea_mesh_upload(fea_ctx c, int64_t n_vert, const double* vert_xy, int
     }
     std::vector<int64_t> el2u(n_elem);
     std::iota(el2u.begin(), el2u.end(), 0);
-    std::stable_sort(el2u.begin(), el2u.end(), [&](int64_t a, int64_t b) { return emin[a] < emin[b]; });
+    {  // (min DOF, user id) packed in 64 bits, sorted in parallel (= a stable sort by min DOF)
+        std::vector<uint64_t> ek(n_elem);
+        for (int64_t e = 0; e < n_elem; ++e) ek[e] = (uint64_t)(uint32_t)emin[e] << 32 | (uint64_t)e;
+        __gnu_parallel::sort(ek.begin(), ek.end());
+        for (int64_t e = 0; e < n_elem; ++e) el2u[e] = (int64_t)(ek[e] & 0xffffffffu);
+    }
 
+    ptime("element order");
     c->n_vert = n_vert;
     c->n_e = n_elem;
     c->n_dof = n_dof;
@@ -691,6 +731,7 @@ fea_status fea_mesh_upload(fea_ctx c, int64_t n_vert, const double* vert_xy, int
         c->have_mesh = true;
         return FEA_OK;
     }
+    ptime("library numbering");
     // device: DOF coordinates (vertex DOFs give B_e); the DOF map travels in the block records
     FEA_CUDA(c, cudaMalloc(&c->d_xy, n_dof * sizeof(double2)));
     FEA_CUDA(c, cudaMemcpy(c->d_xy, c->dxy.data(), n_dof * sizeof(double2), cudaMemcpyHostToDevice));
@@ -797,10 +838,10 @@ static std::vector<int32_t> bank_split_order(const uint16_t* off, int n, int C, 
 // nonsymmetric element matrices (the tensor contraction C o2 v).
 struct PlanData {
     std::vector<FeaBlock> blocks;
-    std::vector<uint8_t> records;
-    std::vector<int32_t> dofs;
+    dvec<uint8_t> records;
+    dvec<int32_t> dofs;
     std::vector<int64_t> row_ptr;
-    std::vector<int32_t> col_idx;
+    dvec<int32_t> col_idx;
     int64_t nnz = 0, rec_max = 16, visits = 0, owned = 0, ncon = 0, rbytes = 0;
 };
 
@@ -839,6 +880,7 @@ static fea_status build_blocks(fea_ctx c, bool v5, bool orient, int64_t e_max, i
     if (orient && (int64_t)T * EM >= 32768)
         return c->fail(FEA_E_UNSUPPORTED, "tensor plan: V offsets need 15 bits");
 
+    ptime("plan: incidence");
     // ---- greedy row blocks: elements <= e_max and record upper bound <= rec_budget
     // record upper bound: slots <= entries, so counts + contrib + chunks <= 3 entries + entries/8
     std::vector<int64_t> brow;
@@ -866,6 +908,7 @@ static fea_status build_blocks(fea_ctx c, bool v5, bool orient, int64_t e_max, i
     const int64_t nb = (int64_t)brow.size();
     brow.push_back(nr);
 
+    ptime("plan: row blocks");
     // ---- per block: element set, (row, col) records sorted -> slots, contributors, record
     struct BOut {
         std::vector<int32_t> rownnz, cols, dofs;
@@ -895,21 +938,35 @@ static fea_status build_blocks(fea_ctx c, bool v5, bool orient, int64_t e_max, i
         }
         struct Rec { int32_t row, col, le, t; };  // t: V row (| 0x10000 if orient and i > j: Vdn)
         std::vector<Rec> recs;
-        for (int64_t le = 0; le < (int64_t)E.size(); ++le) {
-            const int32_t* d = &c->ed[(size_t)E[le] * np];
-            for (int i = 0; i < np; ++i) {
-                if (d[i] < ga || d[i] >= gb) continue;
-                for (int j = 0; j < np; ++j)
-                    // tensor plans (orient): V row fea_trow (off-diagonal pairs first), flag i > j
-                    recs.push_back({d[i], d[j], (int32_t)le,
-                                    orient ? fea_trow(np, std::min(i, j), std::max(i, j)) | (i > j ? 0x10000 : 0)
-                                           : tri_index(np, std::min(i, j), std::max(i, j))});
+        recs.reserve((size_t)(iptr[rb] - iptr[ra]) * np);
+        // row by row (the incident elements in ascending library element order), each row's
+        // records sorted by column -- stable, so a slot's contributors stay in ascending le
+        for (int64_t r = ra; r < rb; ++r) {
+            const size_t r0 = recs.size();
+            for (int64_t k = iptr[r]; k < iptr[r + 1]; ++k) {
+                const int32_t e = inc[k];
+                const int32_t le = (int32_t)(std::lower_bound(E.begin(), E.end(), e) - E.begin());
+                const int32_t* d = &c->ed[(size_t)e * np];
+                for (int i = 0; i < np; ++i) {
+                    if (d[i] != R0 + r) continue;
+                    for (int j = 0; j < np; ++j)
+                        // tensor plans (orient): V row fea_trow (off-diagonal pairs first), flag i > j
+                        recs.push_back({d[i], d[j], le,
+                                        orient ? fea_trow(np, std::min(i, j), std::max(i, j)) | (i > j ? 0x10000 : 0)
+                                               : tri_index(np, std::min(i, j), std::max(i, j))});
+                }
+            }
+            // stable insertion sort by column (a row has a few dozen records; no allocation)
+            for (size_t a = r0 + 1; a < recs.size(); ++a) {
+                const Rec x = recs[a];
+                size_t q = a;
+                while (q > r0 && recs[q - 1].col > x.col) {
+                    recs[q] = recs[q - 1];
+                    --q;
+                }
+                recs[q] = x;
             }
         }
-        // stable: within a (row, col) slot the contributors stay in ascending le (= library element)
-        std::stable_sort(recs.begin(), recs.end(), [](const Rec& x, const Rec& y) {
-            return x.row != y.row ? x.row < y.row : x.col < y.col;
-        });
         // slots (row, col) in CSR order, each with its contributors in ascending le
         std::vector<int32_t> sstart, scount;  // per slot: first record, count
         o.rownnz.assign(rb - ra, 0);
@@ -924,42 +981,6 @@ static fea_status build_blocks(fea_ctx c, bool v5, bool orient, int64_t e_max, i
             k = k2;
         }
         const int32_t nslot = (int32_t)sstart.size();
-        // items: slots sorted by (count, slot); classes of equal count
-        std::vector<int32_t> order(nslot);
-        std::iota(order.begin(), order.end(), 0);
-        // v5: single-contributor slots join the two-contributor class with a second read of a
-        // zero cell (V row 0, column e_max: never written by the kernel, zeroed at its start), so
-        // each warp's stores of that class cover denser slot ranges (C2: ~16 -> ~9 sectors per
-        // store instruction); the sum is unchanged (x + 0.0).
-        bool pad1 = v5 && !v6 && !orient && c->tune_pad1 && EM > e_max;
-        if (pad1) {  // only where the padded record still fits the block's record budget
-            std::map<int32_t, int32_t> n_by;
-            for (int32_t sl = 0; sl < nslot; ++sl) n_by[scount[sl] == 1 ? 2 : scount[sl]]++;
-            int64_t sz = 16 * (int64_t)n_by.size();
-            for (const auto& kv : n_by) sz += fea_pad16(kv.second * fea5_item_bytes(kv.first));
-            pad1 = sz <= rec_budget;
-        }
-        auto ecount = [&](int32_t sl) { return pad1 && scount[sl] == 1 ? 2 : scount[sl]; };
-        std::stable_sort(order.begin(), order.end(), [&](int32_t x, int32_t y) { return ecount(x) < ecount(y); });
-        std::vector<int32_t> cls;
-        std::vector<uint16_t> items(nslot), contrib;
-        contrib.reserve(recs.size());
-        for (int32_t it = 0; it < nslot; ++it) {
-            const int32_t sl = order[it];
-            if (it == 0 || ecount(sl) != ecount(order[it - 1])) {
-                cls.push_back(ecount(sl));
-                cls.push_back(it);
-                cls.push_back((int32_t)contrib.size());
-            }
-            if (sl > 65535) {
-                o.err = "more than 65536 slots in one block";
-                return;
-            }
-            items[it] = (uint16_t)sl;
-            for (int32_t m = sstart[sl]; m < sstart[sl] + scount[sl]; ++m)
-                contrib.push_back((uint16_t)(((recs[m].t & 0xffff) * EM + recs[m].le) | ((recs[m].t >> 16) << 15)));
-            if (ecount(sl) != scount[sl]) contrib.push_back((uint16_t)e_max);  // the zero cell
-        }
         if (v6) {  // kernel v6 record: class A in slot order, class B (> 2 contributors) as flat items
             if (nslot > 65535) {
                 o.err = "more than 65535 slots in one block";
@@ -1016,6 +1037,42 @@ static fea_status build_blocks(fea_ctx c, bool v5, bool orient, int64_t e_max, i
             for (int64_t le = E.size(); le < nEp; ++le)
                 for (int i = 0; i < np; ++i) o.dofs[i * nEp + le] = o.dofs[i * nEp];
             return;
+        }
+        // items: slots sorted by (count, slot); classes of equal count
+        std::vector<int32_t> order(nslot);
+        std::iota(order.begin(), order.end(), 0);
+        // v5: single-contributor slots join the two-contributor class with a second read of a
+        // zero cell (V row 0, column e_max: never written by the kernel, zeroed at its start), so
+        // each warp's stores of that class cover denser slot ranges (C2: ~16 -> ~9 sectors per
+        // store instruction); the sum is unchanged (x + 0.0).
+        bool pad1 = v5 && !v6 && !orient && c->tune_pad1 && EM > e_max;
+        if (pad1) {  // only where the padded record still fits the block's record budget
+            std::map<int32_t, int32_t> n_by;
+            for (int32_t sl = 0; sl < nslot; ++sl) n_by[scount[sl] == 1 ? 2 : scount[sl]]++;
+            int64_t sz = 16 * (int64_t)n_by.size();
+            for (const auto& kv : n_by) sz += fea_pad16(kv.second * fea5_item_bytes(kv.first));
+            pad1 = sz <= rec_budget;
+        }
+        auto ecount = [&](int32_t sl) { return pad1 && scount[sl] == 1 ? 2 : scount[sl]; };
+        std::stable_sort(order.begin(), order.end(), [&](int32_t x, int32_t y) { return ecount(x) < ecount(y); });
+        std::vector<int32_t> cls;
+        std::vector<uint16_t> items(nslot), contrib;
+        contrib.reserve(recs.size());
+        for (int32_t it = 0; it < nslot; ++it) {
+            const int32_t sl = order[it];
+            if (it == 0 || ecount(sl) != ecount(order[it - 1])) {
+                cls.push_back(ecount(sl));
+                cls.push_back(it);
+                cls.push_back((int32_t)contrib.size());
+            }
+            if (sl > 65535) {
+                o.err = "more than 65536 slots in one block";
+                return;
+            }
+            items[it] = (uint16_t)sl;
+            for (int32_t m = sstart[sl]; m < sstart[sl] + scount[sl]; ++m)
+                contrib.push_back((uint16_t)(((recs[m].t & 0xffff) * EM + recs[m].le) | ((recs[m].t >> 16) << 15)));
+            if (ecount(sl) != scount[sl]) contrib.push_back((uint16_t)e_max);  // the zero cell
         }
         FeaBlock& F = o.fb;
         F.nslots = nslot;
@@ -1084,6 +1141,7 @@ static fea_status build_blocks(fea_ctx c, bool v5, bool orient, int64_t e_max, i
     for (auto& o : bo)
         if (!o.err.empty()) return c->fail(FEA_E_UNSUPPORTED, "plan: %s", o.err.c_str());
 
+    ptime("plan: block records");
     // ---- concatenate
     std::vector<FeaBlock> blocks(nb);
     int64_t nnz = 0, rbytes = 0, ncon = 0, visits = 0, owned = 0, rec_max = 16, ndofs = 0;
@@ -1103,32 +1161,32 @@ static fea_status build_blocks(fea_ctx c, bool v5, bool orient, int64_t e_max, i
     }
     if (nnz >= (1ll << 31)) return c->fail(FEA_E_UNSUPPORTED, "nnz %lld >= 2^31 on one rank", (long long)nnz);
     std::vector<int64_t>& row_ptr = P.row_ptr;
-    std::vector<int32_t>& col_idx = P.col_idx;
+    auto& col_idx = P.col_idx;
     row_ptr.assign(nr + 1, 0);
-    col_idx.resize(nnz);
-    std::vector<uint8_t> records(std::max<int64_t>(rbytes, 16));
-    std::vector<int32_t> alldofs(std::max<int64_t>(ndofs, 4));
+    col_idx.resize(nnz);  // default-initialised (no zero fill): every element is written below
+    P.records.resize(std::max<int64_t>(rbytes, 16));
+    P.dofs.resize(std::max<int64_t>(ndofs, 4));
+    auto& records = P.records;
+    auto& alldofs = P.dofs;
     parallel_for(nb, [&](int64_t b) {
         const FeaBlock& B = blocks[b];
         std::copy(bo[b].dofs.begin(), bo[b].dofs.end(), alldofs.begin() + B.dof_off);
-        std::vector<int32_t>().swap(bo[b].dofs);
         std::copy(bo[b].cols.begin(), bo[b].cols.end(), col_idx.begin() + B.slot0);
         std::memcpy(records.data() + B.rec_off, bo[b].rec.data(), B.rec_bytes);
         if (!v5) reinterpret_cast<FeaRecHdr4*>(records.data() + B.rec_off)->slot0 = B.slot0;
         for (int64_t r = brow[b]; r < brow[b + 1]; ++r) row_ptr[r + 1] = bo[b].rownnz[r - brow[b]];
-        std::vector<uint8_t>().swap(bo[b].rec);
+        bo[b] = BOut();  // the per-block buffers are released here, in parallel
     });
     for (int64_t r = 0; r < nr; ++r) row_ptr[r + 1] += row_ptr[r];
     bo.clear();
     P.blocks.swap(blocks);
-    P.records.swap(records);
-    P.dofs.swap(alldofs);
     P.nnz = nnz;
     P.rec_max = rec_max;
     P.visits = visits;
     P.owned = owned;
     P.ncon = ncon;
     P.rbytes = rbytes;
+    ptime("plan: concatenate");
     return FEA_OK;
 }
 
@@ -1220,8 +1278,8 @@ fea_status fea_build_pattern(fea_ctx c, int64_t* row_begin, int64_t* n_rows_loca
     c->row_ptr.swap(P.row_ptr);
     c->col_idx.swap(P.col_idx);
     std::vector<FeaBlock>& blocks = P.blocks;
-    std::vector<uint8_t>& records = P.records;
-    std::vector<int32_t>& alldofs = P.dofs;
+    auto& records = P.records;
+    auto& alldofs = P.dofs;
     const int64_t visits = P.visits, owned = P.owned, ncon = P.ncon, rbytes = P.rbytes;
     int32_t L[FEA_L_N];
     if (v6) fea6_smem_layout(L, (int)e_max, c->order, dm, dcm);
@@ -1305,6 +1363,7 @@ fea_status fea_build_pattern(fea_ctx c, int64_t* row_begin, int64_t* n_rows_loca
     c->grid = (int)std::min<int64_t>(std::max<int64_t>(nb, 1), (int64_t)occ * c->sm_count);
     // our kernels per fea_reassemble: the assembly, plus pack + unpack of the exchange (world > 1)
     c->launches_per_call = c->world > 1 ? 2 + (c->exchange == 0 ? 2 : 0) : 1;
+    ptime("plan: upload");
     c->have_plan = true;
     if (row_begin) *row_begin = R0;
     if (n_rows_local) *n_rows_local = nr;
@@ -1392,6 +1451,9 @@ static fea_status launch(fea_ctx c, const double* u, double* vm, double* vc, boo
     prm.nq = rule_c ? c->nq_c : c->nq;
     prm.same_coef = same_coef(c->coef_m, c->coef_c) ? 1 : 0;
     std::memcpy(prm.lay, c->lay, sizeof(prm.lay));
+    prm.n_dof = c->n_dof;
+    prm.n_slots = c->nnz;
+    prm.rec_size = c->record_bytes;
     // a single-matrix pass on a plan sized for the other matrix: its V region has size 0 in the
     // layout, so it takes the planned matrix's region (same size, same contributor offsets)
     // (kernel v6 has one V region either way: its single-matrix passes use it with 8-byte cells)
@@ -1730,6 +1792,7 @@ fea_status fea_assemble_tensor(fea_ctx c, const double* u_full, const double* v_
     prm.coef_m = c->coef_m;
     prm.coef_c = c->coef_c;
     prm.same_coef = same_coef(c->coef_m, c->coef_c) ? 1 : 0;
+    prm.n_dof = c->n_dof;
     if (prm.out_m || prm.out_c) {
         const int rc = fea_launch_tensor(prm, c->order, c->t_smem, c->t_grid, c->stream);
         if (rc != 0) return c->fail(FEA_E_CUDA, "k_tensor launch: %s", cudaGetErrorString((cudaError_t)rc));

@@ -178,6 +178,7 @@ struct FeaKParams {
     int32_t same_coef;        // mass and stiffness share k -> one Lambda
     int32_t dbg_mode;         // diagnostics only (FEA_DEBUG_MODE): 1 skip B stores, 2 skip B, 4 skip A2
     int32_t lay[FEA_L_N];     // shared-memory layout (byte offsets)
+    int64_t n_dof, n_slots, rec_size;  // extents, for the FEA_BOUNDS_CHECK build's device-side checks
     FeaCoef coef_m;
     FeaCoef coef_c;
     double ctab[FEA_CTAB_MAX];  // Phi [np][nq] at 0, w [nq] at pad2(np nq)
@@ -271,6 +272,7 @@ struct FeaTParams {
     const double* qfrag;  // k_tensor4: the rule's fragment buffer (Q_m at 0, R_d at fea_rfrag_off)
     int32_t nblocks, e_max, nq, kver;  // kver: 1 = k_tensor (lane per element), 4 = k_tensor4 (DMMA)
     int32_t same_coef, pad_;           // m == c: k_tensor4 evaluates the derivative once
+    int64_t n_dof;                     // extent, for the FEA_BOUNDS_CHECK build
     int32_t lay[FEA_LT_N];
     FeaCoef coef_m, coef_c;  // k' of these
 };

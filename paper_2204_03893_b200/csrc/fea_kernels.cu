@@ -100,6 +100,8 @@ __global__ void __launch_bounds__(fea_threads(P), fea_ctas(P)) k_reassemble(cons
             double2* gx = gXb(gs);
             for (int le = lane; le < blk.nE; le += 32) {
 #pragma unroll
+                for (int i = 0; i < NP; ++i) FEA_CHECK(gd[i * nEp + le] >= 0 && gd[i * nEp + le] < prm.n_dof);
+#pragma unroll
                 for (int i = 0; i < NP; ++i) cp_async8(gu + i * ls + le, prm.u + gd[i * nEp + le]);
 #pragma unroll
                 for (int v = 0; v < 3; ++v) cp_async16(gx + v * e_max + le, prm.xy + gd[v * nEp + le]);

@@ -165,6 +165,8 @@ __global__ void __launch_bounds__(fea5_threads(P), 1) k_reassemble5(const __grid
         if (ls >= nb) return;
         if ((lu / NS) * 32 + lane < blk_of(ls).nE) {
 #pragma unroll
+            for (int i = 0; i < NP; ++i) FEA_CHECK(dof[i] >= 0 && dof[i] < prm.n_dof);
+#pragma unroll
             for (int i = 0; i < NP; ++i) g.u[i] = ldg_f64(prm.u + dof[i]);
 #pragma unroll
             for (int v = 0; v < 3; ++v) g.x[v] = ldg_f64x2(prm.xy + dof[v]);

@@ -125,6 +125,7 @@ __global__ void __launch_bounds__(fea6_threads(P), 1) k_reassemble6(const __grid
             const FeaBlock* B = prm.blocks + b0 + j * G;
             const int nE = __ldg(&B->nE), nEp = fea_pad4(nE);
             const int32_t* gd = prm.dofs + __ldg(&B->dof_off);
+            FEA_CHECK(nE >= 1 && nE <= e_max);
             double* gu = sGU(g);
             double* gw = sGW(g);
             double* W = sLW(l3) + NQP * ls;
@@ -132,6 +133,8 @@ __global__ void __launch_bounds__(fea6_threads(P), 1) k_reassemble6(const __grid
                 int32_t d[NP];
 #pragma unroll
                 for (int i = 0; i < NP; ++i) d[i] = ldg_s32(gd + i * nEp + le);
+#pragma unroll
+                for (int i = 0; i < NP; ++i) FEA_CHECK(d[i] >= 0 && d[i] < prm.n_dof);
 #pragma unroll
                 for (int i = 0; i < NP; ++i) cp_async8(gu + i * ls + le, prm.u + d[i]);
                 // element geometry once per element: b_e = |det B_e|, vec A_e
@@ -265,6 +268,7 @@ __global__ void __launch_bounds__(fea6_threads(P), 1) k_reassemble6(const __grid
                     }
                     const int t = tt * 8 + g8;
                     if (t < T) {
+                        FEA_CHECK(le0 + 1 < e_max + 1 && (t * vs + le0 + 1) * (IL ? 16 : 8) < prm.lay[FEA6_L_VB]);
                         double k0 = 0.0, k1 = 0.0;
                         if (DO_C) {
                             const double2 w0 = *reinterpret_cast<const double2*>(W + le0);
@@ -328,6 +332,8 @@ __global__ void __launch_bounds__(fea6_threads(P), 1) k_reassemble6(const __grid
             slot0 = __ldg(&B->slot0);
             rec = prm.records + __ldg(&B->rec_off);
             nch = (nslots + 31) >> 5;
+            FEA_CHECK(slot0 >= 0 && slot0 + nslots <= prm.n_slots && __ldg(&B->rec_off) + __ldg(&B->rec_bytes) <= prm.rec_size);
+            FEA_CHECK(4 * 32 * nch + (int64_t)ncls * rB <= __ldg(&B->rec_bytes));
             loadA(wa, bw);
             loadA(wb, bw + U * NB);
             if (bt < ncls)
@@ -355,6 +361,7 @@ __global__ void __launch_bounds__(fea6_threads(P), 1) k_reassemble6(const __grid
                     const int o0 = it & 0xffff, o1 = it >> 16;
                     if (o0 != 0xffff) {
                         const int p = (c0 + u * NB) * 32 + lane;
+                        FEA_CHECK(p < nslots && o0 < T * vs && o1 < T * vs);
                         if (IL) {
                             const double2 x0 = reinterpret_cast<const double2*>(Vb)[o0];
                             const double2 x1 = reinterpret_cast<const double2*>(Vb)[o1];
@@ -384,10 +391,12 @@ __global__ void __launch_bounds__(fea6_threads(P), 1) k_reassemble6(const __grid
                 const uint16_t* wrd = reinterpret_cast<const uint16_t*>(rec + 4 * ((nslots + 31) & ~31) + (size_t)it * rB);
                 const uint4 h = it == bt ? ib : __ldg(reinterpret_cast<const uint4*>(wrd));
                 const int sl = h.x & 0xffff, C = h.x >> 16;
+                FEA_CHECK(sl < nslots && C >= 3 && 2 * (C + 2) <= rB);
                 double am = 0.0, ac = 0.0;
                 for (int q = 0; q < C; ++q) {
                     const uint32_t hw = q < 2 ? h.y : q < 4 ? h.z : h.w;  // no local-memory indexing
                     const int o = q < 6 ? (int)((hw >> (16 * (q & 1))) & 0xffff) : (int)__ldg(wrd + 2 + q);
+                    FEA_CHECK(o < T * vs);
                     if (IL) {
                         const double2 x = reinterpret_cast<const double2*>(Vb)[o];
                         am += x.x;

@@ -75,6 +75,8 @@ __global__ void __launch_bounds__(FEA_T_WARPS * 32, 1) k_tensor(const __grid_con
 #pragma unroll
             for (int i = 0; i < NP; ++i) d[i] = prm.dofs[blk.dof_off + i * nEp + le];
 #pragma unroll
+            for (int i = 0; i < NP; ++i) FEA_CHECK(d[i] >= 0 && d[i] < prm.n_dof);
+#pragma unroll
             for (int i = 0; i < NP; ++i) {
                 ue[i] = __ldg(prm.u + d[i]);
                 ve[i] = __ldg(prm.v + d[i]);
@@ -239,6 +241,7 @@ __global__ void __launch_bounds__(fea_t4_threads(P, DO_M, DO_C), 1) k_tensor4(co
 #pragma unroll
                 for (int i = 0; i < NP; ++i) {
                     const int d = gd[i * nEp + le];
+                    FEA_CHECK(d >= 0 && d < prm.n_dof);
                     cp_async8(gu + i * ls + le, prm.u + d);
                     cp_async8(gv + i * ls + le, prm.v + d);
                 }
