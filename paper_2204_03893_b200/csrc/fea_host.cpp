@@ -1216,7 +1216,7 @@ fea_status fea_build_pattern(fea_ctx c, int64_t* row_begin, int64_t* n_rows_loca
     if (v6) {
         // two V buffers, two gather / Lambda / W stages (fea6_smem_layout); records stay in global memory
         const int64_t budget = c->tune_smem ? c->tune_smem : 227 * 1024;
-        e_max = std::min<int64_t>(512, 65535 / T - 2) / 8 * 8;
+        e_max = std::min<int64_t>(32 * fea6_prod_rounds(c->order), 65535 / T - 2) / 8 * 8;
         if (c->tune_emax) e_max = std::min<int64_t>(e_max, c->tune_emax / 8 * 8);
         int32_t L6[FEA_L_N];
         for (; e_max >= 8; e_max -= 8) {

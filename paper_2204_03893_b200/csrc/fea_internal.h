@@ -304,13 +304,21 @@ int fea_kernel_occupancy5(int order, int do_m, int do_c, int smem_bytes, int* ct
 #ifndef FEA6_A1MODE
 #define FEA6_A1MODE(p) ((p) == 4 ? 2 : 0)
 #endif
+// phase-B warps: P4 (FEA6_P4_MERGED 1) none -- the 15 DMMA warps (one row tile each) run phase B of
+// the previous block after their A2, v5-style; P3: 7 (the DMMA warps run A2 only)
+#ifndef FEA6_P4_MERGED
+#define FEA6_P4_MERGED 0  // measured: C5 16.17 ms merged vs 14.18 with phase-B warps
+#endif
 #ifndef FEA6_NB
 #define FEA6_NB 7
 #endif
+__host__ __device__ constexpr int fea6_nb(int p) { return p == 4 && FEA6_P4_MERGED ? 0 : FEA6_NB; }
 __host__ __device__ constexpr bool fea6_supported(int p, int nq) { return p >= 3 && nq == fea_nq_native(p); }
-__host__ __device__ constexpr int fea6_na(int p) { return p == 4 ? 8 : 7; }
-__host__ __device__ constexpr int fea6_rt(int p) { return p == 4 ? 2 : 1; }
-__host__ __device__ constexpr int fea6_threads(int p) { return (fea6_na(p) + FEA6_NB + 1) * 32; }
+__host__ __device__ constexpr int fea6_na(int p) { return p == 4 ? (FEA6_P4_MERGED ? 15 : 8) : 7; }
+__host__ __device__ constexpr int fea6_rt(int p) { return p == 4 && !FEA6_P4_MERGED ? 2 : 1; }
+__host__ __device__ constexpr int fea6_threads(int p) { return (fea6_na(p) + fea6_nb(p) + 1) * 32; }
+// producer rounds (elements le = 32 h + lane, h < rounds): caps e_max at 32 * rounds
+__host__ __device__ constexpr int fea6_prod_rounds(int p) { return p == 4 ? 2 : 4; }
 // Lambda / gathered-u row stride (doubles): == 4 (mod 16), so the DMMA B-fragment loads
 // [(4 kk + c) ls + 8 et + g] are conflict-free per half-warp
 __host__ __device__ inline int32_t fea6_lstride(int32_t e_max) { return e_max + ((4 - e_max) % 16 + 16) % 16; }
@@ -329,7 +337,7 @@ __host__ __device__ inline int32_t fea6_vstride(int32_t e_max) { return e_max + 
 // GW [2][4][e_max] (|det B_e|, A00, A11, A01 from the producer); LW [3] Lambda [nqp][ls] then
 // W [3][e_max] (A1's copy for A2); mbarriers.
 enum { FEA6_L_V = 0, FEA6_L_VB = 1, FEA6_L_GU = 2, FEA6_L_GUB = 3, FEA6_L_GW = 4, FEA6_L_GWB = 5, FEA6_L_LW = 6,
-       FEA6_L_LWB = 7, FEA6_L_BARS = 10, FEA6_L_TOTAL = 11 };
+       FEA6_L_LWB = 7, FEA6_L_PF = 8, FEA6_L_BARS = 10, FEA6_L_TOTAL = 11 };
 __host__ __device__ inline void fea6_smem_layout(int32_t* L, int e_max, int p, int do_m, int do_c) {
     const int T = fea_T(p), np = fea_np(p), nqp = 4 * fea_nk(fea_nq_native(p));
     const int ls = fea6_lstride(e_max), vs = fea6_vstride(e_max);
@@ -344,6 +352,7 @@ __host__ __device__ inline void fea6_smem_layout(int32_t* L, int e_max, int p, i
     L[FEA6_L_GW] = o; o += 2 * L[FEA6_L_GWB];
     L[FEA6_L_LWB] = fea_align(8 * (nqp * ls + 3 * e_max), 128);
     L[FEA6_L_LW] = o; o += 3 * L[FEA6_L_LWB];  // three Lambda / W buffers (A1 runs two blocks ahead)
+    L[FEA6_L_PF] = o; o += fea_align(8 * ((nqp + 7) / 8) * fea_kt(p) * 32, 128);  // Phi^T A-fragments (A1)
     L[FEA6_L_BARS] = o; o += 14 * 8;
     L[FEA6_L_TOTAL] = o;
 }

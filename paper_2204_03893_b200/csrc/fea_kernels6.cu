@@ -56,7 +56,7 @@ template <int P, bool DO_M, bool DO_C, bool DIAG>
 __global__ void __launch_bounds__(fea6_threads(P), 1) k_reassemble6(const __grid_constant__ FeaKParams prm) {
     constexpr int NP = fea_np(P), T = fea_T(P), NTT = fea_ntt(P);
     constexpr int NQ = fea_nq_native(P), NK = fea_nk(NQ), NQP = 4 * NK;
-    constexpr int NA = fea6_na(P), RT = fea6_rt(P), NB = FEA6_NB;
+    constexpr int NA = fea6_na(P), RT = fea6_rt(P), NB = fea6_nb(P);
     constexpr int MT = (NQP + 7) / 8, KT = fea_kt(P);
     constexpr bool IL = DO_M && DO_C;  // {m, c} cells
     constexpr int oW = (NP * NQ + 1) & ~1;
@@ -84,13 +84,17 @@ __global__ void __launch_bounds__(fea6_threads(P), 1) k_reassemble6(const __grid
             mbar_init(&gat_full[b], 33);  // 32 lanes' cp.async completions + the geometry stores
             mbar_init(&gat_free[b], FEA6_A1MODE(P) == 2 ? NA : NB);
             mbar_init(&v_full[b], NA);
-            mbar_init(&v_free[b], NB);
+            mbar_init(&v_free[b], NB > 0 ? NB : NA);
         }
         for (int b = 0; b < 3; ++b) {
             mbar_init(&lam_full[b], FEA6_A1MODE(P) == 2 ? NA : NB);
             mbar_init(&lam_free[b], NA);
         }
         fence_mbar_init();
+    }
+    {  // Phi^T A-fragments of A1 into shared memory (A1 runs with a ~1 KB L1: no global reads there)
+        double* spf = reinterpret_cast<double*>(smem + prm.lay[FEA6_L_PF]);
+        for (int i = tid; i < MT * KT * 32; i += blockDim.x) spf[i] = __ldg(prm.qfrag + 4 * NTT * NK * 32 + i);
     }
     if (tid < 6) {  // the zero cell (row 0, column e_max) of both V buffers: double e_max (8-byte
                     // cells) and doubles 2 e_max, 2 e_max + 1 ({m, c} cells); A2 never writes it
@@ -113,6 +117,33 @@ __global__ void __launch_bounds__(fea6_threads(P), 1) k_reassemble6(const __grid
         };
         if (lane == 0)
             for (int k = 0; k < 2 && k < nb; ++k) prefetch_blk(k);
+        // software-pipelined across blocks (every global read is an L2 round trip): the DOFs of
+        // block j + 1 load while block j's gathers and geometry run, its descriptor one block
+        // earlier still; element le = 32 h + lane, h < PR rounds
+        constexpr int PR = fea6_prod_rounds(P);
+        FEA_CHECK(e_max <= 32 * PR);
+        int32_t dn[PR][NP];
+        int nE_c = 0, nE_n = 0, nEp_n = 0;
+        const int32_t* gd_n = nullptr;
+        auto load_desc = [&](int k) {
+            const FeaBlock* B = prm.blocks + b0 + k * G;
+            nE_n = ldg_s32(&B->nE);
+            gd_n = prm.dofs + __ldg(&B->dof_off);
+        };
+        auto load_dofs = [&]() {  // the DOFs of the block whose descriptor load_desc fetched
+            nEp_n = fea_pad4(nE_n);
+#pragma unroll
+            for (int h = 0; h < PR; ++h)
+#pragma unroll
+                for (int i = 0; i < NP; ++i)
+                    dn[h][i] = 32 * h + lane < nE_n ? ldg_s32(gd_n + i * nEp_n + 32 * h + lane) : 0;
+        };
+        if (nb > 0) {
+            load_desc(0);
+            load_dofs();
+            nE_c = nE_n;
+            if (nb > 1) load_desc(1);
+        }
         T6_DECL
         for (int j = 0; j < nb; ++j) {
             const int g = j & 1;
@@ -122,34 +153,48 @@ __global__ void __launch_bounds__(fea6_threads(P), 1) k_reassemble6(const __grid
             const int l3 = j % 3;
             if (j >= 3) mbar_wait(&lam_free[l3], (uint32_t)(((j / 3) - 1) & 1));  // W goes to LW[j % 3]
             T6_TICK(0)
-            const FeaBlock* B = prm.blocks + b0 + j * G;
-            const int nE = __ldg(&B->nE), nEp = fea_pad4(nE);
-            const int32_t* gd = prm.dofs + __ldg(&B->dof_off);
+            const int nE = nE_c;
             FEA_CHECK(nE >= 1 && nE <= e_max);
             double* gu = sGU(g);
             double* gw = sGW(g);
             double* W = sLW(l3) + NQP * ls;
-            for (int le = lane; le < nE; le += 32) {
-                int32_t d[NP];
+            const int nEr = DIAG && (prm.dbg_mode & 8) ? 0 : nE;  // (diagnostics: no gathers)
+            double2 xa[PR], xb[PR], xc[PR];
 #pragma unroll
-                for (int i = 0; i < NP; ++i) d[i] = ldg_s32(gd + i * nEp + le);
+            for (int h = 0; h < PR; ++h) {  // u gathers and vertex coordinates of every round
+                const int le = 32 * h + lane;
+                if (le < nEr) {
 #pragma unroll
-                for (int i = 0; i < NP; ++i) FEA_CHECK(d[i] >= 0 && d[i] < prm.n_dof);
+                    for (int i = 0; i < NP; ++i) FEA_CHECK(dn[h][i] >= 0 && dn[h][i] < prm.n_dof);
 #pragma unroll
-                for (int i = 0; i < NP; ++i) cp_async8(gu + i * ls + le, prm.u + d[i]);
-                // element geometry once per element: b_e = |det B_e|, vec A_e
-                const double2 a = ldg_f64x2(prm.xy + d[0]), b = ldg_f64x2(prm.xy + d[1]), c = ldg_f64x2(prm.xy + d[2]);
-                const double B00 = b.x - a.x, B10 = b.y - a.y, B01 = c.x - a.x, B11 = c.y - a.y;
-                const double det = B00 * B11 - B01 * B10;
-                const double inv = 1.0 / (det * det);  // det(B^T B) = det(B)^2
-                gw[le] = fabs(det);
-                W[le] = (B01 * B01 + B11 * B11) * inv;
-                W[e_max + le] = (B00 * B00 + B10 * B10) * inv;
-                W[2 * e_max + le] = -(B00 * B01 + B10 * B11) * inv;
+                    for (int i = 0; i < NP; ++i) cp_async8(gu + i * ls + le, prm.u + dn[h][i]);
+                    xa[h] = ldg_f64x2(prm.xy + dn[h][0]);
+                    xb[h] = ldg_f64x2(prm.xy + dn[h][1]);
+                    xc[h] = ldg_f64x2(prm.xy + dn[h][2]);
+                }
+            }
+            cp_async_mbar_arrive(&gat_full[g]);  // (noinc) counts when this lane's gathers land
+            if (j + 1 < nb) {  // the next block's DOFs (registers dn are free again), its successor's descriptor
+                load_dofs();
+                nE_c = nE_n;
+                if (j + 2 < nb) load_desc(j + 2);
+            }
+#pragma unroll
+            for (int h = 0; h < PR; ++h) {
+                const int le = 32 * h + lane;
+                if (le < nEr) {  // element geometry once per element: b_e = |det B_e|, vec A_e
+                    const double B00 = xb[h].x - xa[h].x, B10 = xb[h].y - xa[h].y;
+                    const double B01 = xc[h].x - xa[h].x, B11 = xc[h].y - xa[h].y;
+                    const double det = B00 * B11 - B01 * B10;
+                    const double inv = 1.0 / (det * det);  // det(B^T B) = det(B)^2
+                    gw[le] = fabs(det);
+                    W[le] = (B01 * B01 + B11 * B11) * inv;
+                    W[e_max + le] = (B00 * B00 + B10 * B10) * inv;
+                    W[2 * e_max + le] = -(B00 * B01 + B10 * B11) * inv;
+                }
             }
             for (int le = nE + lane; le < ((nE + 7) & ~7); le += 32)  // padding columns of the last tile
                 W[le] = W[e_max + le] = W[2 * e_max + le] = 0.0;
-            cp_async_mbar_arrive(&gat_full[g]);  // (noinc) counts when this lane's gathers land
             warp_arrive(&gat_full[g], lane);     // the geometry stores
             T6_TICK(1)
         }
@@ -176,12 +221,14 @@ __global__ void __launch_bounds__(fea6_threads(P), 1) k_reassemble6(const __grid
         if (aw < net) mbar_wait(&gat_full[g], (uint32_t)((j >> 1) & 1));
         const double* gU = sGU(g);
         const double* gw = sGW(g);
-        for (int et = aw; et < net; et += naw) {  // one element tile, all m-tiles (independent chains)
-            double pf[MT][KT];  // Phi^T A-fragments (L1 / L2)
+        const int net_run = DIAG && (prm.dbg_mode & 2) ? 0 : net;  // diagnostics: A1 skipped
+        for (int et = aw; et < net_run; et += naw) {  // one element tile, all m-tiles (independent chains)
+            const double* spf = reinterpret_cast<const double*>(smem + prm.lay[FEA6_L_PF]);
+            double pf[MT][KT];  // Phi^T A-fragments (shared memory)
 #pragma unroll
             for (int mt = 0; mt < MT; ++mt)
 #pragma unroll
-                for (int kt = 0; kt < KT; ++kt) pf[mt][kt] = __ldg(prm.qfrag + 4 * NTT * NK * 32 + (mt * KT + kt) * 32 + lane);
+                for (int kt = 0; kt < KT; ++kt) pf[mt][kt] = spf[(mt * KT + kt) * 32 + lane];
             double uq[MT][2];
 #pragma unroll
             for (int mt = 0; mt < MT; ++mt) uq[mt][0] = uq[mt][1] = 0.0;
@@ -214,6 +261,116 @@ __global__ void __launch_bounds__(fea6_threads(P), 1) k_reassemble6(const __grid
         }
     };
 
+    // ------------------------------------------------------------------ phase B helpers
+    // B(jb): every CSR slot of the block = sum of its contributors, in ascending
+    // library element order (no atomics).  Class A (<= 2 contributors): warp bw of nbw takes the
+    // 32-slot chunks bw, bw + nbw, ... (U per round, two rounds of item loads in flight per lane);
+    // class B: one item per thread.  With nearly all shared memory in use the L1 holds ~1 KB, so
+    // every global read is an L2 round trip: the next phase B's descriptor and first items are
+    // loaded (prefetchB) right after the current one.
+    constexpr int U = 8;
+    struct BState {
+        int nslots, ncls, rB, nch;
+        int64_t slot0;
+        const uint8_t* rec;
+        uint32_t wa[U], wb[U];
+        uint4 ib;
+    };
+    auto loadA = [&](const BState& st, uint32_t (&w)[U], int c0, int nbw) {
+        const uint32_t* ia = reinterpret_cast<const uint32_t*>(st.rec);
+#pragma unroll
+        for (int u = 0; u < U; ++u) {
+            const int ch = c0 + u * nbw;
+            w[u] = ch < st.nch ? ldg_u32(ia + ch * 32 + lane) : 0xffffffffu;
+        }
+    };
+    auto prefetchB = [&](BState& st, int jb, int bt, int bw, int nbw) {
+        const FeaBlock* B = prm.blocks + b0 + jb * G;
+        st.nslots = __ldg(&B->nslots);
+        st.ncls = __ldg(&B->ncls);
+        st.rB = __ldg(&B->pad_);
+        st.slot0 = __ldg(&B->slot0);
+        st.rec = prm.records + __ldg(&B->rec_off);
+        st.nch = (st.nslots + 31) >> 5;
+        FEA_CHECK(st.slot0 >= 0 && st.slot0 + st.nslots <= prm.n_slots &&
+                  __ldg(&B->rec_off) + __ldg(&B->rec_bytes) <= prm.rec_size);
+        FEA_CHECK(4 * 32 * st.nch + (int64_t)st.ncls * st.rB <= __ldg(&B->rec_bytes));
+        loadA(st, st.wa, bw, nbw);
+        loadA(st, st.wb, bw + U * nbw, nbw);
+        st.ib = make_uint4(0, 0, 0, 0);
+        if (bt < st.ncls)
+            st.ib = __ldg(reinterpret_cast<const uint4*>(st.rec + 4 * ((st.nslots + 31) & ~31) + (size_t)bt * st.rB));
+    };
+    auto phaseB = [&](BState& st, int jb, int bt, int bw, int nbw) {
+        const int g = jb & 1;
+        if (DIAG && (prm.dbg_mode & 1)) {  // diagnostics: phase B skipped (synchronisation kept)
+            mbar_wait(&v_full[g], (uint32_t)((jb >> 1) & 1));
+            warp_arrive(&v_free[g], lane);
+            return;
+        }
+        const int nslots = st.nslots;
+        double* om = DO_M ? prm.out_m + st.slot0 : nullptr;
+        double* oc = DO_C ? prm.out_c + st.slot0 : nullptr;
+        const uint8_t* Vb = sV(g);
+        auto run = [&](const uint32_t (&w)[U], int c0) {
+#pragma unroll
+            for (int u = 0; u < U; ++u) {
+                const uint32_t it = w[u];
+                const int o0 = it & 0xffff, o1 = it >> 16;
+                if (o0 != 0xffff) {
+                    const int p = (c0 + u * nbw) * 32 + lane;
+                    FEA_CHECK(p < nslots && o0 < T * vs && o1 < T * vs);
+                    if (IL) {
+                        const double2 x0 = reinterpret_cast<const double2*>(Vb)[o0];
+                        const double2 x1 = reinterpret_cast<const double2*>(Vb)[o1];
+                        om[p] = x0.x + x1.x;
+                        oc[p] = x0.y + x1.y;
+                    } else {
+                        const double sum = reinterpret_cast<const double*>(Vb)[o0] + reinterpret_cast<const double*>(Vb)[o1];
+                        if (DO_M) om[p] = sum;
+                        else oc[p] = sum;
+                    }
+                }
+            }
+        };
+        mbar_wait(&v_full[g], (uint32_t)((jb >> 1) & 1));
+        for (int c0 = bw; c0 < st.nch; c0 += 2 * U * nbw) {
+            run(st.wa, c0);
+            loadA(st, st.wa, c0 + 2 * U * nbw, nbw);
+            run(st.wb, c0 + U * nbw);
+            loadA(st, st.wb, c0 + 3 * U * nbw, nbw);
+        }
+        // class B (more than two contributors: vertex diagonals), one item per thread
+        for (int it = bt; it < st.ncls; it += nbw * 32) {
+            const uint16_t* wrd = reinterpret_cast<const uint16_t*>(st.rec + 4 * ((nslots + 31) & ~31) + (size_t)it * st.rB);
+            const uint4 h = it == bt ? st.ib : __ldg(reinterpret_cast<const uint4*>(wrd));
+            const int sl = h.x & 0xffff, C = h.x >> 16;
+            FEA_CHECK(sl < nslots && C >= 3 && 2 * (C + 2) <= st.rB);
+            double am = 0.0, ac = 0.0;
+            for (int q = 0; q < C; ++q) {
+                const uint32_t hw = q < 2 ? h.y : q < 4 ? h.z : h.w;  // no local-memory indexing
+                const int o = q < 6 ? (int)((hw >> (16 * (q & 1))) & 0xffff) : (int)__ldg(wrd + 2 + q);
+                FEA_CHECK(o < T * vs);
+                if (IL) {
+                    const double2 x = reinterpret_cast<const double2*>(Vb)[o];
+                    am += x.x;
+                    ac += x.y;
+                } else {
+                    am += reinterpret_cast<const double*>(Vb)[o];
+                }
+            }
+            if (IL) {
+                om[sl] = am;
+                oc[sl] = ac;
+            } else if (DO_M) {
+                om[sl] = am;
+            } else {
+                oc[sl] = am;
+            }
+        }
+        warp_arrive(&v_free[g], lane);
+    };
+
     if (warp < NA) {
         // ------------------------------------------------------------------ A warps: A2
         const int g8 = lane >> 2, cq = lane & 3;
@@ -231,6 +388,8 @@ __global__ void __launch_bounds__(fea6_threads(P), 1) k_reassemble6(const __grid
         T6_DECL
         int nE_n = nb > 0 ? ldg_s32(&prm.blocks[b0].nE) : 0;  // one block ahead (L2 latency; asm volatile: issued here)
         if (A1MODE == 2 && nb > 0) do_a1(0, NA - 1 - warp, NA, nE_n);
+        BState st;  // NB == 0: the A warps also run phase B (of the previous block, after their A2)
+        if (NB == 0 && nb > 0) prefetchB(st, 0, tid, warp, NA);
         for (int j = 0; j < nb; ++j) {
             const int g = j & 1;
             const int nE = nE_n;
@@ -245,7 +404,9 @@ __global__ void __launch_bounds__(fea6_threads(P), 1) k_reassemble6(const __grid
             if (j >= 2) mbar_wait(&v_free[g], (uint32_t)(((j >> 1) - 1) & 1));
             T6_TICK(3)
             uint8_t* Vb = sV(g);
-            for (int et = 0; et < net; ++et) {
+            const int net_a2 = DIAG && (prm.dbg_mode & 4) ? 0 : net;  // diagnostics: A2 skipped
+            if (DIAG && (prm.dbg_mode & 4) && A1MODE == 2 && j + 1 < nb) do_a1(j + 1, NA - 1 - warp, NA, nE_n);
+            for (int et = 0; et < net_a2; ++et) {
                 // (units to the last warps first: warp NA - 1 holds one row tile less)
                 if (A1MODE == 2 && et == (net >> 1) && j + 1 < nb) do_a1(j + 1, NA - 1 - warp, NA, nE_n);
                 const int col = et * 8 + g8, le0 = et * 8 + 2 * cq;
@@ -295,51 +456,25 @@ __global__ void __launch_bounds__(fea6_threads(P), 1) k_reassemble6(const __grid
                 mbar_arrive(&lam_free[l3]);
                 mbar_arrive(&v_full[g]);
             }
+            if (NB == 0 && j >= 1) {
+                phaseB(st, j - 1, tid, warp, NA);
+                prefetchB(st, j, tid, warp, NA);
+                T6_TICK(6)
+            }
         }
+        if (NB == 0 && nb > 0) phaseB(st, nb - 1, tid, warp, NA);
         T6_FLUSH(0)
         return;
     }
 
     // ------------------------------------------------------------------ B warps: [A1(j)], then B(j - LAG)
-    // (A1 runs two blocks ahead of phase B and one to two ahead of A2: three Lambda buffers).  With
-    // nearly all shared memory in use the L1 holds ~1 KB, so every global read is an L2 round trip:
-    // the next phase B's descriptor and first items are loaded right after the current one.
-    {
+    // (A1 runs two blocks ahead of phase B and one to two ahead of A2: three Lambda buffers).
+    if (NB > 0) {
         const int bt = tid - NA * 32, bw = bt >> 5;
         constexpr int LAG = A1MODE == 2 ? 0 : 2;  // phase B of block j - LAG after A1(j) (B warps running A1)
         int nE_a = nb > 0 ? ldg_s32(&prm.blocks[b0].nE) : 0;  // A1's block size, one block ahead
-        // phase B: warp bw takes the 32-slot chunks bw, bw + NB, ... (U per round, two rounds of item
-        // loads in flight per lane)
-        constexpr int U = 8;
-        int nslots = 0, ncls = 0, rB = 0, nch = 0;
-        int64_t slot0 = 0;
-        const uint8_t* rec = nullptr;
-        uint32_t wa[U], wb[U];
-        uint4 ib = make_uint4(0, 0, 0, 0);
-        auto loadA = [&](uint32_t (&w)[U], int c0) {
-            const uint32_t* ia = reinterpret_cast<const uint32_t*>(rec);
-#pragma unroll
-            for (int u = 0; u < U; ++u) {
-                const int ch = c0 + u * NB;
-                w[u] = ch < nch ? ldg_u32(ia + ch * 32 + lane) : 0xffffffffu;
-            }
-        };
-        auto prefetchB = [&](int jb) {  // descriptor, first two rounds, this thread's first class-B item
-            const FeaBlock* B = prm.blocks + b0 + jb * G;
-            nslots = __ldg(&B->nslots);
-            ncls = __ldg(&B->ncls);
-            rB = __ldg(&B->pad_);
-            slot0 = __ldg(&B->slot0);
-            rec = prm.records + __ldg(&B->rec_off);
-            nch = (nslots + 31) >> 5;
-            FEA_CHECK(slot0 >= 0 && slot0 + nslots <= prm.n_slots && __ldg(&B->rec_off) + __ldg(&B->rec_bytes) <= prm.rec_size);
-            FEA_CHECK(4 * 32 * nch + (int64_t)ncls * rB <= __ldg(&B->rec_bytes));
-            loadA(wa, bw);
-            loadA(wb, bw + U * NB);
-            if (bt < ncls)
-                ib = __ldg(reinterpret_cast<const uint4*>(rec + 4 * ((nslots + 31) & ~31) + (size_t)bt * rB));
-        };
-        if (nb > 0) prefetchB(0);
+        BState st;
+        if (nb > 0) prefetchB(st, 0, bt, bw, NB);
         T6_DECL
         for (int j = 0; j < nb + LAG; ++j) {
             if (A1MODE == 0 && j < nb) {
@@ -349,74 +484,10 @@ __global__ void __launch_bounds__(fea6_threads(P), 1) k_reassemble6(const __grid
                 T6_TICK(6)
             }
             if (j < LAG) continue;
-            // ---- B(j - LAG): every CSR slot of the block = sum of its contributors
-            const int jb = j - LAG, g = jb & 1;
-            double* om = DO_M ? prm.out_m + slot0 : nullptr;
-            double* oc = DO_C ? prm.out_c + slot0 : nullptr;
-            const uint8_t* Vb = sV(g);
-            auto run = [&](const uint32_t (&w)[U], int c0) {
-#pragma unroll
-                for (int u = 0; u < U; ++u) {
-                    const uint32_t it = w[u];
-                    const int o0 = it & 0xffff, o1 = it >> 16;
-                    if (o0 != 0xffff) {
-                        const int p = (c0 + u * NB) * 32 + lane;
-                        FEA_CHECK(p < nslots && o0 < T * vs && o1 < T * vs);
-                        if (IL) {
-                            const double2 x0 = reinterpret_cast<const double2*>(Vb)[o0];
-                            const double2 x1 = reinterpret_cast<const double2*>(Vb)[o1];
-                            om[p] = x0.x + x1.x;
-                            oc[p] = x0.y + x1.y;
-                        } else {
-                            const double sum = reinterpret_cast<const double*>(Vb)[o0] + reinterpret_cast<const double*>(Vb)[o1];
-                            if (DO_M) om[p] = sum;
-                            else oc[p] = sum;
-                        }
-                    }
-                }
-            };
             T6_TICK(0)
-            mbar_wait(&v_full[g], (uint32_t)((jb >> 1) & 1));
-            T6_TICK(1)
-            for (int c0 = bw; c0 < nch; c0 += 2 * U * NB) {
-                run(wa, c0);
-                loadA(wa, c0 + 2 * U * NB);
-                run(wb, c0 + U * NB);
-                loadA(wb, c0 + 3 * U * NB);
-            }
+            phaseB(st, j - LAG, bt, bw, NB);
             T6_TICK(2)
-            // class B (more than two contributors: vertex diagonals), one item per thread, summed in
-            // ascending library element order
-            for (int it = bt; it < ncls; it += NB * 32) {
-                const uint16_t* wrd = reinterpret_cast<const uint16_t*>(rec + 4 * ((nslots + 31) & ~31) + (size_t)it * rB);
-                const uint4 h = it == bt ? ib : __ldg(reinterpret_cast<const uint4*>(wrd));
-                const int sl = h.x & 0xffff, C = h.x >> 16;
-                FEA_CHECK(sl < nslots && C >= 3 && 2 * (C + 2) <= rB);
-                double am = 0.0, ac = 0.0;
-                for (int q = 0; q < C; ++q) {
-                    const uint32_t hw = q < 2 ? h.y : q < 4 ? h.z : h.w;  // no local-memory indexing
-                    const int o = q < 6 ? (int)((hw >> (16 * (q & 1))) & 0xffff) : (int)__ldg(wrd + 2 + q);
-                    FEA_CHECK(o < T * vs);
-                    if (IL) {
-                        const double2 x = reinterpret_cast<const double2*>(Vb)[o];
-                        am += x.x;
-                        ac += x.y;
-                    } else {
-                        am += reinterpret_cast<const double*>(Vb)[o];
-                    }
-                }
-                if (IL) {
-                    om[sl] = am;
-                    oc[sl] = ac;
-                } else if (DO_M) {
-                    om[sl] = am;
-                } else {
-                    oc[sl] = am;
-                }
-            }
-            T6_TICK(3)
-            warp_arrive(&v_free[g], lane);
-            if (jb + 1 < nb) prefetchB(jb + 1);
+            if (j - LAG + 1 < nb) prefetchB(st, j - LAG + 1, bt, bw, NB);
             T6_TICK(7)
         }
         T6_FLUSH(8)
