@@ -274,6 +274,82 @@ __device__ __forceinline__ void phase_b5(const uint8_t* __restrict__ rec, int nc
     }
 }
 
+// ---- phase B in CSR slot order (kernel v5 with the v6 record format, fea_internal.h): class A =
+// one u32 item per slot {u16 V offset 0, u16 V offset 1} (one contributor: offset 1 = the zero
+// cell; more than two: 0xffff, a hole), lane l of a warp takes slot 32 c + l of chunk c, so the CSR
+// stores of a warp are 256 contiguous bytes per matrix; class B = nB flat items of R bytes {u16 slot,
+// u16 C, u16 V offset [C]}, one per thread.  Every slot sums its contributors in ascending library
+// element order (the same order as phase_b5).  `rec` is in shared memory; cells are {m, c} double2
+// (IL) or doubles.
+template <bool DO_M, bool DO_C, bool IL>
+__device__ __forceinline__ void phase_b_slots(const uint8_t* __restrict__ rec, int nslots, int nB, int R,
+                                              const double* __restrict__ sV, double* om, double* oc, int warp,
+                                              int lane, int nwarps) {
+    constexpr int U = 4;  // chunks per round (their loads in flight together)
+    const uint32_t* ia = reinterpret_cast<const uint32_t*>(rec);
+    const int nch = (nslots + 31) >> 5;
+    for (int c0 = warp; c0 < nch; c0 += U * nwarps) {
+        uint32_t w[U];
+#pragma unroll
+        for (int u = 0; u < U; ++u) {
+            const int ch = c0 + u * nwarps;
+            w[u] = ch < nch ? ia[ch * 32 + lane] : 0xffffffffu;
+        }
+        double2 x0[U], x1[U];
+#pragma unroll
+        for (int u = 0; u < U; ++u) {
+            const int o0 = w[u] & 0xffff, o1 = w[u] >> 16;
+            const bool hole = o0 == 0xffff;
+            if (IL) {
+                x0[u] = reinterpret_cast<const double2*>(sV)[hole ? 0 : o0];
+                x1[u] = reinterpret_cast<const double2*>(sV)[hole ? 0 : o1];
+            } else {
+                x0[u].x = sV[hole ? 0 : o0];
+                x1[u].x = sV[hole ? 0 : o1];
+            }
+        }
+#pragma unroll
+        for (int u = 0; u < U; ++u) {
+            if ((w[u] & 0xffff) == 0xffff) continue;
+            const int p = (c0 + u * nwarps) * 32 + lane;
+            FEA_CHECK(p < nslots);
+            if (IL) {
+                om[p] = x0[u].x + x1[u].x;
+                oc[p] = x0[u].y + x1[u].y;
+            } else if (DO_M) {
+                om[p] = x0[u].x + x1[u].x;
+            } else {
+                oc[p] = x0[u].x + x1[u].x;
+            }
+        }
+    }
+    const uint8_t* bB = rec + 4 * (nch * 32);
+    for (int it = warp * 32 + lane; it < nB; it += nwarps * 32) {
+        const uint16_t* wrd = reinterpret_cast<const uint16_t*>(bB + (size_t)it * R);
+        const int sl = wrd[0], C = wrd[1];
+        FEA_CHECK(sl < nslots && 2 * (C + 2) <= R);
+        double am = 0.0, ac = 0.0;
+        for (int q = 0; q < C; ++q) {
+            const int o = wrd[2 + q];
+            if (IL) {
+                const double2 x = reinterpret_cast<const double2*>(sV)[o];
+                am += x.x;
+                ac += x.y;
+            } else {
+                am += sV[o];
+            }
+        }
+        if (IL) {
+            om[sl] = am;
+            oc[sl] = ac;
+        } else if (DO_M) {
+            om[sl] = am;
+        } else {
+            oc[sl] = am;
+        }
+    }
+}
+
 // derivative k'(u) of the coefficient (fea.h FEA_K_*); PWL: slope of the segment of u
 __device__ __forceinline__ double dkeval(const FeaCoef& c, double u) {
     if (c.kind == 0) {

@@ -981,7 +981,7 @@ static fea_status build_blocks(fea_ctx c, bool v5, bool orient, int64_t e_max, i
             k = k2;
         }
         const int32_t nslot = (int32_t)sstart.size();
-        if (v6) {  // kernel v6 record: class A in slot order, class B (> 2 contributors) as flat items
+        if (v6 || (v5 && !orient && FEA5_SLOT)) {  // kernel v6 (and v5) record: class A in slot order, class B as flat items
             if (nslot > 65535) {
                 o.err = "more than 65535 slots in one block";
                 return;
@@ -1008,6 +1008,10 @@ static fea_status build_blocks(fea_ctx c, bool v5, bool orient, int64_t e_max, i
                 return;
             }
             const int32_t bytes = (4 * nA + (int32_t)clsB.size() * R + 127) & ~127;
+            if (bytes > rec_budget) {  // v5: the record must fit its shared-memory stage
+                o.err = "record exceeds the shared-memory budget";
+                return;
+            }
             o.rec.assign(bytes, 0);
             std::memcpy(o.rec.data(), ia.data(), 4 * (size_t)nA);
             for (size_t it = 0; it < clsB.size(); ++it) {

@@ -32,6 +32,9 @@ __host__ __device__ constexpr int fea_rstages(int p) { return p <= 2 ? 3 : 2; }
 #define FEA5_PF 3  // kernel v5: L2 prefetch distance (blocks); at most 5 (the descriptor ring)
 #endif
 static_assert(FEA5_PF >= 1 && FEA5_PF <= 5, "FEA5_PF: the 8-entry descriptor ring is filled 6 blocks ahead");
+#ifndef FEA5_SLOT
+#define FEA5_SLOT 1  // kernel v5 phase B in CSR slot order (the v6 record format); 0: count classes
+#endif
 #ifndef FEA4_A1FIRST
 #define FEA4_A1FIRST 1  // kernel v4: warps running A1(j+1) before B(j): 0 none, 1 odd warps, 2 all
 #endif

@@ -340,9 +340,14 @@ __global__ void __launch_bounds__(fea5_threads(P), 1) k_reassemble5(const __grid
             {
                 double* om = DO_M ? prm.out_m + bk.slot0 : nullptr;
                 double* oc = DO_C ? prm.out_c + bk.slot0 : nullptr;
-                phase_b5<DO_M, DO_C, false, DO_M && DO_C>(sRec0 + b * rec_stride, bk.ncls,
-                                     sVm0 + b * (DO_M && DO_C ? 2 : 1) * vbuf, sVc0 + b * vbuf, om, oc, tid,
-                                     NW * 32);
+                if (FEA5_SLOT)  // CSR slot order (contiguous stores)
+                    phase_b_slots<DO_M, DO_C, DO_M && DO_C>(sRec0 + b * rec_stride, bk.nslots, bk.ncls, bk.pad_,
+                                                           DO_M ? sVm0 + b * (DO_C ? 2 : 1) * vbuf : sVc0 + b * vbuf,
+                                                           om, oc, warp, lane, NW);
+                else
+                    phase_b5<DO_M, DO_C, false, DO_M && DO_C>(sRec0 + b * rec_stride, bk.ncls,
+                                         sVm0 + b * (DO_M && DO_C ? 2 : 1) * vbuf, sVc0 + b * vbuf, om, oc, tid,
+                                         NW * 32);
             }
             tick(4);
             __syncwarp();

@@ -59,6 +59,13 @@ __global__ void __launch_bounds__(fea6_threads(P), 1) k_reassemble6(const __grid
     constexpr int NA = fea6_na(P), RT = fea6_rt(P), NB = fea6_nb(P);
     constexpr int MT = (NQP + 7) / 8, KT = fea_kt(P);
     constexpr bool IL = DO_M && DO_C;  // {m, c} cells
+    // FEA_DEBUG_MODE skip bits (1 phase B, 2 A1, 4 A2, 8 gathers; timing diagnostics, results wrong
+    // by design): honoured by the DIAG instantiation, and by every one in a -DFEA6_DBGMODES build
+#ifdef FEA6_DBGMODES
+    constexpr bool DBGM = true;
+#else
+    constexpr bool DBGM = DIAG;
+#endif
     constexpr int oW = (NP * NQ + 1) & ~1;
     static_assert(NA * RT >= NTT, "row tiles");
     const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
@@ -158,7 +165,7 @@ __global__ void __launch_bounds__(fea6_threads(P), 1) k_reassemble6(const __grid
             double* gu = sGU(g);
             double* gw = sGW(g);
             double* W = sLW(l3) + NQP * ls;
-            const int nEr = DIAG && (prm.dbg_mode & 8) ? 0 : nE;  // (diagnostics: no gathers)
+            const int nEr = DBGM && (prm.dbg_mode & 8) ? 0 : nE;  // (diagnostics: no gathers)
             double2 xa[PR], xb[PR], xc[PR];
 #pragma unroll
             for (int h = 0; h < PR; ++h) {  // u gathers and vertex coordinates of every round
@@ -221,7 +228,7 @@ __global__ void __launch_bounds__(fea6_threads(P), 1) k_reassemble6(const __grid
         if (aw < net) mbar_wait(&gat_full[g], (uint32_t)((j >> 1) & 1));
         const double* gU = sGU(g);
         const double* gw = sGW(g);
-        const int net_run = DIAG && (prm.dbg_mode & 2) ? 0 : net;  // diagnostics: A1 skipped
+        const int net_run = DBGM && (prm.dbg_mode & 2) ? 0 : net;  // diagnostics: A1 skipped
         for (int et = aw; et < net_run; et += naw) {  // one element tile, all m-tiles (independent chains)
             const double* spf = reinterpret_cast<const double*>(smem + prm.lay[FEA6_L_PF]);
             double pf[MT][KT];  // Phi^T A-fragments (shared memory)
@@ -303,7 +310,7 @@ __global__ void __launch_bounds__(fea6_threads(P), 1) k_reassemble6(const __grid
     };
     auto phaseB = [&](BState& st, int jb, int bt, int bw, int nbw) {
         const int g = jb & 1;
-        if (DIAG && (prm.dbg_mode & 1)) {  // diagnostics: phase B skipped (synchronisation kept)
+        if (DBGM && (prm.dbg_mode & 1)) {  // diagnostics: phase B skipped (synchronisation kept)
             mbar_wait(&v_full[g], (uint32_t)((jb >> 1) & 1));
             warp_arrive(&v_free[g], lane);
             return;
@@ -404,8 +411,8 @@ __global__ void __launch_bounds__(fea6_threads(P), 1) k_reassemble6(const __grid
             if (j >= 2) mbar_wait(&v_free[g], (uint32_t)(((j >> 1) - 1) & 1));
             T6_TICK(3)
             uint8_t* Vb = sV(g);
-            const int net_a2 = DIAG && (prm.dbg_mode & 4) ? 0 : net;  // diagnostics: A2 skipped
-            if (DIAG && (prm.dbg_mode & 4) && A1MODE == 2 && j + 1 < nb) do_a1(j + 1, NA - 1 - warp, NA, nE_n);
+            const int net_a2 = DBGM && (prm.dbg_mode & 4) ? 0 : net;  // diagnostics: A2 skipped
+            if (DBGM && (prm.dbg_mode & 4) && A1MODE == 2 && j + 1 < nb) do_a1(j + 1, NA - 1 - warp, NA, nE_n);
             for (int et = 0; et < net_a2; ++et) {
                 // (units to the last warps first: warp NA - 1 holds one row tile less)
                 if (A1MODE == 2 && et == (net >> 1) && j + 1 < nb) do_a1(j + 1, NA - 1 - warp, NA, nE_n);
