@@ -83,6 +83,12 @@ enum {
     FEA_TUNE_TENSOR_KERNEL = 8, /* fea_assemble_tensor kernel: 0 = automatic (DMMA k_tensor4 for p >= 2
                                    or a non-native rule, k_tensor otherwise), 1 = k_tensor (one
                                    thread per element), 4 = k_tensor4 (FP64 tensor cores)            */
+    FEA_TUNE_SKIP = 12,         /* kernel v6 (P3 / P4): 1 = ghost elements compute only the 8-row DMMA
+                                   tiles of V that their block reads, each relabelled by the vertex
+                                   permutation that needs the fewest tiles (a symmetric rule only;
+                                   default): values reproducible run to run, equal to the oracle's
+                                   within the tolerance but not bit-identical across tilings or
+                                   world sizes; 0 = every row (bit-identical to FEA_TUNE_KERNEL 4)  */
     FEA_TUNE_TIMING = 11        /* 1 = fea_reassemble / fea_assemble record CUDA events around the
                                    exchange of u and around the assembly launches (read with
                                    fea_get_stat keys 36 / 37); 0 = off (default).  Keeps the plan.   */
@@ -233,7 +239,8 @@ fea_status fea_sync(fea_ctx ctx);
  * fea_assemble_tensor, else -1): 12 = tensor kernel (1 or 4), 13 = its grid, 16 = blocks,
  * 17 = element visits, 18 = owned elements, 19 = smem bytes per CTA.  With FEA_TUNE_TIMING (waits
  * for the last call's events): 36 = exchange of u in microseconds (world > 1; -1 if none ran),
- * 37 = assembly launches, first start to last end, in microseconds. */
+ * 37 = assembly launches, first start to last end, in microseconds.  38 = kernel v6 contraction
+ * work with FEA_TUNE_SKIP, per mille of every row of every visited element. */
 fea_status fea_get_stat(fea_ctx ctx, int key, int64_t* value);
 
 const char* fea_last_error(fea_ctx ctx);

@@ -145,6 +145,9 @@ struct fea_ctx_s {
     int64_t tune_smem = 0;
     int tune_kver = 0;     // 0 = automatic, 4 = force kernel v4
     int tune_pad1 = 1;     // v5: single-contributor slots padded into the two-contributor class
+    int tune_skip = 1;     // v6: ghost row-tile skipping with element rotations (FEA_TUNE_SKIP)
+    bool rule_sym = false; // the rule (of both matrices) is invariant under the 6 vertex permutations
+    int64_t skip_work = 0, skip_full = 0;  // v6 plan: A2 row-tile work with / without skipping
     int tune_tker = 0;     // tensor kernel: 0 = automatic, 1 = k_tensor, 4 = k_tensor4 (FEA_TUNE_TENSOR_KERNEL)
     int tune_overlap = 1;  // world > 1: interior blocks assemble while u is exchanged (FEA_TUNE_OVERLAP)
     int n_int = 0;         // interior blocks (first n_int of the plan when world > 1)
@@ -503,6 +506,24 @@ static fea_status make_rule(fea_ctx c, int order, int n_q, const double* q_xy, c
     return FEA_OK;
 }
 
+// Is the rule invariant under the 6 permutations of the barycentric coordinates (same points, same
+// weights)?  Then an element may be relabelled by any vertex permutation without changing its
+// quadrature sum beyond rounding (kernel v6 ghost row-tile skipping).
+static bool rule_symmetric(int n_q, const double* q_xy, const double* q_w) {
+    static const int P[6][3] = {{0, 1, 2}, {0, 2, 1}, {1, 0, 2}, {1, 2, 0}, {2, 0, 1}, {2, 1, 0}};
+    for (int s = 0; s < 6; ++s)
+        for (int q = 0; q < n_q; ++q) {
+            const double l[3] = {1.0 - q_xy[2 * q] - q_xy[2 * q + 1], q_xy[2 * q], q_xy[2 * q + 1]};
+            const double x = l[P[s][1]], y = l[P[s][2]];
+            bool found = false;
+            for (int r = 0; r < n_q && !found; ++r)
+                found = std::fabs(q_xy[2 * r] - x) < 1e-12 && std::fabs(q_xy[2 * r + 1] - y) < 1e-12 &&
+                        std::fabs(q_w[r] - q_w[q]) < 1e-14;
+            if (!found) return false;
+        }
+    return true;
+}
+
 static fea_status upload_rule(fea_ctx c, int n_q, const std::vector<double>& ctab, const std::vector<double>& qfrag,
                               const std::vector<double>& jplain, double*& d_qfrag, double*& d_ttab) {
     dfree(d_qfrag);
@@ -543,6 +564,7 @@ fea_status fea_set_element(fea_ctx c, int order, int n_q, const double* q_xy, co
     c->qfrag = qfrag;
     c->jplain = jplain;
     c->split = false;
+    c->rule_sym = rule_symmetric(n_q, q_xy, q_w);
     dfree(c->d_tables_c);
     dfree(c->d_ttab_c);
     return upload_rule(c, n_q, ctab, qfrag, jplain, c->d_tables, c->d_ttab);
@@ -565,6 +587,7 @@ fea_status fea_set_rule(fea_ctx c, int which, int n_q, const double* q_xy, const
         c->qfrag = qfrag;
         c->jplain = jplain;
         c->split = false;
+        c->rule_sym = rule_symmetric(n_q, q_xy, q_w);
         dfree(c->d_tables_c);
         dfree(c->d_ttab_c);
         return upload_rule(c, n_q, ctab, qfrag, jplain, c->d_tables, c->d_ttab);
@@ -770,6 +793,10 @@ fea_status fea_set_tuning(fea_ctx c, int key, int64_t value) {
             if (value != 0 && value != 1 && value != 4) return c->fail(FEA_E_ARG, "tensor kernel must be 0, 1 or 4");
             c->tune_tker = (int)value;
             break;
+        case 12:  // kernel v6: ghost row-tile skipping with element rotations (1, default) or off (0)
+            if (value != 0 && value != 1) return c->fail(FEA_E_ARG, "skip flag must be 0 or 1");
+            c->tune_skip = (int)value;
+            break;
         case 11:  // per-call timing events (fea_get_stat keys 36, 37)
             if (value != 0 && value != 1) return c->fail(FEA_E_ARG, "timing flag must be 0 or 1");
             c->tune_timing = (int)value;
@@ -909,6 +936,34 @@ static fea_status build_blocks(fea_ctx c, bool v5, bool orient, int64_t e_max, i
     brow.push_back(nr);
 
     ptime("plan: row blocks");
+    // ---- kernel v6 row-tile skipping (FEA_TUNE_SKIP): an element recomputed as a ghost needs only
+    // the V rows (i, j) with i or j one of its DOFs in the block's rows; it is relabelled by the
+    // vertex permutation (of 6; the rule must be symmetric) that packs those rows into the fewest
+    // 8-row DMMA tiles, and the block's elements are ordered by their tile masks so each 8-element
+    // column tile skips the row tiles none of its elements needs.
+    const bool skip = v6 && c->tune_skip;
+    const int nperm = skip && c->rule_sym ? 6 : 1;
+    int sig[6][FEA_MAX_NP], siginv[6][FEA_MAX_NP];
+    uint32_t rowmask[FEA_MAX_NP];
+    {
+        static const int PP[6][3] = {{0, 1, 2}, {0, 2, 1}, {1, 0, 2}, {1, 2, 0}, {2, 0, 1}, {2, 1, 0}};
+        int kk[FEA_MAX_NP][3];
+        lib_nodes(c->order, kk);
+        for (int sp = 0; sp < 6; ++sp)
+            for (int i = 0; i < np; ++i) {
+                const int t0 = kk[i][PP[sp][0]], t1 = kk[i][PP[sp][1]], t2 = kk[i][PP[sp][2]];
+                for (int k = 0; k < np; ++k)
+                    if (kk[k][0] == t0 && kk[k][1] == t1 && kk[k][2] == t2) sig[sp][i] = k;
+            }
+        for (int sp = 0; sp < 6; ++sp)
+            for (int i = 0; i < np; ++i) siginv[sp][sig[sp][i]] = i;
+        for (int a = 0; a < np; ++a) {
+            rowmask[a] = 0;
+            for (int b2 = 0; b2 < np; ++b2) rowmask[a] |= 1u << (tri_index(np, std::min(a, b2), std::max(a, b2)) / 8);
+        }
+    }
+    const int NTT6 = (T + 7) / 8;
+    std::atomic<int64_t> skip_work(0), skip_full(0);
     // ---- per block: element set, (row, col) records sorted -> slots, contributors, record
     struct BOut {
         std::vector<int32_t> rownnz, cols, dofs;
@@ -936,6 +991,37 @@ static fea_status build_blocks(fea_ctx c, bool v5, bool orient, int64_t e_max, i
                 }
             o.fb.spare_[0] = inside ? 1 : 0;
         }
+        // element relabelling and column order (identity unless v6 skipping)
+        const int64_t nE0 = (int64_t)E.size();
+        std::vector<int8_t> rot(nE0, 0);
+        std::vector<uint32_t> emask(nE0, (1u << NTT6) - 1);
+        std::vector<int32_t> newpos(nE0);
+        std::iota(newpos.begin(), newpos.end(), 0);
+        if (skip) {
+            for (int64_t le = 0; le < nE0; ++le) {
+                const int32_t* d = &c->ed[(size_t)E[le] * np];
+                uint32_t best = ~0u;
+                int bs = 0;
+                for (int sp = 0; sp < nperm; ++sp) {
+                    uint32_t m = 0;
+                    for (int i = 0; i < np; ++i)
+                        if (d[i] >= ga && d[i] < gb) m |= rowmask[sig[sp][i]];
+                    if (__builtin_popcount(m) < __builtin_popcount(best)) {
+                        best = m;
+                        bs = sp;
+                    }
+                }
+                rot[le] = (int8_t)bs;
+                emask[le] = best;
+            }
+            std::vector<int32_t> ord(nE0);
+            std::iota(ord.begin(), ord.end(), 0);
+            std::stable_sort(ord.begin(), ord.end(), [&](int32_t x, int32_t y) {
+                const int px = __builtin_popcount(emask[x]), py = __builtin_popcount(emask[y]);
+                return px != py ? px > py : emask[x] < emask[y];
+            });
+            for (int64_t q = 0; q < nE0; ++q) newpos[ord[q]] = (int32_t)q;
+        }
         struct Rec { int32_t row, col, le, t; };  // t: V row (| 0x10000 if orient and i > j: Vdn)
         std::vector<Rec> recs;
         recs.reserve((size_t)(iptr[rb] - iptr[ra]) * np);
@@ -945,15 +1031,20 @@ static fea_status build_blocks(fea_ctx c, bool v5, bool orient, int64_t e_max, i
             const size_t r0 = recs.size();
             for (int64_t k = iptr[r]; k < iptr[r + 1]; ++k) {
                 const int32_t e = inc[k];
-                const int32_t le = (int32_t)(std::lower_bound(E.begin(), E.end(), e) - E.begin());
+                const int32_t le0 = (int32_t)(std::lower_bound(E.begin(), E.end(), e) - E.begin());
+                const int32_t le = newpos[le0];
+                const int* sg = sig[(int)rot[le0]];
                 const int32_t* d = &c->ed[(size_t)e * np];
                 for (int i = 0; i < np; ++i) {
                     if (d[i] != R0 + r) continue;
-                    for (int j = 0; j < np; ++j)
-                        // tensor plans (orient): V row fea_trow (off-diagonal pairs first), flag i > j
+                    for (int j = 0; j < np; ++j) {
+                        // tensor plans (orient): V row fea_trow (off-diagonal pairs first), flag i > j;
+                        // v6: the row of the relabelled pair (sigma(i), sigma(j))
+                        const int a = sg[i], b2 = sg[j];
                         recs.push_back({d[i], d[j], le,
                                         orient ? fea_trow(np, std::min(i, j), std::max(i, j)) | (i > j ? 0x10000 : 0)
-                                               : tri_index(np, std::min(i, j), std::max(i, j))});
+                                               : tri_index(np, std::min(a, b2), std::max(a, b2))});
+                    }
                 }
             }
             // stable insertion sort by column (a row has a few dozen records; no allocation)
@@ -1035,11 +1126,28 @@ static fea_status build_blocks(fea_ctx c, bool v5, bool orient, int64_t e_max, i
             F.r0 = (int32_t)ga;
             F.nr = (int32_t)(gb - ga);
             const int32_t nEp = fea_pad4(F.nE);
-            o.dofs.assign((size_t)np * nEp, 0);
-            for (int64_t le = 0; le < (int64_t)E.size(); ++le)
-                for (int i = 0; i < np; ++i) o.dofs[i * nEp + le] = c->ed[(size_t)E[le] * np + i];
+            const int32_t net = (F.nE + 7) / 8;
+            // DOFs [np][nEp] in column order (relabelled: new local k = old sigma^-1(k)), then v6's
+            // row-tile mask of every 8-element column tile [net]
+            o.dofs.assign((size_t)np * nEp + (v6 ? net : 0), 0);
+            for (int64_t le0 = 0; le0 < (int64_t)E.size(); ++le0) {
+                const int* si = siginv[(int)rot[le0]];
+                for (int k = 0; k < np; ++k) o.dofs[k * nEp + newpos[le0]] = c->ed[(size_t)E[le0] * np + si[k]];
+            }
             for (int64_t le = E.size(); le < nEp; ++le)
                 for (int i = 0; i < np; ++i) o.dofs[i * nEp + le] = o.dofs[i * nEp];
+            if (v6) {
+                int64_t w = 0;
+                for (int32_t et = 0; et < net; ++et) {
+                    uint32_t m = 0;
+                    for (int64_t le0 = 0; le0 < (int64_t)E.size(); ++le0)
+                        if (newpos[le0] / 8 == et) m |= emask[le0];
+                    o.dofs[(size_t)np * nEp + et] = (int32_t)m;
+                    w += __builtin_popcount(m);
+                }
+                skip_work += w;
+                skip_full += (int64_t)net * NTT6;
+            }
             return;
         }
         // items: slots sorted by (count, slot); classes of equal count
@@ -1190,6 +1298,10 @@ static fea_status build_blocks(fea_ctx c, bool v5, bool orient, int64_t e_max, i
     P.owned = owned;
     P.ncon = ncon;
     P.rbytes = rbytes;
+    if (v6) {
+        c->skip_work = skip_work;
+        c->skip_full = skip_full;
+    }
     ptime("plan: concatenate");
     return FEA_OK;
 }
@@ -1902,6 +2014,7 @@ fea_status fea_get_stat(fea_ctx c, int key, int64_t* value) {
         case 13: *value = c->have_tplan ? c->t_grid : -1; break;
         case 14: *value = c->maxI; break;
         case 15: *value = c->n_int; break;
+        case 38: *value = c->skip_full ? 1000 * c->skip_work / c->skip_full : 1000; break;  // v6 A2 row-tile work, per mille
     }
     return FEA_OK;
 }

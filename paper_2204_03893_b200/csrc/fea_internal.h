@@ -321,7 +321,7 @@ __host__ __device__ constexpr int fea6_na(int p) { return p == 4 ? (FEA6_P4_MERG
 __host__ __device__ constexpr int fea6_rt(int p) { return p == 4 && !FEA6_P4_MERGED ? 2 : 1; }
 __host__ __device__ constexpr int fea6_threads(int p) { return (fea6_na(p) + fea6_nb(p) + 1) * 32; }
 // producer rounds (elements le = 32 h + lane, h < rounds): caps e_max at 32 * rounds
-__host__ __device__ constexpr int fea6_prod_rounds(int p) { return p == 4 ? 2 : 4; }
+__host__ __device__ constexpr int fea6_prod_rounds(int p) { return p == 4 ? 2 : 3; }
 // Lambda / gathered-u row stride (doubles): == 4 (mod 16), so the DMMA B-fragment loads
 // [(4 kk + c) ls + 8 et + g] are conflict-free per half-warp
 __host__ __device__ inline int32_t fea6_lstride(int32_t e_max) { return e_max + ((4 - e_max) % 16 + 16) % 16; }
@@ -337,8 +337,9 @@ __host__ __device__ inline int32_t fea6_vstride(int32_t e_max) { return e_max + 
 // 32, 48 or 64: C <= 30).  Lane l of a warp handles slot 32 k + l of class A, so its CSR stores
 // are contiguous.
 // Shared memory (byte offsets / per-buffer bytes): V [2][T][vs] cells; GU [2][np][ls] gathered u;
-// GW [2][4][e_max] (|det B_e|, A00, A11, A01 from the producer); LW [3] Lambda [nqp][ls] then
-// W [3][e_max] (A1's copy for A2); mbarriers.
+// GW [2][4][e_max] (|det B_e|, A00, A11, A01 from the producer); LW [3] Lambda [nqp][ls], W [3][e_max]
+// and the row-tile masks of the column tiles (int32 [32], from the producer); mbarriers.
+// Block DOF arrays (v6): [n_p][pad4(nE)] then the row-tile mask of every 8-element column tile.
 enum { FEA6_L_V = 0, FEA6_L_VB = 1, FEA6_L_GU = 2, FEA6_L_GUB = 3, FEA6_L_GW = 4, FEA6_L_GWB = 5, FEA6_L_LW = 6,
        FEA6_L_LWB = 7, FEA6_L_PF = 8, FEA6_L_BARS = 10, FEA6_L_TOTAL = 11 };
 __host__ __device__ inline void fea6_smem_layout(int32_t* L, int e_max, int p, int do_m, int do_c) {
@@ -353,7 +354,7 @@ __host__ __device__ inline void fea6_smem_layout(int32_t* L, int e_max, int p, i
     L[FEA6_L_GU] = o; o += 2 * L[FEA6_L_GUB];
     L[FEA6_L_GWB] = fea_align(8 * 4 * e_max, 128);
     L[FEA6_L_GW] = o; o += 2 * L[FEA6_L_GWB];
-    L[FEA6_L_LWB] = fea_align(8 * (nqp * ls + 3 * e_max), 128);
+    L[FEA6_L_LWB] = fea_align(8 * (nqp * ls + 3 * e_max) + 4 * 32, 128);  // + the column tiles' row-tile masks
     L[FEA6_L_LW] = o; o += 3 * L[FEA6_L_LWB];  // three Lambda / W buffers (A1 runs two blocks ahead)
     L[FEA6_L_PF] = o; o += fea_align(8 * ((nqp + 7) / 8) * fea_kt(p) * 32, 128);  // Phi^T A-fragments (A1)
     L[FEA6_L_BARS] = o; o += 14 * 8;

@@ -132,6 +132,8 @@ __global__ void __launch_bounds__(fea6_threads(P), 1) k_reassemble6(const __grid
         int32_t dn[PR][NP];
         int nE_c = 0, nE_n = 0, nEp_n = 0;
         const int32_t* gd_n = nullptr;
+        const int32_t* gmask = nullptr;  // row-tile masks of the block being gathered
+        const int32_t* gmask_n = nullptr;
         auto load_desc = [&](int k) {
             const FeaBlock* B = prm.blocks + b0 + k * G;
             nE_n = ldg_s32(&B->nE);
@@ -139,6 +141,7 @@ __global__ void __launch_bounds__(fea6_threads(P), 1) k_reassemble6(const __grid
         };
         auto load_dofs = [&]() {  // the DOFs of the block whose descriptor load_desc fetched
             nEp_n = fea_pad4(nE_n);
+            gmask_n = gd_n + NP * nEp_n;
 #pragma unroll
             for (int h = 0; h < PR; ++h)
 #pragma unroll
@@ -149,6 +152,7 @@ __global__ void __launch_bounds__(fea6_threads(P), 1) k_reassemble6(const __grid
             load_desc(0);
             load_dofs();
             nE_c = nE_n;
+            gmask = gmask_n;
             if (nb > 1) load_desc(1);
         }
         T6_DECL
@@ -161,6 +165,7 @@ __global__ void __launch_bounds__(fea6_threads(P), 1) k_reassemble6(const __grid
             if (j >= 3) mbar_wait(&lam_free[l3], (uint32_t)(((j / 3) - 1) & 1));  // W goes to LW[j % 3]
             T6_TICK(0)
             const int nE = nE_c;
+            const int32_t* gmask_j = gmask;
             FEA_CHECK(nE >= 1 && nE <= e_max);
             double* gu = sGU(g);
             double* gw = sGW(g);
@@ -184,6 +189,7 @@ __global__ void __launch_bounds__(fea6_threads(P), 1) k_reassemble6(const __grid
             if (j + 1 < nb) {  // the next block's DOFs (registers dn are free again), its successor's descriptor
                 load_dofs();
                 nE_c = nE_n;
+                gmask = gmask_n;
                 if (j + 2 < nb) load_desc(j + 2);
             }
 #pragma unroll
@@ -202,6 +208,8 @@ __global__ void __launch_bounds__(fea6_threads(P), 1) k_reassemble6(const __grid
             }
             for (int le = nE + lane; le < ((nE + 7) & ~7); le += 32)  // padding columns of the last tile
                 W[le] = W[e_max + le] = W[2 * e_max + le] = 0.0;
+            if (lane < ((nE + 7) >> 3))  // the column tiles' row-tile masks (ghost row skipping)
+                reinterpret_cast<int32_t*>(W + 3 * e_max)[lane] = ldg_s32(gmask_j + lane);
             warp_arrive(&gat_full[g], lane);     // the geometry stores
             T6_TICK(1)
         }
@@ -416,6 +424,7 @@ __global__ void __launch_bounds__(fea6_threads(P), 1) k_reassemble6(const __grid
             for (int et = 0; et < net_a2; ++et) {
                 // (units to the last warps first: warp NA - 1 holds one row tile less)
                 if (A1MODE == 2 && et == (net >> 1) && j + 1 < nb) do_a1(j + 1, NA - 1 - warp, NA, nE_n);
+                const uint32_t tmask = reinterpret_cast<const uint32_t*>(W + 3 * e_max)[et];  // row tiles needed
                 const int col = et * 8 + g8, le0 = et * 8 + 2 * cq;
                 double bl[NK];
 #pragma unroll
@@ -423,7 +432,7 @@ __global__ void __launch_bounds__(fea6_threads(P), 1) k_reassemble6(const __grid
 #pragma unroll
                 for (int r = 0; r < RT; ++r) {  // row tiles one after the other (fused: measured slower)
                     const int tt = warp + r * NA;
-                    if (RT > 1 && tt >= NTT) continue;
+                    if ((RT > 1 && tt >= NTT) || !((tmask >> tt) & 1u)) continue;  // (ghost rows nobody reads)
                     double m0 = 0.0, m1 = 0.0, a0 = 0.0, a1 = 0.0, p0 = 0.0, p1 = 0.0, c0 = 0.0, c1 = 0.0;
 #pragma unroll
                     for (int kk = 0; kk < NK; ++kk) {

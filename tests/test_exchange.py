@@ -79,6 +79,7 @@ def test_fake_world_interface_exchange_bit_identical(name, N, world):
 
     def setup(ctx):
         ctx.set_tuning(4, cfg.which)
+        ctx.set_tuning(12, 0)  # bit-identity across worlds needs the same element labelling (no v6 skipping)
         ctx.build_pattern()
         ctx.set_coefficient(FEA_MASS, *coef)
         ctx.set_coefficient(FEA_STIFF, *coef)
