@@ -148,6 +148,7 @@ struct fea_ctx_s {
     int tune_skip = 1;     // v6: ghost row-tile skipping with element rotations (FEA_TUNE_SKIP)
     bool rule_sym = false; // the rule (of both matrices) is invariant under the 6 vertex permutations
     int64_t skip_work = 0, skip_full = 0;  // v6 plan: A2 row-tile work with / without skipping
+    int64_t skip_crit = 0;                 // v6 plan: sum over blocks of NA x the busiest A warp's row-tile work
     int tune_tker = 0;     // tensor kernel: 0 = automatic, 1 = k_tensor, 4 = k_tensor4 (FEA_TUNE_TENSOR_KERNEL)
     int tune_overlap = 1;  // world > 1: interior blocks assemble while u is exchanged (FEA_TUNE_OVERLAP)
     int n_int = 0;         // interior blocks (first n_int of the plan when world > 1)
@@ -963,7 +964,9 @@ static fea_status build_blocks(fea_ctx c, bool v5, bool orient, int64_t e_max, i
         }
     }
     const int NTT6 = (T + 7) / 8;
-    std::atomic<int64_t> skip_work(0), skip_full(0);
+    std::atomic<int64_t> skip_work(0), skip_full(0), skip_crit(0);
+    std::atomic<int64_t> tile_use[32];
+    for (auto& x : tile_use) x = 0;
     // ---- per block: element set, (row, col) records sorted -> slots, contributors, record
     struct BOut {
         std::vector<int32_t> rownnz, cols, dofs;
@@ -1137,15 +1140,21 @@ static fea_status build_blocks(fea_ctx c, bool v5, bool orient, int64_t e_max, i
             for (int64_t le = E.size(); le < nEp; ++le)
                 for (int i = 0; i < np; ++i) o.dofs[i * nEp + le] = o.dofs[i * nEp];
             if (v6) {
-                int64_t w = 0;
+                int64_t w = 0, ww[32] = {0};
+                const int na = fea6_na(c->order);
                 for (int32_t et = 0; et < net; ++et) {
                     uint32_t m = 0;
                     for (int64_t le0 = 0; le0 < (int64_t)E.size(); ++le0)
                         if (newpos[le0] / 8 == et) m |= emask[le0];
                     o.dofs[(size_t)np * nEp + et] = (int32_t)m;
                     w += __builtin_popcount(m);
+                    for (int tt = 0; tt < NTT6; ++tt) {
+                        ww[tt % na] += (m >> tt) & 1u;
+                        tile_use[tt] += (m >> tt) & 1u;
+                    }
                 }
                 skip_work += w;
+                skip_crit += na * *std::max_element(ww, ww + na);
                 skip_full += (int64_t)net * NTT6;
             }
             return;
@@ -1301,6 +1310,12 @@ static fea_status build_blocks(fea_ctx c, bool v5, bool orient, int64_t e_max, i
     if (v6) {
         c->skip_work = skip_work;
         c->skip_full = skip_full;
+        c->skip_crit = skip_crit;
+        if (getenv("FEA_PLAN_TIMING")) {
+            fprintf(stderr, "[plan] v6 row-tile use:");
+            for (int tt = 0; tt < NTT6; ++tt) fprintf(stderr, " %lld", (long long)tile_use[tt].load());
+            fprintf(stderr, "\n");
+        }
     }
     ptime("plan: concatenate");
     return FEA_OK;
@@ -2015,6 +2030,7 @@ fea_status fea_get_stat(fea_ctx c, int key, int64_t* value) {
         case 14: *value = c->maxI; break;
         case 15: *value = c->n_int; break;
         case 38: *value = c->skip_full ? 1000 * c->skip_work / c->skip_full : 1000; break;  // v6 A2 row-tile work, per mille
+        case 39: *value = c->skip_work ? 1000 * c->skip_crit / c->skip_work : 1000; break;  // v6 A-warp imbalance, per mille
     }
     return FEA_OK;
 }

@@ -320,6 +320,34 @@ __host__ __device__ constexpr bool fea6_supported(int p, int nq) { return p >= 3
 __host__ __device__ constexpr int fea6_na(int p) { return p == 4 ? (FEA6_P4_MERGED ? 15 : 8) : 7; }
 __host__ __device__ constexpr int fea6_rt(int p) { return p == 4 && !FEA6_P4_MERGED ? 2 : 1; }
 __host__ __device__ constexpr int fea6_threads(int p) { return (fea6_na(p) + fea6_nb(p) + 1) * 32; }
+// row tile tt of Q held by A warp w as its r-th tile (-1: none).  FEA6_TILEMAP 0: tt = w + r NA.
+// 1 (default): balanced by the measured frequency with which each tile survives ghost row-tile
+// skipping (tools/plan_stats.py with FEA_PLAN_TIMING; C5: tiles 0, 1 in 2.06 M column tiles, tiles
+// 11-14 in 1.21 M).  P4: balanced per WARP (the A warps meet once per block at the Lambda barrier
+// and one warp issues at most one DMMA per 16 clk), then per SMSP (warp w on SMSP w % 4), A1's
+// element tiles counted on warps 2-7: busiest warp / mean 1.19 -> 1.08 (a per-SMSP-only balance,
+// 1.09 -> 1.004, left one warp with tiles 0 and 1 and measured C5 12.32 -> 12.74 ms).  P3 (one
+// tile per warp, 7 warps on 4 SMSPs): per SMSP 1.26 -> 1.16, C3 1.505 -> 1.466 ms.
+// phase-B item registers per lane: 2 x FEA6_U(p) class-A items (chunks) in flight per warp
+// (measured: P3 12 vs 8: C3 1.460 -> 1.418 ms; P4 8 vs 12: C5 12.17 vs 12.39 ms)
+#ifndef FEA6_U
+#define FEA6_U(p) ((p) == 3 ? 12 : 8)
+#endif
+#ifndef FEA6_TILEMAP
+#define FEA6_TILEMAP 1
+#endif
+__host__ __device__ constexpr int fea6_tile(int p, int w, int r) {
+    if (!FEA6_TILEMAP || (p == 4 && FEA6_P4_MERGED)) {
+        const int na = p == 4 ? (FEA6_P4_MERGED ? 15 : 8) : 7, ntt = p == 4 ? 15 : 7;
+        return w + r * na < ntt ? w + r * na : -1;
+    }
+    // one nibble per (w, r), 15 = none (ALU only: w is a run-time value)
+    // P4: w0 {6, 7} w1 {0, 11} w2 {8, 14} w3 {3, 10} w4 {2, 12} w5 {4, 9} w6 {5, 13} w7 {1}
+    // P3: w0..w6 = 0, 1, 3, 2, 5, 6, 4
+    const unsigned long long M4 = 0xF1D594C2A3E8B076ull, M3 = 0x4652310ull;
+    const int x = p == 4 ? (int)((M4 >> (4 * (2 * w + r))) & 15) : (r == 0 ? (int)((M3 >> (4 * w)) & 15) : 15);
+    return x == 15 ? -1 : x;
+}
 // producer rounds (elements le = 32 h + lane, h < rounds): caps e_max at 32 * rounds
 __host__ __device__ constexpr int fea6_prod_rounds(int p) { return p == 4 ? 2 : 3; }
 // Lambda / gathered-u row stride (doubles): == 4 (mod 16), so the DMMA B-fragment loads

@@ -68,6 +68,7 @@ __global__ void __launch_bounds__(fea6_threads(P), 1) k_reassemble6(const __grid
 #endif
     constexpr int oW = (NP * NQ + 1) & ~1;
     static_assert(NA * RT >= NTT, "row tiles");
+    static_assert(fea6_tile(P, 0, 0) >= 0, "tile map");
     const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
     const int e_max = prm.e_max, ls = fea6_lstride(e_max), vs = fea6_vstride(e_max);
     const int G = gridDim.x, b0 = blockIdx.x;
@@ -283,13 +284,17 @@ __global__ void __launch_bounds__(fea6_threads(P), 1) k_reassemble6(const __grid
     // class B: one item per thread.  With nearly all shared memory in use the L1 holds ~1 KB, so
     // every global read is an L2 round trip: the next phase B's descriptor and first items are
     // loaded (prefetchB) right after the current one.
-    constexpr int U = 8;
+    constexpr int U = FEA6_U(P);
     struct BState {
         int nslots, ncls, rB, nch;
         int64_t slot0;
         const uint8_t* rec;
         uint32_t wa[U], wb[U];
         uint4 ib;
+    };
+    struct BDesc {  // the next phase B's block descriptor, loaded one block ahead of its items
+        int nslots, ncls, rB;
+        int64_t slot0, rec_off, rec_bytes;
     };
     auto loadA = [&](const BState& st, uint32_t (&w)[U], int c0, int nbw) {
         const uint32_t* ia = reinterpret_cast<const uint32_t*>(st.rec);
@@ -299,22 +304,32 @@ __global__ void __launch_bounds__(fea6_threads(P), 1) k_reassemble6(const __grid
             w[u] = ch < st.nch ? ldg_u32(ia + ch * 32 + lane) : 0xffffffffu;
         }
     };
-    auto prefetchB = [&](BState& st, int jb, int bt, int bw, int nbw) {
+    auto loadD = [&](BDesc& d, int jb) {
+        if (jb >= nb) return;
         const FeaBlock* B = prm.blocks + b0 + jb * G;
-        st.nslots = __ldg(&B->nslots);
-        st.ncls = __ldg(&B->ncls);
-        st.rB = __ldg(&B->pad_);
-        st.slot0 = __ldg(&B->slot0);
-        st.rec = prm.records + __ldg(&B->rec_off);
+        d.nslots = __ldg(&B->nslots);
+        d.ncls = __ldg(&B->ncls);
+        d.rB = __ldg(&B->pad_);
+        d.slot0 = __ldg(&B->slot0);
+        d.rec_off = __ldg(&B->rec_off);
+        d.rec_bytes = __ldg(&B->rec_bytes);
+    };
+    // items of block jb (descriptor d, loaded earlier), then the descriptor of block jb + 1 into d
+    auto prefetchB = [&](BState& st, BDesc& d, int jb, int bt, int bw, int nbw) {
+        st.nslots = d.nslots;
+        st.ncls = d.ncls;
+        st.rB = d.rB;
+        st.slot0 = d.slot0;
+        st.rec = prm.records + d.rec_off;
         st.nch = (st.nslots + 31) >> 5;
-        FEA_CHECK(st.slot0 >= 0 && st.slot0 + st.nslots <= prm.n_slots &&
-                  __ldg(&B->rec_off) + __ldg(&B->rec_bytes) <= prm.rec_size);
-        FEA_CHECK(4 * 32 * st.nch + (int64_t)st.ncls * st.rB <= __ldg(&B->rec_bytes));
+        FEA_CHECK(st.slot0 >= 0 && st.slot0 + st.nslots <= prm.n_slots && d.rec_off + d.rec_bytes <= prm.rec_size);
+        FEA_CHECK(4 * 32 * st.nch + (int64_t)st.ncls * st.rB <= d.rec_bytes);
         loadA(st, st.wa, bw, nbw);
         loadA(st, st.wb, bw + U * nbw, nbw);
         st.ib = make_uint4(0, 0, 0, 0);
         if (bt < st.ncls)
             st.ib = __ldg(reinterpret_cast<const uint4*>(st.rec + 4 * ((st.nslots + 31) & ~31) + (size_t)bt * st.rB));
+        loadD(d, jb + 1);
     };
     auto phaseB = [&](BState& st, int jb, int bt, int bw, int nbw) {
         const int g = jb & 1;
@@ -389,22 +404,29 @@ __global__ void __launch_bounds__(fea6_threads(P), 1) k_reassemble6(const __grid
     if (warp < NA) {
         // ------------------------------------------------------------------ A warps: A2
         const int g8 = lane >> 2, cq = lane & 3;
-        double afr[RT][4][NK];  // this warp's row tiles warp, warp + NA, ... of Q_f (f = m, A00, A11, A01)
+        double afr[RT][4][NK];  // this warp's row tiles fea6_tile(P, warp, r) of Q_f (f = m, A00, A11, A01)
+        int tts[RT];
+#pragma unroll
+        for (int r = 0; r < RT; ++r) tts[r] = fea6_tile(P, warp, r);
 #pragma unroll
         for (int r = 0; r < RT; ++r)
 #pragma unroll
             for (int f = 0; f < 4; ++f)
 #pragma unroll
                 for (int kk = 0; kk < NK; ++kk) {
-                    const int tt = warp + r * NA;
-                    afr[r][f][kk] = (f == 0 ? DO_M : DO_C) && tt < NTT
+                    const int tt = tts[r];
+                    afr[r][f][kk] = (f == 0 ? DO_M : DO_C) && tt >= 0 && tt < NTT
                                         ? __ldg(prm.qfrag + ((f * NTT + tt) * NK + kk) * 32 + lane) : 0.0;
                 }
         T6_DECL
         int nE_n = nb > 0 ? ldg_s32(&prm.blocks[b0].nE) : 0;  // one block ahead (L2 latency; asm volatile: issued here)
         if (A1MODE == 2 && nb > 0) do_a1(0, NA - 1 - warp, NA, nE_n);
         BState st;  // NB == 0: the A warps also run phase B (of the previous block, after their A2)
-        if (NB == 0 && nb > 0) prefetchB(st, 0, tid, warp, NA);
+        BDesc bd;
+        if (NB == 0 && nb > 0) {
+            loadD(bd, 0);
+            prefetchB(st, bd, 0, tid, warp, NA);
+        }
         for (int j = 0; j < nb; ++j) {
             const int g = j & 1;
             const int nE = nE_n;
@@ -431,8 +453,8 @@ __global__ void __launch_bounds__(fea6_threads(P), 1) k_reassemble6(const __grid
                 for (int kk = 0; kk < NK; ++kk) bl[kk] = Lam[(kk * 4 + cq) * ls + col];
 #pragma unroll
                 for (int r = 0; r < RT; ++r) {  // row tiles one after the other (fused: measured slower)
-                    const int tt = warp + r * NA;
-                    if ((RT > 1 && tt >= NTT) || !((tmask >> tt) & 1u)) continue;  // (ghost rows nobody reads)
+                    const int tt = tts[r];
+                    if (tt < 0 || !((tmask >> tt) & 1u)) continue;  // (ghost rows nobody reads)
                     double m0 = 0.0, m1 = 0.0, a0 = 0.0, a1 = 0.0, p0 = 0.0, p1 = 0.0, c0 = 0.0, c1 = 0.0;
 #pragma unroll
                     for (int kk = 0; kk < NK; ++kk) {
@@ -474,7 +496,7 @@ __global__ void __launch_bounds__(fea6_threads(P), 1) k_reassemble6(const __grid
             }
             if (NB == 0 && j >= 1) {
                 phaseB(st, j - 1, tid, warp, NA);
-                prefetchB(st, j, tid, warp, NA);
+                prefetchB(st, bd, j, tid, warp, NA);
                 T6_TICK(6)
             }
         }
@@ -490,7 +512,11 @@ __global__ void __launch_bounds__(fea6_threads(P), 1) k_reassemble6(const __grid
         constexpr int LAG = A1MODE == 2 ? 0 : 2;  // phase B of block j - LAG after A1(j) (B warps running A1)
         int nE_a = nb > 0 ? ldg_s32(&prm.blocks[b0].nE) : 0;  // A1's block size, one block ahead
         BState st;
-        if (nb > 0) prefetchB(st, 0, bt, bw, NB);
+        BDesc bd;
+        if (nb > 0) {
+            loadD(bd, 0);
+            prefetchB(st, bd, 0, bt, bw, NB);
+        }
         T6_DECL
         for (int j = 0; j < nb + LAG; ++j) {
             if (A1MODE == 0 && j < nb) {
@@ -503,7 +529,7 @@ __global__ void __launch_bounds__(fea6_threads(P), 1) k_reassemble6(const __grid
             T6_TICK(0)
             phaseB(st, j - LAG, bt, bw, NB);
             T6_TICK(2)
-            if (j - LAG + 1 < nb) prefetchB(st, j - LAG + 1, bt, bw, NB);
+            if (j - LAG + 1 < nb) prefetchB(st, bd, j - LAG + 1, bt, bw, NB);
             T6_TICK(7)
         }
         T6_FLUSH(8)
