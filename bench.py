@@ -402,8 +402,8 @@ def run_ours(args):
             if asm.ctx.stat(11) == 5:  # per-warp timeline of k_reassemble5 (lane 0 of every warp)
                 names = ["compute", "move_refill", "full_wait", "rec_wait", "phaseB", "free_wait", "prologue"]
             elif asm.ctx.stat(11) == 6:  # k_reassemble6: summed over the warps of each role
-                names = ["A_gather_wait", "A_A1", "A_barrier", "A_vfree_wait", "A_A2", "A_loop", "A6", "A7",
-                         "B_setup", "B_vfull_wait", "B_classA", "B_classB", "B4", "B5", "B6", "B7"]
+                names = ["A_lamfull_wait", "A_A1", "A2_", "A_vfree_wait", "A_A2", "A_loop", "A_phaseB", "A7_",
+                         "B_loop", "B_vfull_wait", "B_phaseB", "B3_", "B4_", "B5_", "B_A1", "B_prefetch"]
                 ph = [asm.ctx.stat(20 + i) for i in range(16)] + [asm.ctx.stat(40 + i) for i in range(2)]
                 desc["phase_cycles"] = dict(zip(names + ["P_free_wait", "P_gather"], ph))
                 names = []

@@ -304,6 +304,10 @@ int fea_kernel_occupancy5(int order, int do_m, int do_c, int smem_bytes, int* ct
 // where A1 runs: 2 = on the A warps, in the middle of A2 of the previous block (P4: the contraction
 // dominates and the A warps' DMMA work hides A1's latency); 0 = on the phase-B warps, two blocks
 // ahead of their phase B (P3: measured faster, C3 1.51 vs 1.61 ms)
+#ifndef FEA6_A1POS
+#define FEA6_A1POS 0  // A1MODE 2: a warp's A1 unit at column tile (net * A1POS) / 4 of A2
+                      // (C5: 0 11.76 ms, 1 12.00, 2 12.20, 3 12.32; A1 on the B warps 13.21)
+#endif
 #ifndef FEA6_A1MODE
 #define FEA6_A1MODE(p) ((p) == 4 ? 2 : 0)
 #endif

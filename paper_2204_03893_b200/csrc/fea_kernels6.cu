@@ -443,9 +443,16 @@ __global__ void __launch_bounds__(fea6_threads(P), 1) k_reassemble6(const __grid
             uint8_t* Vb = sV(g);
             const int net_a2 = DBGM && (prm.dbg_mode & 4) ? 0 : net;  // diagnostics: A2 skipped
             if (DBGM && (prm.dbg_mode & 4) && A1MODE == 2 && j + 1 < nb) do_a1(j + 1, NA - 1 - warp, NA, nE_n);
+            // A1(j + 1) inside A2(j): a warp with an A1 unit runs it at column tile a1_at (FEA6_A1POS
+            // quarters of the block), a warp without one only arrives, at the start
+            const int a1_at = NA - 1 - warp < ((nE_n + 7) >> 3) ? (net * FEA6_A1POS) >> 2 : 0;
             for (int et = 0; et < net_a2; ++et) {
                 // (units to the last warps first: warp NA - 1 holds one row tile less)
-                if (A1MODE == 2 && et == (net >> 1) && j + 1 < nb) do_a1(j + 1, NA - 1 - warp, NA, nE_n);
+                if (A1MODE == 2 && et == a1_at && j + 1 < nb) {
+                    T6_TICK(4)
+                    do_a1(j + 1, NA - 1 - warp, NA, nE_n);
+                    T6_TICK(1)
+                }
                 const uint32_t tmask = reinterpret_cast<const uint32_t*>(W + 3 * e_max)[et];  // row tiles needed
                 const int col = et * 8 + g8, le0 = et * 8 + 2 * cq;
                 double bl[NK];
@@ -527,6 +534,8 @@ __global__ void __launch_bounds__(fea6_threads(P), 1) k_reassemble6(const __grid
             }
             if (j < LAG) continue;
             T6_TICK(0)
+            mbar_wait(&v_full[(j - LAG) & 1], (uint32_t)(((j - LAG) >> 1) & 1));  // (again in phaseB: returns at once)
+            T6_TICK(1)
             phaseB(st, j - LAG, bt, bw, NB);
             T6_TICK(2)
             if (j - LAG + 1 < nb) prefetchB(st, bd, j - LAG + 1, bt, bw, NB);
