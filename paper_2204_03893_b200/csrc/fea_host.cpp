@@ -1141,7 +1141,11 @@ static fea_status build_blocks(fea_ctx c, bool v5, bool orient, int64_t e_max, i
                 for (int i = 0; i < np; ++i) o.dofs[i * nEp + le] = o.dofs[i * nEp];
             if (v6) {
                 int64_t w = 0, ww[32] = {0};
-                const int na = fea6_na(c->order);
+                const int na = fea6_na(c->order), rt = fea6_rt(c->order);
+                int own[32];  // the A warp holding each row tile (the kernel's map)
+                for (int wq = 0; wq < na; ++wq)
+                    for (int r = 0; r < rt; ++r)
+                        if (fea6_tile(c->order, wq, r) >= 0) own[fea6_tile(c->order, wq, r)] = wq;
                 for (int32_t et = 0; et < net; ++et) {
                     uint32_t m = 0;
                     for (int64_t le0 = 0; le0 < (int64_t)E.size(); ++le0)
@@ -1149,7 +1153,7 @@ static fea_status build_blocks(fea_ctx c, bool v5, bool orient, int64_t e_max, i
                     o.dofs[(size_t)np * nEp + et] = (int32_t)m;
                     w += __builtin_popcount(m);
                     for (int tt = 0; tt < NTT6; ++tt) {
-                        ww[tt % na] += (m >> tt) & 1u;
+                        ww[own[tt]] += (m >> tt) & 1u;
                         tile_use[tt] += (m >> tt) & 1u;
                     }
                 }

@@ -304,6 +304,12 @@ int fea_kernel_occupancy5(int order, int do_m, int do_c, int smem_bytes, int* ct
 // where A1 runs: 2 = on the A warps, in the middle of A2 of the previous block (P4: the contraction
 // dominates and the A warps' DMMA work hides A1's latency); 0 = on the phase-B warps, two blocks
 // ahead of their phase B (P3: measured faster, C3 1.51 vs 1.61 ms)
+#ifndef FEA6_PROD_ASYNC
+// v6 producer: 1 = coordinates by cp.async into the gather stage, geometry one block late (P4);
+// 0 = coordinates in registers, geometry of the block in its own iteration (P3: its 3-round
+// stages would cost e_max 96 -> 88 of shared memory)
+#define FEA6_PROD_ASYNC(p) ((p) == 4)
+#endif
 #ifndef FEA6_A1POS
 #define FEA6_A1POS 0  // A1MODE 2: a warp's A1 unit at column tile (net * A1POS) / 4 of A2
                       // (C5: 0 11.76 ms, 1 12.00, 2 12.20, 3 12.32; A1 on the B warps 13.21)
@@ -321,9 +327,20 @@ int fea_kernel_occupancy5(int order, int do_m, int do_c, int smem_bytes, int* ct
 #endif
 __host__ __device__ constexpr int fea6_nb(int p) { return p == 4 && FEA6_P4_MERGED ? 0 : FEA6_NB; }
 __host__ __device__ constexpr bool fea6_supported(int p, int nq) { return p >= 3 && nq == fea_nq_native(p); }
-__host__ __device__ constexpr int fea6_na(int p) { return p == 4 ? (FEA6_P4_MERGED ? 15 : 8) : 7; }
-__host__ __device__ constexpr int fea6_rt(int p) { return p == 4 && !FEA6_P4_MERGED ? 2 : 1; }
+// P4 A warps: 8 with two row tiles each (default), or (FEA6_P4_NA15) 15 with one row tile each
+// -- four A warps per SM sub-partition keep the FP64 pipe fed while some of them run their
+// epilogue, A1 or wait at a barrier; the CTA then has 23 warps and 88 registers per thread
+#ifndef FEA6_P4_NA15
+#define FEA6_P4_NA15 0
+#endif
+__host__ __device__ constexpr int fea6_na(int p) { return p == 4 ? (FEA6_P4_MERGED || FEA6_P4_NA15 ? 15 : 8) : 7; }
+__host__ __device__ constexpr int fea6_rt(int p) { return p == 4 && !FEA6_P4_MERGED && !FEA6_P4_NA15 ? 2 : 1; }
 __host__ __device__ constexpr int fea6_threads(int p) { return (fea6_na(p) + fea6_nb(p) + 1) * 32; }
+// registers per thread: each SM sub-partition holds 16384 registers for its ceil(warps / 4) warps
+// (warp w on SMSP w % 4), in allocation units of 8
+__host__ __device__ constexpr int fea6_maxnreg(int p) {
+    return 16384 / (32 * ((fea6_threads(p) / 32 + 3) / 4)) / 8 * 8 > 128 ? 128 : 16384 / (32 * ((fea6_threads(p) / 32 + 3) / 4)) / 8 * 8;
+}
 // row tile tt of Q held by A warp w as its r-th tile (-1: none).  FEA6_TILEMAP 0: tt = w + r NA.
 // 1 (default): balanced by the measured frequency with which each tile survives ghost row-tile
 // skipping (tools/plan_stats.py with FEA_PLAN_TIMING; C5: tiles 0, 1 in 2.06 M column tiles, tiles
@@ -348,8 +365,10 @@ __host__ __device__ constexpr int fea6_tile(int p, int w, int r) {
     // one nibble per (w, r), 15 = none (ALU only: w is a run-time value)
     // P4: w0 {6, 7} w1 {0, 11} w2 {8, 14} w3 {3, 10} w4 {2, 12} w5 {4, 9} w6 {5, 13} w7 {1}
     // P3: w0..w6 = 0, 1, 3, 2, 5, 6, 4
-    const unsigned long long M4 = 0xF1D594C2A3E8B076ull, M3 = 0x4652310ull;
-    const int x = p == 4 ? (int)((M4 >> (4 * (2 * w + r))) & 15) : (r == 0 ? (int)((M3 >> (4 * w)) & 15) : 15);
+    // P4 with 15 A warps (per SMSP, A1 on warps 9-14): w0..w14 = 9 12 5 0 2 6 11 3 10 8 13 1 4 14 7
+    const unsigned long long M4 = 0xF1D594C2A3E8B076ull, M3 = 0x4652310ull, M15 = 0x7E41D8A3B6205C9ull;
+    const int x = p == 4 ? (FEA6_P4_NA15 ? (r == 0 ? (int)((M15 >> (4 * w)) & 15) : 15) : (int)((M4 >> (4 * (2 * w + r))) & 15))
+                         : (r == 0 ? (int)((M3 >> (4 * w)) & 15) : 15);
     return x == 15 ? -1 : x;
 }
 // producer rounds (elements le = 32 h + lane, h < rounds): caps e_max at 32 * rounds
@@ -384,7 +403,7 @@ __host__ __device__ inline void fea6_smem_layout(int32_t* L, int e_max, int p, i
     L[FEA6_L_V] = o; o += 2 * L[FEA6_L_VB];
     L[FEA6_L_GUB] = fea_align(8 * np * ls, 128);
     L[FEA6_L_GU] = o; o += 2 * L[FEA6_L_GUB];
-    L[FEA6_L_GWB] = fea_align(8 * 4 * e_max, 128);
+    L[FEA6_L_GWB] = fea_align((FEA6_PROD_ASYNC(p) ? 56 : 8) * e_max, 128);  // [coordinates [3][e_max] double2,] |det B_e| [e_max]
     L[FEA6_L_GW] = o; o += 2 * L[FEA6_L_GWB];
     L[FEA6_L_LWB] = fea_align(8 * (nqp * ls + 3 * e_max) + 4 * 32, 128);  // + the column tiles' row-tile masks
     L[FEA6_L_LW] = o; o += 3 * L[FEA6_L_LWB];  // three Lambda / W buffers (A1 runs two blocks ahead)

@@ -53,7 +53,7 @@ __device__ __forceinline__ void warp_arrive(uint64_t* bar, int lane) {
 #define T6_FLUSH(base) if constexpr (DIAG) { if (prm.dbg && lane == 0) for (int k_ = 0; k_ < 8; ++k_) atomicAdd(prm.dbg + (base) + k_, t6acc[k_]); }
 
 template <int P, bool DO_M, bool DO_C, bool DIAG>
-__global__ void __launch_bounds__(fea6_threads(P), 1) k_reassemble6(const __grid_constant__ FeaKParams prm) {
+__global__ void __maxnreg__(fea6_maxnreg(P)) k_reassemble6(const __grid_constant__ FeaKParams prm) {
     constexpr int NP = fea_np(P), T = fea_T(P), NTT = fea_ntt(P);
     constexpr int NQ = fea_nq_native(P), NK = fea_nk(NQ), NQP = 4 * NK;
     constexpr int NA = fea6_na(P), RT = fea6_rt(P), NB = fea6_nb(P);
@@ -77,7 +77,9 @@ __global__ void __launch_bounds__(fea6_threads(P), 1) k_reassemble6(const __grid
     extern __shared__ __align__(128) uint8_t smem[];
     auto sV = [&](int b) { return smem + prm.lay[FEA6_L_V] + b * prm.lay[FEA6_L_VB]; };
     auto sGU = [&](int b) { return reinterpret_cast<double*>(smem + prm.lay[FEA6_L_GU] + b * prm.lay[FEA6_L_GUB]); };
-    auto sGW = [&](int b) { return reinterpret_cast<double*>(smem + prm.lay[FEA6_L_GW] + b * prm.lay[FEA6_L_GWB]); };
+    // gather stage b: (FEA6_PROD_ASYNC) vertex coordinates [3][e_max] double2, then |det B_e| [e_max]
+    auto sGX = [&](int b) { return reinterpret_cast<double*>(smem + prm.lay[FEA6_L_GW] + b * prm.lay[FEA6_L_GWB]); };
+    auto sDet = [&](int b) { return sGX(b) + (FEA6_PROD_ASYNC(P) ? 6 * e_max : 0); };
     auto sLW = [&](int b) { return reinterpret_cast<double*>(smem + prm.lay[FEA6_L_LW] + b * prm.lay[FEA6_L_LWB]); };
     uint64_t* bars = reinterpret_cast<uint64_t*>(smem + prm.lay[FEA6_L_BARS]);
     uint64_t* gat_full = bars;       // [2] producer: 32 cp.async completions + 32 arrivals (geometry)
@@ -125,16 +127,19 @@ __global__ void __launch_bounds__(fea6_threads(P), 1) k_reassemble6(const __grid
         };
         if (lane == 0)
             for (int k = 0; k < 2 && k < nb; ++k) prefetch_blk(k);
-        // software-pipelined across blocks (every global read is an L2 round trip): the DOFs of
-        // block j + 1 load while block j's gathers and geometry run, its descriptor one block
-        // earlier still; element le = 32 h + lane, h < PR rounds
+        // software-pipelined across blocks (every global read is an L2 round trip): the DOFs and
+        // row-tile masks of block j + 1 load while block j's gathers are issued, its descriptor one
+        // block earlier still.  Every gather is asynchronous (cp.async: u(N_e) and the three vertex
+        // coordinates into gather stage j & 1), so the warp never waits on a gathered value; the
+        // element geometry of block j - 1 is computed from its landed coordinates right after block
+        // j's gathers are issued (FEA6_PROD_ASYNC; 0: coordinates in registers, geometry of block j
+        // in iteration j -- one exposed round trip per block).  Element le = 32 h + lane, h < PR.
         constexpr int PR = fea6_prod_rounds(P);
         FEA_CHECK(e_max <= 32 * PR);
         int32_t dn[PR][NP];
+        int32_t msk = 0, msk_n = 0;  // column tile `lane`'s row-tile mask (v6 ghost row skipping)
         int nE_c = 0, nE_n = 0, nEp_n = 0;
         const int32_t* gd_n = nullptr;
-        const int32_t* gmask = nullptr;  // row-tile masks of the block being gathered
-        const int32_t* gmask_n = nullptr;
         auto load_desc = [&](int k) {
             const FeaBlock* B = prm.blocks + b0 + k * G;
             nE_n = ldg_s32(&B->nE);
@@ -142,20 +147,45 @@ __global__ void __launch_bounds__(fea6_threads(P), 1) k_reassemble6(const __grid
         };
         auto load_dofs = [&]() {  // the DOFs of the block whose descriptor load_desc fetched
             nEp_n = fea_pad4(nE_n);
-            gmask_n = gd_n + NP * nEp_n;
 #pragma unroll
             for (int h = 0; h < PR; ++h)
 #pragma unroll
                 for (int i = 0; i < NP; ++i)
                     dn[h][i] = 32 * h + lane < nE_n ? ldg_s32(gd_n + i * nEp_n + 32 * h + lane) : 0;
+            msk_n = lane < ((nE_n + 7) >> 3) ? ldg_s32(gd_n + NP * nEp_n + lane) : 0;
+        };
+        // element geometry: b_e = |det B_e| -> gdet, vec A_e -> W (rows 0..2);
+        // zero W columns of the last tile's padding
+        auto geometry_el = [&](int le, double2 xa, double2 xb, double2 xc, double* gdet, double* W) {
+            const double B00 = xb.x - xa.x, B10 = xb.y - xa.y;
+            const double B01 = xc.x - xa.x, B11 = xc.y - xa.y;
+            const double det = B00 * B11 - B01 * B10;
+            const double inv = 1.0 / (det * det);  // det(B^T B) = det(B)^2
+            gdet[le] = fabs(det);
+            W[le] = (B01 * B01 + B11 * B11) * inv;
+            W[e_max + le] = (B00 * B00 + B10 * B10) * inv;
+            W[2 * e_max + le] = -(B00 * B01 + B10 * B11) * inv;
+        };
+        auto pad_w = [&](int nE, double* W) {  // zero W columns of the last tile's padding
+            for (int le = nE + lane; le < ((nE + 7) & ~7); le += 32) W[le] = W[e_max + le] = W[2 * e_max + le] = 0.0;
+        };
+        auto geometry_blk = [&](int nE, const double2* gx, double* gdet, double* W) {
+#pragma unroll
+            for (int h = 0; h < PR; ++h) {
+                const int le = 32 * h + lane;
+                if (le < nE) geometry_el(le, gx[le], gx[e_max + le], gx[2 * e_max + le], gdet, W);
+            }
+            pad_w(nE, W);
         };
         if (nb > 0) {
             load_desc(0);
             load_dofs();
             nE_c = nE_n;
-            gmask = gmask_n;
+            msk = msk_n;
             if (nb > 1) load_desc(1);
         }
+        int nE_p = 0;        // the previous block's size and masks (its geometry runs one iteration late)
+        int32_t msk_p = 0;
         T6_DECL
         for (int j = 0; j < nb; ++j) {
             const int g = j & 1;
@@ -163,16 +193,16 @@ __global__ void __launch_bounds__(fea6_threads(P), 1) k_reassemble6(const __grid
             T6_TICK(1)
             if (j >= 2) mbar_wait(&gat_free[g], (uint32_t)(((j >> 1) - 1) & 1));
             const int l3 = j % 3;
-            if (j >= 3) mbar_wait(&lam_free[l3], (uint32_t)(((j / 3) - 1) & 1));  // W goes to LW[j % 3]
+            // W of block j goes to LW[j % 3] (the async variant writes it one iteration later and waits there)
+            if (!FEA6_PROD_ASYNC(P) && j >= 3) mbar_wait(&lam_free[l3], (uint32_t)(((j / 3) - 1) & 1));
             T6_TICK(0)
             const int nE = nE_c;
-            const int32_t* gmask_j = gmask;
             FEA_CHECK(nE >= 1 && nE <= e_max);
             double* gu = sGU(g);
-            double* gw = sGW(g);
             double* W = sLW(l3) + NQP * ls;
             const int nEr = DBGM && (prm.dbg_mode & 8) ? 0 : nE;  // (diagnostics: no gathers)
-            double2 xa[PR], xb[PR], xc[PR];
+            if constexpr (FEA6_PROD_ASYNC(P)) {
+            double2* gx = reinterpret_cast<double2*>(sGX(g));
 #pragma unroll
             for (int h = 0; h < PR; ++h) {  // u gathers and vertex coordinates of every round
                 const int le = 32 * h + lane;
@@ -181,38 +211,72 @@ __global__ void __launch_bounds__(fea6_threads(P), 1) k_reassemble6(const __grid
                     for (int i = 0; i < NP; ++i) FEA_CHECK(dn[h][i] >= 0 && dn[h][i] < prm.n_dof);
 #pragma unroll
                     for (int i = 0; i < NP; ++i) cp_async8(gu + i * ls + le, prm.u + dn[h][i]);
+#pragma unroll
+                    for (int v = 0; v < 3; ++v) cp_async16(gx + v * e_max + le, prm.xy + dn[h][v]);
+                }
+            }
+            cp_async_mbar_arrive(&gat_full[g]);  // (noinc) counts when this lane's gathers land
+            asm volatile("cp.async.commit_group;" ::: "memory");
+            const int32_t msk_j = msk;
+            if (j + 1 < nb) {  // the next block's DOFs (registers dn are free again), its successor's descriptor
+                load_dofs();
+                nE_c = nE_n;
+                msk = msk_n;
+                if (j + 2 < nb) load_desc(j + 2);
+            }
+            if (j >= 1) {  // block j - 1: geometry (its coordinates landed: all but the newest group) and
+                           // row-tile masks into its W buffer, once A2(j - 4) released that buffer
+                const int l3p = (j - 1) % 3;
+                if (j - 1 >= 3) mbar_wait(&lam_free[l3p], (uint32_t)((((j - 1) / 3) - 1) & 1));
+                asm volatile("cp.async.wait_group 1;" ::: "memory");
+                const int gp = (j - 1) & 1;
+                double* Wp = sLW(l3p) + NQP * ls;
+                if (!(DBGM && (prm.dbg_mode & 8))) geometry_blk(nE_p, reinterpret_cast<const double2*>(sGX(gp)), sDet(gp), Wp);
+                if (lane < ((nE_p + 7) >> 3)) reinterpret_cast<int32_t*>(Wp + 3 * e_max)[lane] = msk_p;
+                warp_arrive(&gat_full[gp], lane);
+            }
+            nE_p = nE;
+            msk_p = msk_j;
+            } else {
+            double2 xa[PR], xb[PR], xc[PR];
+#pragma unroll
+            for (int h = 0; h < PR; ++h) {
+                const int le = 32 * h + lane;
+                if (le < nEr) {
+#pragma unroll
+                    for (int i = 0; i < NP; ++i) cp_async8(gu + i * ls + le, prm.u + dn[h][i]);
                     xa[h] = ldg_f64x2(prm.xy + dn[h][0]);
                     xb[h] = ldg_f64x2(prm.xy + dn[h][1]);
                     xc[h] = ldg_f64x2(prm.xy + dn[h][2]);
                 }
             }
-            cp_async_mbar_arrive(&gat_full[g]);  // (noinc) counts when this lane's gathers land
-            if (j + 1 < nb) {  // the next block's DOFs (registers dn are free again), its successor's descriptor
+            cp_async_mbar_arrive(&gat_full[g]);
+            if (lane < ((nE + 7) >> 3)) reinterpret_cast<int32_t*>(W + 3 * e_max)[lane] = msk;
+            if (j + 1 < nb) {
                 load_dofs();
                 nE_c = nE_n;
-                gmask = gmask_n;
+                msk = msk_n;
                 if (j + 2 < nb) load_desc(j + 2);
             }
 #pragma unroll
             for (int h = 0; h < PR; ++h) {
                 const int le = 32 * h + lane;
-                if (le < nEr) {  // element geometry once per element: b_e = |det B_e|, vec A_e
-                    const double B00 = xb[h].x - xa[h].x, B10 = xb[h].y - xa[h].y;
-                    const double B01 = xc[h].x - xa[h].x, B11 = xc[h].y - xa[h].y;
-                    const double det = B00 * B11 - B01 * B10;
-                    const double inv = 1.0 / (det * det);  // det(B^T B) = det(B)^2
-                    gw[le] = fabs(det);
-                    W[le] = (B01 * B01 + B11 * B11) * inv;
-                    W[e_max + le] = (B00 * B00 + B10 * B10) * inv;
-                    W[2 * e_max + le] = -(B00 * B01 + B10 * B11) * inv;
-                }
+                if (le < nEr) geometry_el(le, xa[h], xb[h], xc[h], sDet(g), W);
             }
-            for (int le = nE + lane; le < ((nE + 7) & ~7); le += 32)  // padding columns of the last tile
-                W[le] = W[e_max + le] = W[2 * e_max + le] = 0.0;
-            if (lane < ((nE + 7) >> 3))  // the column tiles' row-tile masks (ghost row skipping)
-                reinterpret_cast<int32_t*>(W + 3 * e_max)[lane] = ldg_s32(gmask_j + lane);
-            warp_arrive(&gat_full[g], lane);     // the geometry stores
+            pad_w(nE, W);
+            warp_arrive(&gat_full[g], lane);
+            }
             T6_TICK(1)
+        }
+        if (FEA6_PROD_ASYNC(P) && nb > 0) {  // geometry and masks of the last block
+            const int l3p = (nb - 1) % 3;
+            if (nb - 1 >= 3) mbar_wait(&lam_free[l3p], (uint32_t)((((nb - 1) / 3) - 1) & 1));
+            asm volatile("cp.async.wait_group 0;" ::: "memory");
+            const int gp = (nb - 1) & 1;
+            double* Wp = sLW(l3p) + NQP * ls;
+            if (!(DBGM && (prm.dbg_mode & 8))) geometry_blk(nE_p, reinterpret_cast<const double2*>(sGX(gp)), sDet(gp), Wp);
+            if (lane < ((nE_p + 7) >> 3)) reinterpret_cast<int32_t*>(Wp + 3 * e_max)[lane] = msk_p;
+            warp_arrive(&gat_full[gp], lane);
         }
         asm volatile("cp.async.wait_all;" ::: "memory");
         T6_FLUSH(16)
@@ -236,7 +300,7 @@ __global__ void __launch_bounds__(fea6_threads(P), 1) k_reassemble6(const __grid
         if (j >= 3) mbar_wait(&lam_free[l3], (uint32_t)(((j / 3) - 1) & 1));
         if (aw < net) mbar_wait(&gat_full[g], (uint32_t)((j >> 1) & 1));
         const double* gU = sGU(g);
-        const double* gw = sGW(g);
+        const double* gw = sDet(g);
         const int net_run = DBGM && (prm.dbg_mode & 2) ? 0 : net;  // diagnostics: A1 skipped
         for (int et = aw; et < net_run; et += naw) {  // one element tile, all m-tiles (independent chains)
             const double* spf = reinterpret_cast<const double*>(smem + prm.lay[FEA6_L_PF]);
