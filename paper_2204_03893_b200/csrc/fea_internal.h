@@ -310,9 +310,16 @@ int fea_kernel_occupancy5(int order, int do_m, int do_c, int smem_bytes, int* ct
 // stages would cost e_max 96 -> 88 of shared memory)
 #define FEA6_PROD_ASYNC(p) ((p) == 4)
 #endif
+#ifndef FEA6_A2PF
+#define FEA6_A2PF 0  // A2: bit 0 next column tile's B fragments prefetched, bit 1 W once per column tile
+                     // (measured C5: 0 11.65 ms, 1 14.15, 2 12.12, 3 14.57 -- register pressure)
+#endif
 #ifndef FEA6_A1POS
 #define FEA6_A1POS 0  // A1MODE 2: a warp's A1 unit at column tile (net * A1POS) / 4 of A2
                       // (C5: 0 11.76 ms, 1 12.00, 2 12.20, 3 12.32; A1 on the B warps 13.21)
+#endif
+#if defined(FEA6_A1MODE_P4)  // (experiments: the P4 mode alone)
+#define FEA6_A1MODE(p) ((p) == 4 ? FEA6_A1MODE_P4 : 0)
 #endif
 #ifndef FEA6_A1MODE
 #define FEA6_A1MODE(p) ((p) == 4 ? 2 : 0)
@@ -333,7 +340,10 @@ __host__ __device__ constexpr bool fea6_supported(int p, int nq) { return p >= 3
 #ifndef FEA6_P4_NA15
 #define FEA6_P4_NA15 0
 #endif
-__host__ __device__ constexpr int fea6_na(int p) { return p == 4 ? (FEA6_P4_MERGED || FEA6_P4_NA15 ? 15 : 8) : 7; }
+#ifndef FEA6_P4_NA
+#define FEA6_P4_NA 8  // P4 A warps with two row tiles (9 / 10 with FEA6_NB 6 / 5: experiments)
+#endif
+__host__ __device__ constexpr int fea6_na(int p) { return p == 4 ? (FEA6_P4_MERGED || FEA6_P4_NA15 ? 15 : FEA6_P4_NA) : 7; }
 __host__ __device__ constexpr int fea6_rt(int p) { return p == 4 && !FEA6_P4_MERGED && !FEA6_P4_NA15 ? 2 : 1; }
 __host__ __device__ constexpr int fea6_threads(int p) { return (fea6_na(p) + fea6_nb(p) + 1) * 32; }
 // registers per thread: each SM sub-partition holds 16384 registers for its ceil(warps / 4) warps
@@ -359,15 +369,24 @@ __host__ __device__ constexpr int fea6_maxnreg(int p) {
 #endif
 __host__ __device__ constexpr int fea6_tile(int p, int w, int r) {
     if (!FEA6_TILEMAP || (p == 4 && FEA6_P4_MERGED)) {
-        const int na = p == 4 ? (FEA6_P4_MERGED ? 15 : 8) : 7, ntt = p == 4 ? 15 : 7;
+        const int na = p == 4 ? (FEA6_P4_MERGED ? 15 : FEA6_P4_NA) : 7, ntt = p == 4 ? 15 : 7;
         return w + r * na < ntt ? w + r * na : -1;
     }
     // one nibble per (w, r), 15 = none (ALU only: w is a run-time value)
     // P4: w0 {6, 7} w1 {0, 11} w2 {8, 14} w3 {3, 10} w4 {2, 12} w5 {4, 9} w6 {5, 13} w7 {1}
     // P3: w0..w6 = 0, 1, 3, 2, 5, 6, 4
     // P4 with 15 A warps (per SMSP, A1 on warps 9-14): w0..w14 = 9 12 5 0 2 6 11 3 10 8 13 1 4 14 7
-    const unsigned long long M4 = 0xF1D594C2A3E8B076ull, M3 = 0x4652310ull, M15 = 0x7E41D8A3B6205C9ull;
-    const int x = p == 4 ? (FEA6_P4_NA15 ? (r == 0 ? (int)((M15 >> (4 * w)) & 15) : 15) : (int)((M4 >> (4 * (2 * w + r))) & 15))
+    // P4 with A1 on the producer (A1MODE 3; its DMMAs on SMSP 3): w0 {1, 14} w1 {6, 9} w2 {4, 7}
+    // w3 {2, 12} w4 {5, 11} w5 {8, 10} w6 {3, 13} w7 {0}
+    const unsigned long long M4 = FEA6_A1MODE(4) == 3 ? 0xF0D3A8B5C27496E1ull : 0xF1D594C2A3E8B076ull;
+    const unsigned long long M3 = 0x4652310ull, M15 = 0x7E41D8A3B6205C9ull;
+    // P4 with 9 / 10 A warps (experiments; nibbles 16.. in the high word)
+    const unsigned long long M9[2] = {0xE2A84BF17D69C0F3ull, 0xF5ull}, M10[2] = {0xB3C24DF897A6F5F1ull, 0xFEF0ull};
+    const int n = 2 * w + r;
+    const unsigned long long* Mx = FEA6_P4_NA == 9 ? M9 : M10;
+    const int x = p == 4 ? (FEA6_P4_NA15 ? (r == 0 ? (int)((M15 >> (4 * w)) & 15) : 15)
+                            : FEA6_P4_NA >= 9 ? (int)((Mx[n >> 4] >> (4 * (n & 15))) & 15)
+                                              : (int)((M4 >> (4 * n)) & 15))
                          : (r == 0 ? (int)((M3 >> (4 * w)) & 15) : 15);
     return x == 15 ? -1 : x;
 }

@@ -69,6 +69,7 @@ __global__ void __maxnreg__(fea6_maxnreg(P)) k_reassemble6(const __grid_constant
     constexpr int oW = (NP * NQ + 1) & ~1;
     static_assert(NA * RT >= NTT, "row tiles");
     static_assert(fea6_tile(P, 0, 0) >= 0, "tile map");
+    static_assert(FEA6_A1MODE(P) != 3 || FEA6_PROD_ASYNC(P), "A1 on the producer needs the async producer");
     const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
     const int e_max = prm.e_max, ls = fea6_lstride(e_max), vs = fea6_vstride(e_max);
     const int G = gridDim.x, b0 = blockIdx.x;
@@ -92,12 +93,12 @@ __global__ void __maxnreg__(fea6_maxnreg(P)) k_reassemble6(const __grid_constant
     if (tid == 0) {
         for (int b = 0; b < 2; ++b) {
             mbar_init(&gat_full[b], 33);  // 32 lanes' cp.async completions + the geometry stores
-            mbar_init(&gat_free[b], FEA6_A1MODE(P) == 2 ? NA : NB);
+            mbar_init(&gat_free[b], FEA6_A1MODE(P) == 2 ? NA : FEA6_A1MODE(P) == 3 ? 1 : NB);
             mbar_init(&v_full[b], NA);
             mbar_init(&v_free[b], NB > 0 ? NB : NA);
         }
         for (int b = 0; b < 3; ++b) {
-            mbar_init(&lam_full[b], FEA6_A1MODE(P) == 2 ? NA : NB);
+            mbar_init(&lam_full[b], FEA6_A1MODE(P) == 2 ? NA : FEA6_A1MODE(P) == 3 ? 1 : NB);
             mbar_init(&lam_free[b], NA);
         }
         fence_mbar_init();
@@ -112,6 +113,65 @@ __global__ void __maxnreg__(fea6_maxnreg(P)) k_reassemble6(const __grid_constant
         reinterpret_cast<double*>(sV(tid / 3))[k == 0 ? e_max : 2 * e_max + k - 1] = 0.0;
     }
     __syncthreads();
+    // ------------------------------------------------------------------ A1 (warp aw of naw)
+    // A1(j): U = Phi^T U_e on DMMA, epilogue Lambda_qe = w_q b_e k(u_qe) (PAPER.md:200), into the
+    // Lambda buffer j % 3 (W_e came from the producer).  FEA6_A1MODE 3: the producer warp runs A1(j)
+    // right after the geometry of block j (P4 with the async producer); 2: the A warps run A1(j + 1)
+    // in the middle of A2(j) (its latency hides behind the other warps' DMMA work); 0: the B warps
+    // run A1(j) two blocks ahead of their phase B.
+    constexpr int A1MODE = FEA6_A1MODE(P);
+    const double* cW = prm.ctab + oW;
+    const FeaCoef& cf = DO_M ? prm.coef_m : prm.coef_c;  // one coefficient (distinct ones: two passes)
+    auto do_a1 = [&](int j, int aw, int naw, int nE) {
+        const int g8 = lane >> 2, cq = lane & 3;
+        const int g = j & 1;
+        const int net = (nE + 7) >> 3;
+        const int l3 = j % 3;
+        double* Lam = sLW(l3);
+        if (j >= 3) mbar_wait(&lam_free[l3], (uint32_t)(((j / 3) - 1) & 1));
+        if (aw < net) mbar_wait(&gat_full[g], (uint32_t)((j >> 1) & 1));
+        const double* gU = sGU(g);
+        const double* gw = sDet(g);
+        const int net_run = DBGM && (prm.dbg_mode & 2) ? 0 : net;  // diagnostics: A1 skipped
+        for (int et = aw; et < net_run; et += naw) {  // one element tile, all m-tiles (independent chains)
+            const double* spf = reinterpret_cast<const double*>(smem + prm.lay[FEA6_L_PF]);
+            double pf[MT][KT];  // Phi^T A-fragments (shared memory)
+#pragma unroll
+            for (int mt = 0; mt < MT; ++mt)
+#pragma unroll
+                for (int kt = 0; kt < KT; ++kt) pf[mt][kt] = spf[(mt * KT + kt) * 32 + lane];
+            double uq[MT][2];
+#pragma unroll
+            for (int mt = 0; mt < MT; ++mt) uq[mt][0] = uq[mt][1] = 0.0;
+#pragma unroll
+            for (int kt = 0; kt < KT; ++kt) {
+                const int i = kt * 4 + cq;
+                const double b = i < NP ? gU[i * ls + et * 8 + g8] : 0.0;
+#pragma unroll
+                for (int mt = 0; mt < MT; ++mt) dmma(uq[mt][0], uq[mt][1], pf[mt][kt], b);
+            }
+            const int le0 = et * 8 + 2 * cq;
+            const bool v0 = le0 < nE, v1 = le0 + 1 < nE;
+            const double d0 = v0 ? gw[le0] : 0.0, d1 = v1 ? gw[le0 + 1] : 0.0;
+#pragma unroll
+            for (int mt = 0; mt < MT; ++mt) {
+                const int q = mt * 8 + g8;
+                double l0 = 0.0, l1 = 0.0;
+                if (q < NQ) {
+                    const double w = cW[q];
+                    l0 = w * d0 * keval(cf, uq[mt][0]);
+                    l1 = w * d1 * keval(cf, uq[mt][1]);
+                }
+                if (q < NQP) *reinterpret_cast<double2*>(Lam + q * ls + le0) = make_double2(l0, l1);
+            }
+        }
+        __syncwarp();
+        if (lane == 0) {
+            mbar_arrive(&gat_free[g]);
+            mbar_arrive(&lam_full[l3]);
+        }
+    };
+
     if (warp == NA + NB) {
         // ------------------------------------------------------------------ producer
         auto prefetch_range = [&](const void* p, size_t bytes) {
@@ -234,6 +294,7 @@ __global__ void __maxnreg__(fea6_maxnreg(P)) k_reassemble6(const __grid_constant
                 if (!(DBGM && (prm.dbg_mode & 8))) geometry_blk(nE_p, reinterpret_cast<const double2*>(sGX(gp)), sDet(gp), Wp);
                 if (lane < ((nE_p + 7) >> 3)) reinterpret_cast<int32_t*>(Wp + 3 * e_max)[lane] = msk_p;
                 warp_arrive(&gat_full[gp], lane);
+                if (A1MODE == 3) do_a1(j - 1, 0, 1, nE_p);  // A1 of block j - 1 on this warp
             }
             nE_p = nE;
             msk_p = msk_j;
@@ -277,69 +338,12 @@ __global__ void __maxnreg__(fea6_maxnreg(P)) k_reassemble6(const __grid_constant
             if (!(DBGM && (prm.dbg_mode & 8))) geometry_blk(nE_p, reinterpret_cast<const double2*>(sGX(gp)), sDet(gp), Wp);
             if (lane < ((nE_p + 7) >> 3)) reinterpret_cast<int32_t*>(Wp + 3 * e_max)[lane] = msk_p;
             warp_arrive(&gat_full[gp], lane);
+            if (A1MODE == 3) do_a1(nb - 1, 0, 1, nE_p);
         }
         asm volatile("cp.async.wait_all;" ::: "memory");
         T6_FLUSH(16)
         return;
     }
-
-    // ------------------------------------------------------------------ A1 (warp aw of naw)
-    // A1(j): U = Phi^T U_e on DMMA, epilogue Lambda_qe = w_q b_e k(u_qe) (PAPER.md:200), into the
-    // Lambda buffer j % 3 (W_e came from the producer).  FEA6_A1MODE 2: the A warps run A1(j + 1)
-    // in the middle of A2(j) (its latency hides behind the other warps' DMMA work); 0: the B warps
-    // run A1(j) two blocks ahead of their phase B.
-    constexpr int A1MODE = FEA6_A1MODE(P);
-    const double* cW = prm.ctab + oW;
-    const FeaCoef& cf = DO_M ? prm.coef_m : prm.coef_c;  // one coefficient (distinct ones: two passes)
-    auto do_a1 = [&](int j, int aw, int naw, int nE) {
-        const int g8 = lane >> 2, cq = lane & 3;
-        const int g = j & 1;
-        const int net = (nE + 7) >> 3;
-        const int l3 = j % 3;
-        double* Lam = sLW(l3);
-        if (j >= 3) mbar_wait(&lam_free[l3], (uint32_t)(((j / 3) - 1) & 1));
-        if (aw < net) mbar_wait(&gat_full[g], (uint32_t)((j >> 1) & 1));
-        const double* gU = sGU(g);
-        const double* gw = sDet(g);
-        const int net_run = DBGM && (prm.dbg_mode & 2) ? 0 : net;  // diagnostics: A1 skipped
-        for (int et = aw; et < net_run; et += naw) {  // one element tile, all m-tiles (independent chains)
-            const double* spf = reinterpret_cast<const double*>(smem + prm.lay[FEA6_L_PF]);
-            double pf[MT][KT];  // Phi^T A-fragments (shared memory)
-#pragma unroll
-            for (int mt = 0; mt < MT; ++mt)
-#pragma unroll
-                for (int kt = 0; kt < KT; ++kt) pf[mt][kt] = spf[(mt * KT + kt) * 32 + lane];
-            double uq[MT][2];
-#pragma unroll
-            for (int mt = 0; mt < MT; ++mt) uq[mt][0] = uq[mt][1] = 0.0;
-#pragma unroll
-            for (int kt = 0; kt < KT; ++kt) {
-                const int i = kt * 4 + cq;
-                const double b = i < NP ? gU[i * ls + et * 8 + g8] : 0.0;
-#pragma unroll
-                for (int mt = 0; mt < MT; ++mt) dmma(uq[mt][0], uq[mt][1], pf[mt][kt], b);
-            }
-            const int le0 = et * 8 + 2 * cq;
-            const bool v0 = le0 < nE, v1 = le0 + 1 < nE;
-            const double d0 = v0 ? gw[le0] : 0.0, d1 = v1 ? gw[le0 + 1] : 0.0;
-#pragma unroll
-            for (int mt = 0; mt < MT; ++mt) {
-                const int q = mt * 8 + g8;
-                double l0 = 0.0, l1 = 0.0;
-                if (q < NQ) {
-                    const double w = cW[q];
-                    l0 = w * d0 * keval(cf, uq[mt][0]);
-                    l1 = w * d1 * keval(cf, uq[mt][1]);
-                }
-                if (q < NQP) *reinterpret_cast<double2*>(Lam + q * ls + le0) = make_double2(l0, l1);
-            }
-        }
-        __syncwarp();
-        if (lane == 0) {
-            mbar_arrive(&gat_free[g]);
-            mbar_arrive(&lam_full[l3]);
-        }
-    };
 
     // ------------------------------------------------------------------ phase B helpers
     // B(jb): every CSR slot of the block = sum of its contributors, in ascending
@@ -510,6 +514,15 @@ __global__ void __maxnreg__(fea6_maxnreg(P)) k_reassemble6(const __grid_constant
             // A1(j + 1) inside A2(j): a warp with an A1 unit runs it at column tile a1_at (FEA6_A1POS
             // quarters of the block), a warp without one only arrives, at the start
             const int a1_at = NA - 1 - warp < ((nE_n + 7) >> 3) ? (net * FEA6_A1POS) >> 2 : 0;
+            // FEA6_A2PF: the next column tile's B fragments and row-tile mask load while this tile's
+            // DMMAs run; the W factors once per column tile, before its DMMAs
+            uint32_t tm_n = 0;
+            double bl_n[NK];
+            auto load_tile = [&](int et2, uint32_t& tm, double (&b)[NK]) {
+                tm = reinterpret_cast<const uint32_t*>(W + 3 * e_max)[et2];  // row tiles needed
+#pragma unroll
+                for (int kk = 0; kk < NK; ++kk) b[kk] = Lam[(kk * 4 + cq) * ls + et2 * 8 + g8];
+            };
             for (int et = 0; et < net_a2; ++et) {
                 // (units to the last warps first: warp NA - 1 holds one row tile less)
                 if (A1MODE == 2 && et == a1_at && j + 1 < nb) {
@@ -517,11 +530,22 @@ __global__ void __maxnreg__(fea6_maxnreg(P)) k_reassemble6(const __grid_constant
                     do_a1(j + 1, NA - 1 - warp, NA, nE_n);
                     T6_TICK(1)
                 }
-                const uint32_t tmask = reinterpret_cast<const uint32_t*>(W + 3 * e_max)[et];  // row tiles needed
-                const int col = et * 8 + g8, le0 = et * 8 + 2 * cq;
+                const int le0 = et * 8 + 2 * cq;
+                uint32_t tmask;
                 double bl[NK];
+                if (!(FEA6_A2PF & 1) || et == 0) load_tile(et, tmask, bl);
+                else {
+                    tmask = tm_n;
 #pragma unroll
-                for (int kk = 0; kk < NK; ++kk) bl[kk] = Lam[(kk * 4 + cq) * ls + col];
+                    for (int kk = 0; kk < NK; ++kk) bl[kk] = bl_n[kk];
+                }
+                if ((FEA6_A2PF & 1) && et + 1 < net_a2) load_tile(et + 1, tm_n, bl_n);
+                double2 w0 = make_double2(0.0, 0.0), w1 = w0, w2 = w0;
+                if ((FEA6_A2PF & 2) && DO_C) {
+                    w0 = *reinterpret_cast<const double2*>(W + le0);
+                    w1 = *reinterpret_cast<const double2*>(W + e_max + le0);
+                    w2 = *reinterpret_cast<const double2*>(W + 2 * e_max + le0);
+                }
 #pragma unroll
                 for (int r = 0; r < RT; ++r) {  // row tiles one after the other (fused: measured slower)
                     const int tt = tts[r];
@@ -541,9 +565,11 @@ __global__ void __maxnreg__(fea6_maxnreg(P)) k_reassemble6(const __grid_constant
                         FEA_CHECK(le0 + 1 < e_max + 1 && (t * vs + le0 + 1) * (IL ? 16 : 8) < prm.lay[FEA6_L_VB]);
                         double k0 = 0.0, k1 = 0.0;
                         if (DO_C) {
-                            const double2 w0 = *reinterpret_cast<const double2*>(W + le0);
-                            const double2 w1 = *reinterpret_cast<const double2*>(W + e_max + le0);
-                            const double2 w2 = *reinterpret_cast<const double2*>(W + 2 * e_max + le0);
+                            if (!(FEA6_A2PF & 2)) {
+                                w0 = *reinterpret_cast<const double2*>(W + le0);
+                                w1 = *reinterpret_cast<const double2*>(W + e_max + le0);
+                                w2 = *reinterpret_cast<const double2*>(W + 2 * e_max + le0);
+                            }
                             k0 = fma(w0.x, a0, fma(w1.x, p0, w2.x * c0));
                             k1 = fma(w0.y, a1, fma(w1.y, p1, w2.y * c1));
                         }
@@ -580,7 +606,7 @@ __global__ void __maxnreg__(fea6_maxnreg(P)) k_reassemble6(const __grid_constant
     // (A1 runs two blocks ahead of phase B and one to two ahead of A2: three Lambda buffers).
     if (NB > 0) {
         const int bt = tid - NA * 32, bw = bt >> 5;
-        constexpr int LAG = A1MODE == 2 ? 0 : 2;  // phase B of block j - LAG after A1(j) (B warps running A1)
+        constexpr int LAG = A1MODE == 0 ? 2 : 0;  // phase B of block j - LAG after A1(j) (B warps running A1)
         int nE_a = nb > 0 ? ldg_s32(&prm.blocks[b0].nE) : 0;  // A1's block size, one block ahead
         BState st;
         BDesc bd;
