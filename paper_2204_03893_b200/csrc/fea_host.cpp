@@ -876,7 +876,7 @@ struct PlanData {
 // v6: kernel v6 record (fea_internal.h): class-A u32 items in slot order + class-B items; the
 // DOFs travel separately as for v5 (pass v5 = true); records stay in global memory.
 static fea_status build_blocks(fea_ctx c, bool v5, bool orient, int64_t e_max, int64_t rec_budget, int64_t EM,
-                               PlanData& P, bool il = false, bool v6 = false) {
+                               PlanData& P, bool il = false, bool v6 = false, int64_t vcap = 0) {
     const int np = c->np, T = c->T;
     const int64_t n_e = c->n_e;
     const int64_t R0 = c->row_begin, nr = c->n_rows;
@@ -933,7 +933,6 @@ static fea_status build_blocks(fea_ctx c, bool v5, bool orient, int64_t e_max, i
             ent += rent;
         }
     }
-    const int64_t nb = (int64_t)brow.size();
     brow.push_back(nr);
 
     ptime("plan: row blocks");
@@ -964,41 +963,19 @@ static fea_status build_blocks(fea_ctx c, bool v5, bool orient, int64_t e_max, i
         }
     }
     const int NTT6 = (T + 7) / 8;
-    std::atomic<int64_t> skip_work(0), skip_full(0), skip_crit(0);
-    std::atomic<int64_t> tile_use[32];
-    for (auto& x : tile_use) x = 0;
-    // ---- per block: element set, (row, col) records sorted -> slots, contributors, record
-    struct BOut {
-        std::vector<int32_t> rownnz, cols, dofs;
-        std::vector<uint8_t> rec;
-        FeaBlock fb{};
-        int64_t nghost = 0, nown = 0;
-        std::string err;
-    };
-    std::vector<BOut> bo(nb);
-    parallel_for(nb, [&](int64_t b) {
-        BOut& o = bo[b];
-        const int64_t ra = brow[b], rb = brow[b + 1];
-        const int64_t ga = R0 + ra, gb = R0 + rb;  // global library rows
-        std::vector<int32_t> E;
+    // a block's elements E (ascending library element), their relabelling rot, row-tile masks
+    // emask, column positions newpos (sorted by mask) and the column tiles' masks ctm
+    auto layout_block = [&](int64_t ra, int64_t rb, std::vector<int32_t>& E, std::vector<int8_t>& rot,
+                            std::vector<uint32_t>& emask, std::vector<int32_t>& newpos, std::vector<uint32_t>& ctm) {
+        const int64_t ga = R0 + ra, gb = R0 + rb;
+        E.clear();
         for (int64_t r = ra; r < rb; ++r) E.insert(E.end(), inc.begin() + iptr[r], inc.begin() + iptr[r + 1]);
         std::sort(E.begin(), E.end());
         E.erase(std::unique(E.begin(), E.end()), E.end());
-        for (int32_t e : E) (c->elem_min[e] < ga ? o.nghost : o.nown)++;
-        {  // interior: every DOF of every element of the block is owned by this rank (overlap, NEXT-3)
-            bool inside = true;
-            for (int32_t e : E)
-                for (int i = 0; i < np && inside; ++i) {
-                    const int32_t d = c->ed[(size_t)e * np + i];
-                    inside = d >= R0 && d < R1;
-                }
-            o.fb.spare_[0] = inside ? 1 : 0;
-        }
-        // element relabelling and column order (identity unless v6 skipping)
         const int64_t nE0 = (int64_t)E.size();
-        std::vector<int8_t> rot(nE0, 0);
-        std::vector<uint32_t> emask(nE0, (1u << NTT6) - 1);
-        std::vector<int32_t> newpos(nE0);
+        rot.assign(nE0, 0);
+        emask.assign(nE0, (1u << NTT6) - 1);
+        newpos.resize(nE0);
         std::iota(newpos.begin(), newpos.end(), 0);
         if (skip) {
             for (int64_t le = 0; le < nE0; ++le) {
@@ -1025,6 +1002,86 @@ static fea_status build_blocks(fea_ctx c, bool v5, bool orient, int64_t e_max, i
             });
             for (int64_t q = 0; q < nE0; ++q) newpos[ord[q]] = (int32_t)q;
         }
+        ctm.assign((nE0 + 7) / 8, 0);
+        for (int64_t le0 = 0; le0 < nE0; ++le0) ctm[newpos[le0] / 8] |= emask[le0];
+    };
+    // ---- v6 compact V (FEA6_VCOMPACT): a block's V needs 1 + 64 sum_et popc(m_et) cells; a greedy
+    // block over the capacity is cut at its longest row prefix that fits, the rest starts a block
+    if (v6 && vcap > 0) {
+        const int64_t nb0 = (int64_t)brow.size() - 1;
+        std::vector<std::vector<int64_t>> cuts(nb0);
+        std::atomic<int> bad(0);
+        parallel_for(nb0, [&](int64_t b) {
+            std::vector<int32_t> E, newpos;
+            std::vector<int8_t> rot;
+            std::vector<uint32_t> emask, ctm;
+            auto cells = [&](int64_t ra, int64_t rb) {
+                layout_block(ra, rb, E, rot, emask, newpos, ctm);
+                int64_t t = 0;
+                for (uint32_t m : ctm) t += __builtin_popcount(m);
+                return 1 + 64 * t;
+            };
+            int64_t ra = brow[b];
+            const int64_t rb = brow[b + 1];
+            while (ra < rb) {
+                if (cells(ra, rb) <= vcap) {
+                    cuts[b].push_back(ra);
+                    break;
+                }
+                int64_t lo = ra + 1, hi = rb - 1;  // the longest fitting prefix [ra, lo) (a single row must fit)
+                if (cells(ra, lo) > vcap) {
+                    bad = 1;
+                    return;
+                }
+                while (lo < hi) {
+                    const int64_t mid = (lo + hi + 1) / 2;
+                    if (cells(ra, mid) <= vcap) lo = mid;
+                    else hi = mid - 1;
+                }
+                cuts[b].push_back(ra);
+                ra = lo;
+            }
+        });
+        if (bad) return c->fail(FEA_E_UNSUPPORTED, "compact V: one row's elements exceed %lld cells", (long long)vcap);
+        std::vector<int64_t> brow2;
+        for (int64_t b = 0; b < nb0; ++b) brow2.insert(brow2.end(), cuts[b].begin(), cuts[b].end());
+        brow2.push_back(nr);
+        brow.swap(brow2);
+        ptime("plan: compact-V block cuts");
+    }
+    const int64_t nb = (int64_t)brow.size() - 1;
+    std::atomic<int64_t> skip_work(0), skip_full(0), skip_crit(0);
+    std::atomic<int64_t> tile_use[32];
+    for (auto& x : tile_use) x = 0;
+    // ---- per block: element set, (row, col) records sorted -> slots, contributors, record
+    struct BOut {
+        std::vector<int32_t> rownnz, cols, dofs;
+        std::vector<uint8_t> rec;
+        FeaBlock fb{};
+        int64_t nghost = 0, nown = 0;
+        std::string err;
+    };
+    std::vector<BOut> bo(nb);
+    parallel_for(nb, [&](int64_t b) {
+        BOut& o = bo[b];
+        const int64_t ra = brow[b], rb = brow[b + 1];
+        const int64_t ga = R0 + ra, gb = R0 + rb;  // global library rows
+        std::vector<int32_t> E, newpos;
+        std::vector<int8_t> rot;
+        std::vector<uint32_t> emask, ctm;
+        layout_block(ra, rb, E, rot, emask, newpos, ctm);  // (element relabelling and column order: identity unless v6 skipping)
+        for (int32_t e : E) (c->elem_min[e] < ga ? o.nghost : o.nown)++;
+        {  // interior: every DOF of every element of the block is owned by this rank (overlap, NEXT-3)
+            bool inside = true;
+            for (int32_t e : E)
+                for (int i = 0; i < np && inside; ++i) {
+                    const int32_t d = c->ed[(size_t)e * np + i];
+                    inside = d >= R0 && d < R1;
+                }
+            o.fb.spare_[0] = inside ? 1 : 0;
+        }
+        std::vector<int32_t> cb(ctm.size() + 1, 0);  // compact V: needed row tiles before column tile et
+        for (size_t et = 0; et < ctm.size(); ++et) cb[et + 1] = cb[et] + __builtin_popcount(ctm[et]);
         struct Rec { int32_t row, col, le, t; };  // t: V row (| 0x10000 if orient and i > j: Vdn)
         std::vector<Rec> recs;
         recs.reserve((size_t)(iptr[rb] - iptr[ra]) * np);
@@ -1075,6 +1132,13 @@ static fea_status build_blocks(fea_ctx c, bool v5, bool orient, int64_t e_max, i
             k = k2;
         }
         const int32_t nslot = (int32_t)sstart.size();
+        // V cell of (symmetric row t, column le): dense t EM + le, or the compact layout (fea6_vcell)
+        auto vcell = [&](int32_t t, int32_t le) -> uint32_t {
+            if (vcap <= 0) return (uint32_t)(t * EM + le);
+            const uint32_t mk = ctm[le / 8];
+            if (!((mk >> (t / 8)) & 1u)) o.err = "compact V: a contribution outside its column tile's mask";
+            return (uint32_t)fea6_vcell(cb[le / 8], mk, t / 8, t % 8, le % 8);
+        };
         if (v6 || (v5 && !orient && FEA5_SLOT)) {  // kernel v6 (and v5) record: class A in slot order, class B as flat items
             if (nslot > 65535) {
                 o.err = "more than 65535 slots in one block";
@@ -1086,8 +1150,8 @@ static fea_status build_blocks(fea_ctx c, bool v5, bool orient, int64_t e_max, i
             int32_t cmax = 0;
             for (int32_t sl = 0; sl < nslot; ++sl) {
                 const int32_t C = scount[sl];
-                auto off = [&](int32_t m) { return (uint32_t)((recs[m].t & 0xffff) * EM + recs[m].le); };
-                if (C == 1) ia[sl] = off(sstart[sl]) | (uint32_t)e_max << 16;  // + the zero cell
+                auto off = [&](int32_t m) { return vcell(recs[m].t & 0xffff, recs[m].le); };
+                if (C == 1) ia[sl] = off(sstart[sl]) | (uint32_t)(vcap > 0 ? 0 : e_max) << 16;  // + the zero cell
                 else if (C == 2) ia[sl] = off(sstart[sl]) | off(sstart[sl] + 1) << 16;
                 else {
                     clsB.push_back(sl);
@@ -1115,7 +1179,7 @@ static fea_status build_blocks(fea_ctx c, bool v5, bool orient, int64_t e_max, i
                 w[1] = (uint16_t)scount[sl];
                 for (int q = 0; q < scount[sl]; ++q) {
                     const int32_t m = sstart[sl] + q;
-                    w[2 + q] = (uint16_t)((recs[m].t & 0xffff) * EM + recs[m].le);
+                    w[2 + q] = (uint16_t)vcell(recs[m].t & 0xffff, recs[m].le);
                 }
             }
             const int32_t ncl = (int32_t)clsB.size();
@@ -1348,15 +1412,36 @@ fea_status fea_build_pattern(fea_ctx c, int64_t* row_begin, int64_t* n_rows_loca
     c->kver = v6 ? 6 : v5 ? 5 : 4;
     const int rstages = c->order <= 2 ? 3 : 2;  // fea_rstages (v4)
     int64_t e_max, rec_budget;
+    int64_t vcap = 0, e_target = 0;  // v6 compact V: capacity (cells per buffer) and greedy block target
     if (v6) {
         // two V buffers, two gather / Lambda / W stages (fea6_smem_layout); records stay in global memory
         const int64_t budget = c->tune_smem ? c->tune_smem : 227 * 1024;
         e_max = std::min<int64_t>(32 * fea6_prod_rounds(c->order), 65535 / T - 2) / 8 * 8;
         if (c->tune_emax) e_max = std::min<int64_t>(e_max, c->tune_emax / 8 * 8);
         int32_t L6[FEA_L_N];
-        for (; e_max >= 8; e_max -= 8) {
-            fea6_smem_layout(L6, (int)e_max, c->order, dm, dcm);
-            if (L6[FEA6_L_TOTAL] <= budget) break;
+        if (FEA6_VCOMPACT) {
+            // compact V: the capacity left by the e_max-sized buffers; the greedy blocks target the
+            // elements that capacity holds at an expected post-skip tile fraction (blocks over it
+            // are cut in build_blocks); e_max (buffers) chosen to maximise min(e_max, target)
+            const int cellb = nmat == 2 ? 16 : 8, ntt = (T + 7) / 8;
+            const double frac = c->tune_skip && c->rule_sym ? (c->order == 4 ? FEA6_VFRAC / 100.0 : 0.86) : 1.0;
+            int64_t best_el = -1, best_e = 0, best_cap = 0;
+            for (int64_t em = e_max; em >= 8; em -= 8) {
+                fea6_smem_layout(L6, (int)em, c->order, dm, dcm, 1);
+                const int64_t cap = std::min<int64_t>(65535, (budget - L6[FEA6_L_TOTAL] + L6[FEA6_L_VB] * 2) / 2 / 128 * 128 / cellb);
+                if (cap < 1 + 64 * 2 * ntt) continue;
+                const int64_t tgt = std::min<int64_t>(em, (int64_t)((cap - 1) / 64 / (ntt * frac / 8.0)));
+                if (tgt > best_el) best_el = tgt, best_e = em, best_cap = cap;
+            }
+            if (best_el < 8) return c->fail(FEA_E_UNSUPPORTED, "shared-memory budget too small for kernel v6");
+            e_max = best_e;
+            vcap = best_cap;  // (cells; whole 128-byte lines)
+            e_target = best_el;
+        } else {
+            for (; e_max >= 8; e_max -= 8) {
+                fea6_smem_layout(L6, (int)e_max, c->order, dm, dcm);
+                if (L6[FEA6_L_TOTAL] <= budget) break;
+            }
         }
         rec_budget = INT64_MAX / 4;
     } else if (v5) {
@@ -1399,7 +1484,7 @@ fea_status fea_build_pattern(fea_ctx c, int64_t* row_begin, int64_t* n_rows_loca
     PlanData P;
     {
         // v5 with both matrices: V_m, V_c interleaved, phase B reads 16-byte {m, c} pairs
-        const fea_status st = v6 ? build_blocks(c, true, false, e_max, rec_budget, EM, P, nmat == 2, true)
+        const fea_status st = v6 ? build_blocks(c, true, false, vcap > 0 ? e_target : e_max, rec_budget, EM, P, nmat == 2, true, vcap)
                                  : build_blocks(c, v5, false, e_max, rec_budget, EM, P, v5 && nmat == 2);
         if (st != FEA_OK) return st;
     }
@@ -1417,7 +1502,7 @@ fea_status fea_build_pattern(fea_ctx c, int64_t* row_begin, int64_t* n_rows_loca
     auto& alldofs = P.dofs;
     const int64_t visits = P.visits, owned = P.owned, ncon = P.ncon, rbytes = P.rbytes;
     int32_t L[FEA_L_N];
-    if (v6) fea6_smem_layout(L, (int)e_max, c->order, dm, dcm);
+    if (v6) fea6_smem_layout(L, (int)e_max, c->order, dm, dcm, (int)vcap);
     else if (v5) fea5_smem_layout(L, (int)rec_max, (int)e_max, c->order, dm, dcm);
     else fea_smem_layout(L, rstages, (int)rec_max, (int)e_max, c->order, c->split ? 0 : nq, dm, dcm);
     c->nblocks = (int)nb;

@@ -364,6 +364,9 @@ __host__ __device__ constexpr int fea6_maxnreg(int p) {
 #ifndef FEA6_U
 #define FEA6_U(p) ((p) == 3 ? 12 : 8)
 #endif
+#ifndef FEA6_P4MAP
+#define FEA6_P4MAP 1  // (C5: map 1 11.52 ms, 0 11.64, 2 11.65)
+#endif
 #ifndef FEA6_TILEMAP
 #define FEA6_TILEMAP 1
 #endif
@@ -373,12 +376,18 @@ __host__ __device__ constexpr int fea6_tile(int p, int w, int r) {
         return w + r * na < ntt ? w + r * na : -1;
     }
     // one nibble per (w, r), 15 = none (ALU only: w is a run-time value)
-    // P4: w0 {6, 7} w1 {0, 11} w2 {8, 14} w3 {3, 10} w4 {2, 12} w5 {4, 9} w6 {5, 13} w7 {1}
+    // P4 (FEA6_P4MAP 1, A1 units weighted 1.5 tile units): w0 {0, 10} w1 {3, 8} w2 {7, 13} w3 {4, 9}
+    // w4 {5, 11} w5 {6, 12} w6 {2, 14} w7 {1}; (map 0, weight 0.7): w0 {6, 7} w1 {0, 11} w2 {8, 14}
+    // w3 {3, 10} w4 {2, 12} w5 {4, 9} w6 {5, 13} w7 {1}
     // P3: w0..w6 = 0, 1, 3, 2, 5, 6, 4
     // P4 with 15 A warps (per SMSP, A1 on warps 9-14): w0..w14 = 9 12 5 0 2 6 11 3 10 8 13 1 4 14 7
     // P4 with A1 on the producer (A1MODE 3; its DMMAs on SMSP 3): w0 {1, 14} w1 {6, 9} w2 {4, 7}
     // w3 {2, 12} w4 {5, 11} w5 {8, 10} w6 {3, 13} w7 {0}
-    const unsigned long long M4 = FEA6_A1MODE(4) == 3 ? 0xF0D3A8B5C27496E1ull : 0xF1D594C2A3E8B076ull;
+    // (FEA6_P4MAP 1 / 2: A1 units weighted 1.5 / 2.5 tile units instead of 0.7 -- experiments)
+    const unsigned long long M4 = FEA6_A1MODE(4) == 3 ? 0xF0D3A8B5C27496E1ull
+                                  : FEA6_P4MAP == 1   ? 0xF1E2C6B594D783A0ull
+                                  : FEA6_P4MAP == 2   ? 0xF0E5D4B8A9C76132ull
+                                                      : 0xF1D594C2A3E8B076ull;
     const unsigned long long M3 = 0x4652310ull, M15 = 0x7E41D8A3B6205C9ull;
     // P4 with 9 / 10 A warps (experiments; nibbles 16.. in the high word)
     const unsigned long long M9[2] = {0xE2A84BF17D69C0F3ull, 0xF5ull}, M10[2] = {0xB3C24DF897A6F5F1ull, 0xFEF0ull};
@@ -391,7 +400,10 @@ __host__ __device__ constexpr int fea6_tile(int p, int w, int r) {
     return x == 15 ? -1 : x;
 }
 // producer rounds (elements le = 32 h + lane, h < rounds): caps e_max at 32 * rounds
-__host__ __device__ constexpr int fea6_prod_rounds(int p) { return p == 4 ? 2 : 3; }
+#ifndef FEA6_P3_ROUNDS
+#define FEA6_P3_ROUNDS 3
+#endif
+__host__ __device__ constexpr int fea6_prod_rounds(int p) { return p == 4 ? 2 : FEA6_P3_ROUNDS; }
 // Lambda / gathered-u row stride (doubles): == 4 (mod 16), so the DMMA B-fragment loads
 // [(4 kk + c) ls + 8 et + g] are conflict-free per half-warp
 __host__ __device__ inline int32_t fea6_lstride(int32_t e_max) { return e_max + ((4 - e_max) % 16 + 16) % 16; }
@@ -412,13 +424,42 @@ __host__ __device__ inline int32_t fea6_vstride(int32_t e_max) { return e_max + 
 // Block DOF arrays (v6): [n_p][pad4(nE)] then the row-tile mask of every 8-element column tile.
 enum { FEA6_L_V = 0, FEA6_L_VB = 1, FEA6_L_GU = 2, FEA6_L_GUB = 3, FEA6_L_GW = 4, FEA6_L_GWB = 5, FEA6_L_LW = 6,
        FEA6_L_LWB = 7, FEA6_L_PF = 8, FEA6_L_BARS = 10, FEA6_L_TOTAL = 11 };
-__host__ __device__ inline void fea6_smem_layout(int32_t* L, int e_max, int p, int do_m, int do_c) {
+// V layout (FEA6_VCOMPACT 1, default): per block, only the 8-row tiles each 8-element column
+// tile computes (its row-tile mask m_et) are stored: cell 0 = the zero cell, then the needed
+// row tiles in order, tile k = sum_{et' < et} popc(m_et') + popc(m_et & ((1 << tt) - 1)) at cells
+// 1 + 64 k ...; inside it row r, column c at 8 r + (c ^ ((r ^ 3k) & 7)): the epilogue's 16-byte
+// stores stay conflict-free per quarter warp, and phase B's reads of one element column spread
+// over the banks by row and tile (with c ^ (r & 1) they all hit one bank group: C3 +7 %).  Ghost elements then cost V
+// space only for the rows their block reads, so a block holds more elements (fewer ghosts).
+// 0: dense [T][e_max + 1] cells, the zero cell at column e_max of row 0.
+#ifndef FEA6_VSWZ
+#define FEA6_VSWZ 0  // compact V column swizzle: 0 xor with (r ^ 3k), 1 rotation by (r + 3k)
+#endif
+#ifndef FEA6_VFRAC
+#define FEA6_VFRAC 83  // compact V: expected post-skip tile fraction (percent) for the P4 block target
+#endif
+#ifndef FEA6_VCOMPACT
+#define FEA6_VCOMPACT 0  // measured slower: C5 11.83 ms (frac 0.83: fewer, uneven blocks) vs dense 11.50; C3 1.461 vs 1.437
+#endif
+__host__ __device__ inline int fea6_popc(uint32_t x) {
+#ifdef __CUDA_ARCH__
+    return __popc(x);
+#else
+    return __builtin_popcount(x);
+#endif
+}
+__host__ __device__ inline int32_t fea6_vcell(int32_t cbase, uint32_t m_et, int tt, int r, int col) {
+    const int32_t k = cbase + fea6_popc(m_et & ((1u << tt) - 1u));
+    return 1 + 64 * k + 8 * r + (FEA6_VSWZ ? ((col + r + 3 * k) & 7) : (col ^ ((r ^ (3 * k)) & 7)));
+}
+// vcells: V capacity per buffer in cells (compact layout; 0: dense, from e_max)
+__host__ __device__ inline void fea6_smem_layout(int32_t* L, int e_max, int p, int do_m, int do_c, int vcells = 0) {
     const int T = fea_T(p), np = fea_np(p), nqp = 4 * fea_nk(fea_nq_native(p));
     const int ls = fea6_lstride(e_max), vs = fea6_vstride(e_max);
     const int cell = (do_m && do_c) ? 16 : 8;
     for (int i = 0; i < FEA_L_N; ++i) L[i] = 0;
     int32_t o = 0;
-    L[FEA6_L_VB] = fea_align(T * vs * cell, 128);
+    L[FEA6_L_VB] = fea_align((vcells > 0 ? vcells : T * vs) * cell, 128);
     L[FEA6_L_V] = o; o += 2 * L[FEA6_L_VB];
     L[FEA6_L_GUB] = fea_align(8 * np * ls, 128);
     L[FEA6_L_GU] = o; o += 2 * L[FEA6_L_GUB];

@@ -107,11 +107,13 @@ __global__ void __maxnreg__(fea6_maxnreg(P)) k_reassemble6(const __grid_constant
         double* spf = reinterpret_cast<double*>(smem + prm.lay[FEA6_L_PF]);
         for (int i = tid; i < MT * KT * 32; i += blockDim.x) spf[i] = __ldg(prm.qfrag + 4 * NTT * NK * 32 + i);
     }
-    if (tid < 6) {  // the zero cell (row 0, column e_max) of both V buffers: double e_max (8-byte
-                    // cells) and doubles 2 e_max, 2 e_max + 1 ({m, c} cells); A2 never writes it
+    if (tid < 6) {  // the zero cell of both V buffers (A2 never writes it): compact layout cell 0
+                    // (doubles 0, 1); dense: row 0, column e_max -- double e_max (8-byte cells) and
+                    // doubles 2 e_max, 2 e_max + 1 ({m, c} cells)
         const int k = tid % 3;
-        reinterpret_cast<double*>(sV(tid / 3))[k == 0 ? e_max : 2 * e_max + k - 1] = 0.0;
+        reinterpret_cast<double*>(sV(tid / 3))[FEA6_VCOMPACT ? (k & 1) : k == 0 ? e_max : 2 * e_max + k - 1] = 0.0;
     }
+    const int vcells = prm.lay[FEA6_L_VB] / (IL ? 16 : 8);  // V capacity per buffer (cells)
     __syncthreads();
     // ------------------------------------------------------------------ A1 (warp aw of naw)
     // A1(j): U = Phi^T U_e on DMMA, epilogue Lambda_qe = w_q b_e k(u_qe), into the
@@ -417,7 +419,7 @@ __global__ void __maxnreg__(fea6_maxnreg(P)) k_reassemble6(const __grid_constant
                 const int o0 = it & 0xffff, o1 = it >> 16;
                 if (o0 != 0xffff) {
                     const int p = (c0 + u * nbw) * 32 + lane;
-                    FEA_CHECK(p < nslots && o0 < T * vs && o1 < T * vs);
+                    FEA_CHECK(p < nslots && o0 < vcells && o1 < vcells);
                     if (IL) {
                         const double2 x0 = reinterpret_cast<const double2*>(Vb)[o0];
                         const double2 x1 = reinterpret_cast<const double2*>(Vb)[o1];
@@ -448,7 +450,7 @@ __global__ void __maxnreg__(fea6_maxnreg(P)) k_reassemble6(const __grid_constant
             for (int q = 0; q < C; ++q) {
                 const uint32_t hw = q < 2 ? h.y : q < 4 ? h.z : h.w;  // no local-memory indexing
                 const int o = q < 6 ? (int)((hw >> (16 * (q & 1))) & 0xffff) : (int)__ldg(wrd + 2 + q);
-                FEA_CHECK(o < T * vs);
+                FEA_CHECK(o < vcells);
                 if (IL) {
                     const double2 x = reinterpret_cast<const double2*>(Vb)[o];
                     am += x.x;
@@ -523,6 +525,7 @@ __global__ void __maxnreg__(fea6_maxnreg(P)) k_reassemble6(const __grid_constant
 #pragma unroll
                 for (int kk = 0; kk < NK; ++kk) b[kk] = Lam[(kk * 4 + cq) * ls + et2 * 8 + g8];
             };
+            int32_t cbase = 0;  // compact V: needed row tiles of the column tiles before et
             for (int et = 0; et < net_a2; ++et) {
                 // (units to the last warps first: warp NA - 1 holds one row tile less)
                 if (A1MODE == 2 && et == a1_at && j + 1 < nb) {
@@ -562,7 +565,6 @@ __global__ void __maxnreg__(fea6_maxnreg(P)) k_reassemble6(const __grid_constant
                     }
                     const int t = tt * 8 + g8;
                     if (t < T) {
-                        FEA_CHECK(le0 + 1 < e_max + 1 && (t * vs + le0 + 1) * (IL ? 16 : 8) < prm.lay[FEA6_L_VB]);
                         double k0 = 0.0, k1 = 0.0;
                         if (DO_C) {
                             if (!(FEA6_A2PF & 2)) {
@@ -573,17 +575,24 @@ __global__ void __maxnreg__(fea6_maxnreg(P)) k_reassemble6(const __grid_constant
                             k0 = fma(w0.x, a0, fma(w1.x, p0, w2.x * c0));
                             k1 = fma(w0.y, a1, fma(w1.y, p1, w2.y * c1));
                         }
+                        int c0 = t * vs + le0, c1 = c0 + 1;
+                        if (FEA6_VCOMPACT) {
+                            c0 = fea6_vcell(cbase, tmask, tt, g8, 2 * cq);
+                            c1 = fea6_vcell(cbase, tmask, tt, g8, 2 * cq + 1);
+                        }
+                        FEA_CHECK(c0 > 0 && c0 < vcells && c1 > 0 && c1 < vcells);
                         if (IL) {
-                            double2* V2 = reinterpret_cast<double2*>(Vb) + t * vs + le0;
-                            V2[0] = make_double2(m0, k0);
-                            V2[1] = make_double2(m1, k1);
+                            double2* V2 = reinterpret_cast<double2*>(Vb);
+                            V2[c0] = make_double2(m0, k0);
+                            V2[c1] = make_double2(m1, k1);
                         } else {
-                            double* V1 = reinterpret_cast<double*>(Vb) + t * vs + le0;
-                            V1[0] = DO_M ? m0 : k0;
-                            V1[1] = DO_M ? m1 : k1;
+                            double* V1 = reinterpret_cast<double*>(Vb);
+                            V1[c0] = DO_M ? m0 : k0;
+                            V1[c1] = DO_M ? m1 : k1;
                         }
                     }
                 }
+                cbase += fea6_popc(tmask);
             }
             T6_TICK(4)
             __syncwarp();
