@@ -102,7 +102,10 @@ __host__ __device__ constexpr int fea5_item_bytes(int C) {
 
 // ---- kernel v5 (p <= 2 with the configs' native rules): lane-per-element, constant-bank tables.
 // NW warps per CTA (no producer warp), one CTA per SM, and the units per 32-element tile.
-__host__ __device__ constexpr int fea5_nw(int p) { return p == 1 ? 16 : 16; }
+#ifndef FEA5_NW1
+#define FEA5_NW1 16  // warps per CTA for P1 (P2: 16)
+#endif
+__host__ __device__ constexpr int fea5_nw(int p) { return p == 1 ? FEA5_NW1 : 16; }
 __host__ __device__ constexpr int fea5_ctas(int p) { return 1; }
 __host__ __device__ constexpr int fea5_nsplit(int p) { return p == 2 ? 2 : 1; }  // units per tile (P2: column halves)
 __host__ __device__ constexpr int fea5_threads(int p) { return fea5_nw(p) * 32; }
