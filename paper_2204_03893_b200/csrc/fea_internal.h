@@ -103,7 +103,7 @@ __host__ __device__ constexpr int fea5_item_bytes(int C) {
 // ---- kernel v5 (p <= 2 with the configs' native rules): lane-per-element, constant-bank tables.
 // NW warps per CTA (no producer warp), one CTA per SM, and the units per 32-element tile.
 #ifndef FEA5_NW1
-#define FEA5_NW1 16  // warps per CTA for P1 (P2: 16)
+#define FEA5_NW1 20  // warps per CTA for P1 (P2: 16); C4: 16 1.148 ms, 20 1.130, 24 1.191
 #endif
 __host__ __device__ constexpr int fea5_nw(int p) { return p == 1 ? FEA5_NW1 : 16; }
 __host__ __device__ constexpr int fea5_ctas(int p) { return 1; }

@@ -12,7 +12,7 @@ for role in ('A_','B','P_'):
 "
 done
 FEA_BUILD_DEFS="-DFEA6_DBGMODES" python -m paper_2204_03893_b200.build --force > /dev/null 2>&1 || exit 1
-for m in ${MODES:-0 1 3 4 6 11}; do
+for m in ${MODES:-0 1 2 3 4 6 11}; do
   FEA_DEBUG_MODE=$m timeout 300 python bench.py --config $cfg $extra --steps 5 --warmup 3 --no-cpu-baseline > gpurun_out/dm.json 2>/dev/null
   python -c "
 import json; d=json.load(open('gpurun_out/dm.json')); print('skip mode $m', round(d['roofline']['kernel_ms_median'],3))"
