@@ -402,6 +402,20 @@ __host__ __device__ constexpr int fea6_tile(int p, int w, int r) {
                          : (r == 0 ? (int)((M3 >> (4 * w)) & 15) : 15);
     return x == 15 ? -1 : x;
 }
+// the map holds every row tile exactly once (checked at compile time in fea_kernels6.cu)
+__host__ __device__ constexpr bool fea6_tile_map_ok(int p) {
+    const int ntt = p == 4 ? 15 : 7, na = fea6_na(p), rt = fea6_rt(p);
+    for (int t = 0; t < ntt; ++t) {
+        int n = 0;
+        for (int w = 0; w < na; ++w)
+            for (int r = 0; r < rt; ++r) n += fea6_tile(p, w, r) == t;
+        if (n != 1) return false;
+    }
+    for (int w = 0; w < na; ++w)
+        for (int r = 0; r < rt; ++r)
+            if (fea6_tile(p, w, r) >= ntt) return false;
+    return true;
+}
 // producer rounds (elements le = 32 h + lane, h < rounds): caps e_max at 32 * rounds
 #ifndef FEA6_P3_ROUNDS
 #define FEA6_P3_ROUNDS 3

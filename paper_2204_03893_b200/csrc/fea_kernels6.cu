@@ -68,7 +68,7 @@ __global__ void __maxnreg__(fea6_maxnreg(P)) k_reassemble6(const __grid_constant
 #endif
     constexpr int oW = (NP * NQ + 1) & ~1;
     static_assert(NA * RT >= NTT, "row tiles");
-    static_assert(fea6_tile(P, 0, 0) >= 0, "tile map");
+    static_assert(fea6_tile_map_ok(P), "tile map: every row tile on exactly one A warp");
     static_assert(FEA6_A1MODE(P) != 3 || FEA6_PROD_ASYNC(P), "A1 on the producer needs the async producer");
     const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
     const int e_max = prm.e_max, ls = fea6_lstride(e_max), vs = fea6_vstride(e_max);
