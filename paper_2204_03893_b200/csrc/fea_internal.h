@@ -317,6 +317,9 @@ int fea_kernel_occupancy5(int order, int do_m, int do_c, int smem_bytes, int* ct
 #define FEA6_A2PF 0  // A2: bit 0 next column tile's B fragments prefetched, bit 1 W once per column tile
                      // (measured C5: 0 11.65 ms, 1 14.15, 2 12.12, 3 14.57 -- register pressure)
 #endif
+#ifndef FEA6_A1A
+#define FEA6_A1A 4  // A1MODE 4 (split A1): element tiles of A1 the A warps take (at most half)
+#endif
 #ifndef FEA6_A1POS
 #define FEA6_A1POS 0  // A1MODE 2: a warp's A1 unit at column tile (net * A1POS) / 4 of A2
                       // (C5: 0 11.76 ms, 1 12.00, 2 12.20, 3 12.32; A1 on the B warps 13.21)
@@ -324,8 +327,12 @@ int fea_kernel_occupancy5(int order, int do_m, int do_c, int smem_bytes, int* ct
 #if defined(FEA6_A1MODE_P4)  // (experiments: the P4 mode alone)
 #define FEA6_A1MODE(p) ((p) == 4 ? FEA6_A1MODE_P4 : 0)
 #endif
+// 4 = split (P3): the B warps run A1's first element tiles two blocks ahead of their phase B, the
+// A warps the last FEA6_A1A tiles at the start of A2 of the previous block (C3: the B warps were
+// the bottleneck, 61 % of their time in A1 with k = exp(0.5 u); 1.439 -> 1.416 ms; all on the A
+// warps 1.516, FEA6_A1A 2 / 6: 1.605 / 1.479)
 #ifndef FEA6_A1MODE
-#define FEA6_A1MODE(p) ((p) == 4 ? 2 : 0)
+#define FEA6_A1MODE(p) ((p) == 4 ? 2 : 4)
 #endif
 // phase-B warps: P4 (FEA6_P4_MERGED 1) none -- the 15 DMMA warps (one row tile each) run phase B of
 // the previous block after their A2, v5-style; P3: 7 (the DMMA warps run A2 only)

@@ -93,12 +93,12 @@ __global__ void __maxnreg__(fea6_maxnreg(P)) k_reassemble6(const __grid_constant
     if (tid == 0) {
         for (int b = 0; b < 2; ++b) {
             mbar_init(&gat_full[b], 33);  // 32 lanes' cp.async completions + the geometry stores
-            mbar_init(&gat_free[b], FEA6_A1MODE(P) == 2 ? NA : FEA6_A1MODE(P) == 3 ? 1 : NB);
+            mbar_init(&gat_free[b], FEA6_A1MODE(P) == 2 ? NA : FEA6_A1MODE(P) == 3 ? 1 : FEA6_A1MODE(P) == 4 ? NA + NB : NB);
             mbar_init(&v_full[b], NA);
             mbar_init(&v_free[b], NB > 0 ? NB : NA);
         }
         for (int b = 0; b < 3; ++b) {
-            mbar_init(&lam_full[b], FEA6_A1MODE(P) == 2 ? NA : FEA6_A1MODE(P) == 3 ? 1 : NB);
+            mbar_init(&lam_full[b], FEA6_A1MODE(P) == 2 ? NA : FEA6_A1MODE(P) == 3 ? 1 : FEA6_A1MODE(P) == 4 ? NA + NB : NB);
             mbar_init(&lam_free[b], NA);
         }
         fence_mbar_init();
@@ -124,18 +124,21 @@ __global__ void __maxnreg__(fea6_maxnreg(P)) k_reassemble6(const __grid_constant
     constexpr int A1MODE = FEA6_A1MODE(P);
     const double* cW = prm.ctab + oW;
     const FeaCoef& cf = DO_M ? prm.coef_m : prm.coef_c;  // one coefficient (distinct ones: two passes)
-    auto do_a1 = [&](int j, int aw, int naw, int nE) {
+    // part (A1MODE 4): 1 = the B warps' element tiles [0, net - nA), 2 = the A warps' last nA tiles
+    auto a1_na = [&](int net) { return A1MODE == 4 ? min(FEA6_A1A, net >> 1) : 0; };
+    auto do_a1 = [&](int j, int aw, int naw, int nE, int part = 0) {
         const int g8 = lane >> 2, cq = lane & 3;
         const int g = j & 1;
         const int net = (nE + 7) >> 3;
+        const int lo = part == 2 ? net - a1_na(net) : 0, hi = part == 1 ? net - a1_na(net) : net;
         const int l3 = j % 3;
         double* Lam = sLW(l3);
         if (j >= 3) mbar_wait(&lam_free[l3], (uint32_t)(((j / 3) - 1) & 1));
-        if (aw < net) mbar_wait(&gat_full[g], (uint32_t)((j >> 1) & 1));
+        if (lo + aw < hi) mbar_wait(&gat_full[g], (uint32_t)((j >> 1) & 1));
         const double* gU = sGU(g);
         const double* gw = sDet(g);
-        const int net_run = DBGM && (prm.dbg_mode & 2) ? 0 : net;  // diagnostics: A1 skipped
-        for (int et = aw; et < net_run; et += naw) {  // one element tile, all m-tiles (independent chains)
+        const int hi_run = DBGM && (prm.dbg_mode & 2) ? 0 : hi;  // diagnostics: A1 skipped
+        for (int et = lo + aw; et < hi_run; et += naw) {  // one element tile, all m-tiles (independent chains)
             const double* spf = reinterpret_cast<const double*>(smem + prm.lay[FEA6_L_PF]);
             double pf[MT][KT];  // Phi^T A-fragments (shared memory)
 #pragma unroll
@@ -490,7 +493,9 @@ __global__ void __maxnreg__(fea6_maxnreg(P)) k_reassemble6(const __grid_constant
                 }
         T6_DECL
         int nE_n = nb > 0 ? ldg_s32(&prm.blocks[b0].nE) : 0;  // one block ahead (L2 latency; asm volatile: issued here)
-        if (A1MODE == 2 && nb > 0) do_a1(0, NA - 1 - warp, NA, nE_n);
+        constexpr bool A1A = A1MODE == 2 || A1MODE == 4;  // the A warps run (part of) A1
+        constexpr int A1PART = A1MODE == 4 ? 2 : 0;
+        if (A1A && nb > 0) do_a1(0, NA - 1 - warp, NA, nE_n, A1PART);
         BState st;  // NB == 0: the A warps also run phase B (of the previous block, after their A2)
         BDesc bd;
         if (NB == 0 && nb > 0) {
@@ -512,10 +517,11 @@ __global__ void __maxnreg__(fea6_maxnreg(P)) k_reassemble6(const __grid_constant
             T6_TICK(3)
             uint8_t* Vb = sV(g);
             const int net_a2 = DBGM && (prm.dbg_mode & 4) ? 0 : net;  // diagnostics: A2 skipped
-            if (DBGM && (prm.dbg_mode & 4) && A1MODE == 2 && j + 1 < nb) do_a1(j + 1, NA - 1 - warp, NA, nE_n);
+            if (DBGM && (prm.dbg_mode & 4) && A1A && j + 1 < nb) do_a1(j + 1, NA - 1 - warp, NA, nE_n, A1PART);
             // A1(j + 1) inside A2(j): a warp with an A1 unit runs it at column tile a1_at (FEA6_A1POS
             // quarters of the block), a warp without one only arrives, at the start
-            const int a1_at = NA - 1 - warp < ((nE_n + 7) >> 3) ? (net * FEA6_A1POS) >> 2 : 0;
+            const int net_n = (nE_n + 7) >> 3;
+            const int a1_at = NA - 1 - warp < (A1MODE == 4 ? a1_na(net_n) : net_n) ? (net * FEA6_A1POS) >> 2 : 0;
             // FEA6_A2PF: the next column tile's B fragments and row-tile mask load while this tile's
             // DMMAs run; the W factors once per column tile, before its DMMAs
             uint32_t tm_n = 0;
@@ -528,9 +534,9 @@ __global__ void __maxnreg__(fea6_maxnreg(P)) k_reassemble6(const __grid_constant
             int32_t cbase = 0;  // compact V: needed row tiles of the column tiles before et
             for (int et = 0; et < net_a2; ++et) {
                 // (units to the last warps first: warp NA - 1 holds one row tile less)
-                if (A1MODE == 2 && et == a1_at && j + 1 < nb) {
+                if (A1A && et == a1_at && j + 1 < nb) {
                     T6_TICK(4)
-                    do_a1(j + 1, NA - 1 - warp, NA, nE_n);
+                    do_a1(j + 1, NA - 1 - warp, NA, nE_n, A1PART);
                     T6_TICK(1)
                 }
                 const int le0 = et * 8 + 2 * cq;
@@ -615,7 +621,7 @@ __global__ void __maxnreg__(fea6_maxnreg(P)) k_reassemble6(const __grid_constant
     // (A1 runs two blocks ahead of phase B and one to two ahead of A2: three Lambda buffers).
     if (NB > 0) {
         const int bt = tid - NA * 32, bw = bt >> 5;
-        constexpr int LAG = A1MODE == 0 ? 2 : 0;  // phase B of block j - LAG after A1(j) (B warps running A1)
+        constexpr int LAG = A1MODE == 0 || A1MODE == 4 ? 2 : 0;  // phase B of block j - LAG after A1(j) (B warps running A1)
         int nE_a = nb > 0 ? ldg_s32(&prm.blocks[b0].nE) : 0;  // A1's block size, one block ahead
         BState st;
         BDesc bd;
@@ -625,10 +631,10 @@ __global__ void __maxnreg__(fea6_maxnreg(P)) k_reassemble6(const __grid_constant
         }
         T6_DECL
         for (int j = 0; j < nb + LAG; ++j) {
-            if (A1MODE == 0 && j < nb) {
+            if ((A1MODE == 0 || A1MODE == 4) && j < nb) {
                 const int nE = nE_a;
                 if (j + 1 < nb) nE_a = ldg_s32(&prm.blocks[b0 + (j + 1) * G].nE);
-                do_a1(j, bw, NB, nE);
+                do_a1(j, bw, NB, nE, A1MODE == 4 ? 1 : 0);
                 T6_TICK(6)
             }
             if (j < LAG) continue;
