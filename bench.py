@@ -321,7 +321,7 @@ def run_ours(args):
     achieved = B / (kern_ms * 1e-3) / 1e9
     traffic = None
     if tensor:
-        kname = "k_tensor4" if asm.ctx.stat(12) == 4 else "k_tensor"
+        kname = {4: "k_tensor4", 5: "k_tensor5"}.get(asm.ctx.stat(12), "k_tensor")
     else:
         kname = {5: "k_reassemble5", 6: "k_reassemble6"}.get(asm.ctx.stat(11), "k_reassemble")
     prof = os.path.join(ROOT, "profiles", f"ncu_traffic_{cfg.name}_{kname}.json")

@@ -16,7 +16,7 @@ LIB = os.path.join(HERE, "libfea.so")
 OBJ = os.path.join(HERE, "build")
 NVCC = os.environ.get("NVCC", "/usr/local/cuda/bin/nvcc")
 ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
-SOURCES = ["fea_kernels.cu", "fea_kernels5.cu", "fea_kernels6.cu", "fea_kernels_t.cu", "fea_kernels_x.cu", "fea_host.cpp"]
+SOURCES = ["fea_kernels.cu", "fea_kernels5.cu", "fea_kernels6.cu", "fea_kernels_t.cu", "fea_kernels_t5.cu", "fea_kernels_x.cu", "fea_host.cpp"]
 DEPS = SOURCES + ["fea_internal.h", "fea_device.cuh"]
 
 

@@ -134,6 +134,7 @@ struct fea_ctx_s {
     uint8_t* dt_records = nullptr;
     int32_t* dt_dofs = nullptr;
     int t_nblocks = 0, t_emax = 0, t_smem = 0, t_grid = 0, t_kver = 0;
+    bool t_pm = false, t_pc = false;  // k_tensor5 plan: channels its shared-memory layout holds
     int64_t t_visits = 0, t_owned = 0;
     double t_rec_el = 0;  // k_tensor4 plan: record bytes per element of the first plan (re-plan)
     int32_t t_lay[FEA_LT_N] = {0};
@@ -204,6 +205,7 @@ struct fea_ctx_s {
         dfree(dt_records);
         dfree(dt_dofs);
         have_tplan = false;
+        t_pm = t_pc = false;
         t_rec_el = 0;
         dfree(d_vm);
         dfree(d_vc);
@@ -790,8 +792,10 @@ fea_status fea_set_tuning(fea_ctx c, int key, int64_t value) {
             if (value != 0 && value != 1) return c->fail(FEA_E_ARG, "pad flag must be 0 or 1");
             c->tune_pad1 = (int)value;
             break;
-        case 8:  // tensor kernel: 0 = automatic, 1 = lane per element (k_tensor), 4 = DMMA (k_tensor4)
-            if (value != 0 && value != 1 && value != 4) return c->fail(FEA_E_ARG, "tensor kernel must be 0, 1 or 4");
+        case 8:  // tensor kernel: 0 = automatic, 1 = lane per element (k_tensor), 4 = DMMA (k_tensor4),
+                 // 5 = the pipelined lane-per-element kernel (k_tensor5; P1 with the 3-point rule)
+            if (value != 0 && value != 1 && value != 4 && value != 5)
+                return c->fail(FEA_E_ARG, "tensor kernel must be 0, 1, 4 or 5");
             c->tune_tker = (int)value;
             break;
         case 12:  // kernel v6: ghost row-tile skipping with element rotations (1, default) or off (0)
@@ -1917,18 +1921,30 @@ fea_status fea_reassemble_host(fea_ctx c, const double* u_host, double* mass_hos
 }
 
 // Tensor plan: same rows as the matrix plan, v5 record format with orientation bits, blocks sized
-// for V1 + Vup + Vdn (3 T doubles per element) in one CTA per SM.
-static fea_status build_tensor_plan(fea_ctx c) {
+// for V1 + Vup + Vdn (3 T doubles per element) in one CTA per SM (k_tensor5: two buffers of the
+// channels wanted, want_m / want_c; a later call wanting another channel re-plans).
+static fea_status build_tensor_plan(fea_ctx c, bool want_m, bool want_c) {
     const int np = c->np, T = c->T;
     const int64_t budget = 227 * 1024;
     const int64_t tabs = 8LL * (3 * np * 16 + 16) + 256;
-    // kernel: k_tensor4 (DMMA) for p >= 2 or any non-native rule, k_tensor (lane per element) for
-    // P1 with its 3-point rule (measured faster there: 3.26 vs 5.20 ms on C4)
+    // kernel: k_tensor4 (DMMA) for p >= 2 or any non-native rule, k_tensor5 (lane per element,
+    // pipelined) for P1 with its 3-point rule (C4: 3.13 ms with k_tensor, 5.20 with k_tensor4)
     const bool native = c->nq == fea_nq_native(c->order) && (!c->split || c->nq_c == fea_nq_native(c->order));
-    c->t_kver = c->tune_tker ? c->tune_tker : (c->order >= 2 || !native ? 4 : 1);
-    const bool k4 = c->t_kver == 4;
+    const bool t5ok = fea_t5_supported(c->order, c->nq) && !c->split;
+    c->t_kver = c->tune_tker ? c->tune_tker : (t5ok ? 5 : c->order >= 2 || !native ? 4 : 1);
+    if (c->t_kver == 5 && !t5ok)
+        return c->fail(FEA_E_UNSUPPORTED, "k_tensor5 needs P1 with its 3-point rule (one rule for both matrices)");
+    const bool k4 = c->t_kver == 4, k5 = c->t_kver == 5;
     int64_t e_max, rec_budget;
-    if (k4) {  // V1, Vup, Vdn [T][e_max + 2], two record and gather stages, Lambda and p (fea_t4_smem_layout)
+    if (k5) {  // two V buffers of the wanted channels, two record stages (fea_t5_smem_layout)
+        const int rows = fea_t5_rows(c->order, want_m, want_c);
+        const double rec_el = 1.1 * 2.0 * np * np + 8;
+        const int64_t fixed = 64 + 512 + 2 * 256 + 2048;
+        e_max = (int64_t)((budget - fixed) / (16.0 * rows + 2 * rec_el));
+        if (c->tune_emax) e_max = std::min(e_max, c->tune_emax);
+        e_max = std::min<int64_t>(e_max, 32767 / T - 1) / 8 * 8;
+        rec_budget = ((budget - fixed - 16LL * (rows * (e_max | 1) + 16)) / 2) & ~int64_t(15);
+    } else if (k4) {  // V1, Vup, Vdn [T][e_max + 2], two record and gather stages, Lambda and p (fea_t4_smem_layout)
         const int nqp = c->split ? 16 : 4 * fea_nk_kernel(c->order, c->nq);
         const int64_t per_el = 8LL * (3 * T - np) + 2 * (16LL * np + 48) + 3 * 8LL * nqp;
         // record bytes per element: an estimate, then (below) the planned blocks' own ratio
@@ -1954,8 +1970,13 @@ static fea_status build_tensor_plan(fea_ctx c) {
         c->t_smem = c->t_lay[FEA_LT4_TOTAL];
         if (c->t_rec_el == 0 && e_max > 0) {  // one re-plan with the measured record bytes per element
             c->t_rec_el = 1.02 * (double)P.rec_max / (double)e_max;
-            if (budget - c->t_smem > 8 * 1024) return build_tensor_plan(c);
+            if (budget - c->t_smem > 8 * 1024) return build_tensor_plan(c, want_m, want_c);
         }
+    } else if (k5) {
+        fea_t5_smem_layout(c->t_lay, (int)P.rec_max, (int)e_max, c->order, want_m, want_c);
+        c->t_smem = c->t_lay[FEA_LT5_TOTAL];
+        c->t_pm = want_m;
+        c->t_pc = want_c;
     } else {
         fea_t_smem_layout(c->t_lay, (int)P.rec_max, (int)e_max, c->order);
         c->t_smem = c->t_lay[FEA_LT_TOTAL];
@@ -1971,7 +1992,8 @@ static fea_status build_tensor_plan(fea_ctx c) {
     FEA_CUDA(c, cudaMalloc((void**)&c->dt_dofs, P.dofs.size() * sizeof(int32_t)));
     FEA_CUDA(c, cudaMemcpy(c->dt_dofs, P.dofs.data(), P.dofs.size() * sizeof(int32_t), cudaMemcpyHostToDevice));
     int occ = 0, thr = 0;
-    const int rc = fea_tensor_occupancy(c->order, c->nq, c->t_kver, c->t_smem, &occ, &thr);
+    const int rc = k5 ? fea_tensor_occupancy5(c->order, c->nq, c->t_smem, &occ, &thr)
+                      : fea_tensor_occupancy(c->order, c->nq, c->t_kver, c->t_smem, &occ, &thr);
     if (rc != 0) return c->fail(FEA_E_CUDA, "tensor occupancy: %s", cudaGetErrorString((cudaError_t)rc));
     if (occ < 1) return c->fail(FEA_E_UNSUPPORTED, "tensor kernel does not fit: %d B shared memory", c->t_smem);
     c->t_grid = (int)std::min<int64_t>(std::max<int64_t>(nb, 1), (int64_t)occ * c->sm_count);
@@ -1988,8 +2010,15 @@ fea_status fea_assemble_tensor(fea_ctx c, const double* u_full, const double* v_
         return c->fail(FEA_E_ARG, "vals must be 16-byte aligned");
     if (!mt_vals && !ct_vals) return FEA_OK;
     cudaSetDevice(c->device);
+    if (c->have_tplan && c->t_kver == 5 && ((mt_vals && !c->t_pm) || (ct_vals && !c->t_pc))) {
+        // k_tensor5's layout holds only the channels of the first call: re-plan for the union
+        dfree(c->dt_blocks);
+        dfree(c->dt_records);
+        dfree(c->dt_dofs);
+        c->have_tplan = false;
+    }
     if (!c->have_tplan) {
-        const fea_status st = build_tensor_plan(c);
+        const fea_status st = build_tensor_plan(c, mt_vals || c->t_pm, ct_vals || c->t_pc);
         if (st != FEA_OK) return st;
     }
     if (c->t_nblocks == 0) return FEA_OK;
@@ -2013,6 +2042,13 @@ fea_status fea_assemble_tensor(fea_ctx c, const double* u_full, const double* v_
     prm.coef_c = c->coef_c;
     prm.same_coef = same_coef(c->coef_m, c->coef_c) ? 1 : 0;
     prm.n_dof = c->n_dof;
+    if (c->t_kver == 5) {  // constant-bank tables (kernel v5's layout: Phi, w; J)
+        std::memcpy(prm.ctab, c->tables.data(), std::min<size_t>(c->tables.size(), FEA_CTAB_MAX) * sizeof(double));
+        std::memcpy(prm.jtab, c->jplain.data(), std::min<size_t>(c->jplain.size(), FEA_JTAB_MAX) * sizeof(double));
+        const int rc = fea_launch_tensor5(prm, c->order, c->t_smem, c->t_grid, c->stream);
+        if (rc != 0) return c->fail(FEA_E_CUDA, "k_tensor5 launch: %s", cudaGetErrorString((cudaError_t)rc));
+        return FEA_OK;
+    }
     if (prm.out_m || prm.out_c) {
         const int rc = fea_launch_tensor(prm, c->order, c->t_smem, c->t_grid, c->stream);
         if (rc != 0) return c->fail(FEA_E_CUDA, "k_tensor launch: %s", cudaGetErrorString((cudaError_t)rc));

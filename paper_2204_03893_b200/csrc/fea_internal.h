@@ -281,9 +281,45 @@ struct FeaTParams {
     int64_t n_dof;                     // extent, for the FEA_BOUNDS_CHECK build
     int32_t lay[FEA_LT_N];
     FeaCoef coef_m, coef_c;  // k' of these
+    double ctab[FEA_CTAB_MAX];  // k_tensor5: Phi [np][nq] at 0, w [nq] at pad2(np nq) (constant-bank operands)
+    double jtab[FEA_JTAB_MAX];  // k_tensor5: J [2][np][nq]
 };
 int fea_launch_tensor(const FeaTParams& prm, int order, int smem_bytes, int grid, void* stream);
 int fea_tensor_occupancy(int order, int nq, int kver, int smem_bytes, int* ctas_per_sm, int* threads);
+// k_tensor5 (fea_kernels_t5.cu): P1 with its native 3-point rule, the v5 software pipeline (double-
+// buffered V and records, NW warps, descriptor ring).  Shared memory: two V buffers of
+// L[FEA_LT5_VBUF] doubles each holding V1 [T][vs] (at L[FEA_LT5_O1] doubles, if the plan has the
+// mass channel), Vup [T][vs] and Vdn [T - np][vs] (at L[FEA_LT5_OU] / L[FEA_LT5_OD], conductivity
+// channel); two record stages of stride L[FEA_LT5_RS]; mbarriers (6); descriptor ring (8 x 64 B).
+enum { FEA_LT5_V = 0, FEA_LT5_VBUF = 1, FEA_LT5_O1 = 2, FEA_LT5_OU = 3, FEA_LT5_OD = 4, FEA_LT5_REC = 5,
+       FEA_LT5_RS = 6, FEA_LT5_BARS = 7, FEA_LT5_RING = 8, FEA_LT5_TOTAL = 9 };
+#ifndef FEA_T5_NW
+#define FEA_T5_NW 16
+#endif
+__host__ __device__ constexpr int fea_t5_nw(int p) { return FEA_T5_NW; }
+__host__ __device__ constexpr int fea_t5_threads(int p) { return fea_t5_nw(p) * 32; }
+__host__ __device__ constexpr bool fea_t5_supported(int p, int nq) { return p == 1 && nq == 3; }
+// V rows per element of one buffer for the planned channels
+__host__ __device__ constexpr int fea_t5_rows(int p, bool m, bool c) {
+    return (m ? fea_T(p) : 0) + (c ? 2 * fea_T(p) - fea_np(p) : 0);
+}
+__host__ __device__ inline void fea_t5_smem_layout(int32_t* L, int rec_max, int e_max, int p, bool m, bool c) {
+    const int T = fea_T(p), np = fea_np(p), vs = e_max | 1;
+    for (int i = 0; i < FEA_LT_N; ++i) L[i] = 0;
+    L[FEA_LT5_O1] = 0;
+    L[FEA_LT5_OU] = (m ? T : 0) * vs;
+    L[FEA_LT5_OD] = L[FEA_LT5_OU] + (c ? T : 0) * vs;
+    L[FEA_LT5_VBUF] = (L[FEA_LT5_OD] + (c ? T - np : 0) * vs + 15) & ~15;  // 128-byte buffers
+    int32_t o = 0;
+    L[FEA_LT5_V] = o; o += 2 * 8 * L[FEA_LT5_VBUF];
+    L[FEA_LT5_RS] = (rec_max + 127) / 128 * 128;
+    L[FEA_LT5_REC] = o; o += 2 * L[FEA_LT5_RS];
+    L[FEA_LT5_BARS] = o; o += 64;
+    L[FEA_LT5_RING] = o; o += 64 * 8;
+    L[FEA_LT5_TOTAL] = o;
+}
+int fea_launch_tensor5(const FeaTParams& prm, int order, int smem_bytes, int grid, void* stream);
+int fea_tensor_occupancy5(int order, int nq, int smem_bytes, int* ctas_per_sm, int* threads);
 
 // interface-only exchange of u (fea_kernels_x.cu)
 int fea_launch_pack(const double* u_owned, const int32_t* I, int nI, int64_t R0, int maxI, double* send, void* stream);

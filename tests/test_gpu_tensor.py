@@ -19,6 +19,8 @@ TOL = 1e-12
 def _run(mesh, q_xy, q_w, u_user, v_user, p, mcoef, ccoef, do_m=True, do_c=True, reorder=True, tker=0):
     import torch
     from paper_2204_03893_b200.fea import FEA_MASS, FEA_STIFF, FEA_TUNE_TENSOR_KERNEL, Context
+    if tker == 5 and not (p == 1 and len(q_w) == 3):
+        pytest.skip("k_tensor5 covers P1 with its 3-point rule")
     ctx = Context(device=0)
     ctx.set_element(p, q_xy, q_w)
     ctx.mesh_upload(mesh.vert_xy, mesh.elem_vert, mesh.n_dof, mesh.elem_dof, reorder=reorder)
@@ -35,7 +37,7 @@ def _run(mesh, q_xy, q_w, u_user, v_user, p, mcoef, ccoef, do_m=True, do_c=True,
     ct = torch.full((n,), np.nan, dtype=torch.float64, device=dev) if do_c else None
     ctx.assemble_tensor(u, v, mt, ct)
     ctx.sync()
-    assert ctx.stat(12) == (tker or ctx.stat(12)) and ctx.stat(12) in (1, 4)
+    assert ctx.stat(12) == (tker or ctx.stat(12)) and ctx.stat(12) in (1, 4, 5)
     rp, ci = ctx.get_pattern()
     mlib = copy.copy(mesh)
     mlib.elem_dof = lib_numbering(mesh, perm)
@@ -56,7 +58,9 @@ def _run(mesh, q_xy, q_w, u_user, v_user, p, mcoef, ccoef, do_m=True, do_c=True,
     return out
 
 
-TKER = [1, 4]  # FEA_TUNE_TENSOR_KERNEL: k_tensor (lane per element), k_tensor4 (DMMA)
+# FEA_TUNE_TENSOR_KERNEL: k_tensor (lane per element), k_tensor4 (DMMA), k_tensor5 (lane per element,
+# pipelined; P1 with the 3-point rule only: other cases skip)
+TKER = [1, 4, 5]
 
 
 @pytest.mark.parametrize("tker", TKER)
@@ -146,3 +150,56 @@ def test_tensor4_deterministic_across_tilings(p):
     assert outs[2][0] > outs[0][0]  # a finer tiling
     for nb, mt, ct in outs[1:]:
         assert np.array_equal(outs[0][1], mt) and np.array_equal(outs[0][2], ct)
+
+
+def test_tensor5_replan_and_tilings():
+    """k_tensor5 (P1, 3-point rule): a first call with one channel plans shared memory for it only;
+    a later call with both re-plans.  Values are bit-identical across calls, element caps per block
+    (FEA_TUNE_EMAX) and against a fresh context, and match the oracle (reading 11)."""
+    import torch
+    from paper_2204_03893_b200.fea import FEA_MASS, FEA_STIFF, FEA_TUNE_EMAX, FEA_TUNE_TENSOR_KERNEL, Context
+    m = random_mesh_from_structured(24, 1, seed=341)
+    xy, w = triangle_rule(2)
+    assert len(w) == 3
+    rng = np.random.default_rng(41)
+    u = rng.uniform(-1, 1, m.n_dof)
+    v = rng.normal(size=m.n_dof)
+    dev = "cuda:0"
+    runs = []
+    for cap, seq in ((0, ("C", "MC")), (0, ("M", "MC")), (40, ("MC",)), (64, ("C", "M"))):
+        ctx = Context(device=0)
+        ctx.set_element(1, xy, w)
+        ctx.mesh_upload(m.vert_xy, m.elem_vert, m.n_dof, m.elem_dof)
+        ctx.set_tuning(FEA_TUNE_TENSOR_KERNEL, 5)
+        ctx.set_tuning(FEA_TUNE_EMAX, cap)
+        ctx.build_pattern()
+        ctx.set_coefficient(FEA_MASS, K_EXP, (1.3, 0.5))
+        ctx.set_coefficient(FEA_STIFF, K_POLY, (1.0, 0.0, 1.0))
+        perm = ctx.get_dof_perm()
+        ut, vt = torch.tensor(u[perm], device=dev), torch.tensor(v[perm], device=dev)
+        got = {}
+        for which in seq:
+            mt = torch.full((ctx.nnz,), np.nan, dtype=torch.float64, device=dev) if "M" in which else None
+            ct = torch.full((ctx.nnz,), np.nan, dtype=torch.float64, device=dev) if "C" in which else None
+            ctx.assemble_tensor(ut, vt, mt, ct)
+            ctx.sync()
+            assert ctx.stat(12) == 5
+            for k, t in (("M", mt), ("C", ct)):
+                if t is not None:
+                    g = t.cpu().numpy()
+                    assert np.isfinite(g).all()
+                    if k in got:
+                        assert np.array_equal(got[k], g)
+                    got[k] = g
+        runs.append((ctx.stat(16), got))
+        if cap == 0 and seq[0] == "C":
+            mlib = copy.copy(m)
+            mlib.elem_dof = lib_numbering(m, perm)
+            ref = oracle.assemble_tensor_contraction(mlib, xy, w, np.ascontiguousarray(u[perm]),
+                                                     np.ascontiguousarray(v[perm]),
+                                                     m_coef=(K_EXP, (1.3, 0.5)), c_coef=(K_POLY, (1.0, 0.0, 1.0)))
+            assert maxabs_rel(got["M"], ref.M) <= TOL and maxabs_rel(got["C"], ref.K) <= TOL
+        ctx.close()
+    assert runs[2][0] > runs[0][0]  # a finer tiling
+    for _, got in runs[1:]:
+        assert np.array_equal(runs[0][1]["M"], got["M"]) and np.array_equal(runs[0][1]["C"], got["C"])
