@@ -364,6 +364,37 @@ __device__ __forceinline__ double dkeval(const FeaCoef& c, double u) {
     return (c.par[2 * s + 3] - c.par[2 * s + 1]) / (c.par[2 * s + 2] - c.par[2 * s]);
 }
 
+static __device__ __noinline__ double dk_exp(double c0, double c1, double u) { return c0 * c1 * exp(c1 * u); }
+static __device__ __noinline__ double dk_pwl(const FeaCoef& c, double u) { return dkeval(c, u); }
+// k'(u_q) for all N quadrature points at once (the same per-point arithmetic as dkeval: Horner on
+// i par_i from the top, the N points as independent FMA chains; exp / PWL out of line)
+template <int N>
+__device__ __forceinline__ void dkeval_all(const FeaCoef& c, const double (&u)[N], double (&k)[N]) {
+    if (c.kind == 0) {
+        const int n = c.npar;
+        if (n <= 1) {
+#pragma unroll
+            for (int q = 0; q < N; ++q) k[q] = 0.0;
+            return;
+        }
+        const double top = (double)(n - 1) * c.par[n - 1];
+#pragma unroll
+        for (int q = 0; q < N; ++q) k[q] = top;
+#pragma unroll 1
+        for (int i = n - 2; i >= 1; --i) {
+            const double a = (double)i * c.par[i];
+#pragma unroll
+            for (int q = 0; q < N; ++q) k[q] = fma(k[q], u[q], a);
+        }
+    } else if (c.kind == 1) {
+#pragma unroll
+        for (int q = 0; q < N; ++q) k[q] = dk_exp(c.par[0], c.par[1], u[q]);
+    } else {
+#pragma unroll
+        for (int q = 0; q < N; ++q) k[q] = dk_pwl(c, u[q]);
+    }
+}
+
 // L2 prefetch of a byte range (bulk, no completion tracking); bytes a multiple of 16
 __device__ __forceinline__ void prefetch_l2(const void* p, uint32_t bytes) {
     asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;" ::"l"(p), "r"(bytes) : "memory");

@@ -87,35 +87,48 @@ __global__ void __launch_bounds__(fea_t5_threads(P), 1) k_tensor5(const __grid_c
     if (tid == 0)
         for (int k = 0; k < PF && k < nb; ++k) prefetch_blk(k);
 
-    // ---- tile stream cursors: block s of this CTA, 32-element tile t of the block
-    auto ntiles = [&](int k) { return (blk_of(k).nE + 31) >> 5; };
-    auto settle = [&](int& k, int& t) {
-        while (k < nb && t >= ntiles(k)) {
-            ++k;
-            t = warp;
+    // ---- tile stream cursors: block k of this CTA, 32-element tile t of the block; the block's
+    // element count and DOF offset are kept in registers (read from the ring once per block: the
+    // compiler cannot keep shared-memory values across the V stores)
+    struct Cur {
+        int k, t, nE;
+        int64_t doff;
+    };
+    auto enter = [&](Cur& c) {
+        if (c.k < nb) {
+            const FeaBlock& b = blk_of(c.k);
+            c.nE = b.nE;
+            c.doff = b.dof_off;
         }
     };
-    auto advance = [&](int& k, int& t) {
-        t += NW;
-        settle(k, t);
+    auto settle = [&](Cur& c) {
+        while (c.k < nb && c.t * 32 >= c.nE) {
+            ++c.k;
+            c.t = warp;
+            enter(c);
+        }
     };
-    int cs = 0, ct = warp;  // compute cursor
-    settle(cs, ct);
-    int ls = cs, lt = ct;  // load cursor
+    auto advance = [&](Cur& c) {
+        c.t += NW;
+        settle(c);
+    };
+    Cur cc{0, warp, 0, 0};  // compute cursor
+    enter(cc);
+    settle(cc);
+    Cur lc = cc;  // load cursor
     int dof[NP];
-    auto load_dofs = [&](int k, int t) {
-        const FeaBlock& b = blk_of(k);
-        const int le = t * 32 + lane;
-        if (le < b.nE) {
-            const int32_t* d = prm.dofs + b.dof_off + le;
-            const int nEp = fea_pad4(b.nE);
+    auto load_dofs = [&]() {
+        const int le = lc.t * 32 + lane;
+        if (le < lc.nE) {
+            const int32_t* d = prm.dofs + lc.doff + le;
+            const int nEp = fea_pad4(lc.nE);
 #pragma unroll
             for (int i = 0; i < NP; ++i) dof[i] = ldg_s32(d + i * nEp);
         }
     };
     auto refill = [&](GathT<NP>& g) {
-        if (ls >= nb) return;
-        if (lt * 32 + lane < blk_of(ls).nE) {
+        if (lc.k >= nb) return;
+        if (lc.t * 32 + lane < lc.nE) {
 #pragma unroll
             for (int i = 0; i < NP; ++i) FEA_CHECK(dof[i] >= 0 && dof[i] < prm.n_dof);
 #pragma unroll
@@ -126,8 +139,8 @@ __global__ void __launch_bounds__(fea_t5_threads(P), 1) k_tensor5(const __grid_c
 #pragma unroll
             for (int v = 0; v < 3; ++v) g.x[v] = ldg_f64x2(prm.xy + dof[v]);
         }
-        advance(ls, lt);
-        if (ls < nb) load_dofs(ls, lt);
+        advance(lc);
+        if (lc.k < nb) load_dofs();
     };
 
     // ---- A: one element per lane (k_tensor's arithmetic, operands from the constant bank)
@@ -145,25 +158,38 @@ __global__ void __launch_bounds__(fea_t5_threads(P), 1) k_tensor5(const __grid_c
         const double A11 = (B00 * B00 + B10 * B10) * inv;
         const double A01 = -(B00 * B01 + B10 * B11) * inv;
         // per quadrature point: lambda = w m'(u_q) |det| v_q, p = w c'(u_q) |det| A_e J_q^T v_e
+        double uq[NQ], vq[NQ], gxq[NQ], gyq[NQ], dm[NQ], dc[NQ];
+#pragma unroll
+        for (int q = 0; q < NQ; ++q) {
+            uq[q] = vq[q] = gxq[q] = gyq[q] = 0.0;
+#pragma unroll
+            for (int i = 0; i < NP; ++i) {
+                uq[q] = fma(Phi(i, q), g.u[i], uq[q]);
+                if (DO_M) vq[q] = fma(Phi(i, q), g.v[i], vq[q]);
+                if (DO_C) {
+                    gxq[q] = fma(J(0, i, q), g.v[i], gxq[q]);
+                    gyq[q] = fma(J(1, i, q), g.v[i], gyq[q]);
+                }
+            }
+        }
+        if (DO_M) dkeval_all<NQ>(prm.coef_m, uq, dm);
+        if (DO_C) {
+            if (DO_M && prm.same_coef) {
+#pragma unroll
+                for (int q = 0; q < NQ; ++q) dc[q] = dm[q];
+            } else {
+                dkeval_all<NQ>(prm.coef_c, uq, dc);
+            }
+        }
         double lam[NQ], p0[NQ], p1[NQ];
 #pragma unroll
         for (int q = 0; q < NQ; ++q) {
-            double uq = 0.0, vq = 0.0, gxq = 0.0, gyq = 0.0;
-#pragma unroll
-            for (int i = 0; i < NP; ++i) {
-                uq = fma(Phi(i, q), g.u[i], uq);
-                if (DO_M) vq = fma(Phi(i, q), g.v[i], vq);
-                if (DO_C) {
-                    gxq = fma(J(0, i, q), g.v[i], gxq);
-                    gyq = fma(J(1, i, q), g.v[i], gyq);
-                }
-            }
             const double wb = Wq(q) * absdet;
-            if (DO_M) lam[q] = wb * dkeval(prm.coef_m, uq) * vq;
+            if (DO_M) lam[q] = wb * dm[q] * vq[q];
             if (DO_C) {
-                const double lc = wb * dkeval(prm.coef_c, uq);
-                p0[q] = lc * fma(A00, gxq, A01 * gyq);
-                p1[q] = lc * fma(A01, gxq, A11 * gyq);
+                const double lcq = wb * dc[q];
+                p0[q] = lcq * fma(A00, gxq[q], A01 * gyq[q]);
+                p1[q] = lcq * fma(A01, gxq[q], A11 * gyq[q]);
             }
         }
         if (DO_M) {  // symmetric rows i <= k: sum_q phi_i phi_k lambda_q
@@ -203,7 +229,7 @@ __global__ void __launch_bounds__(fea_t5_threads(P), 1) k_tensor5(const __grid_c
 
     // ---- prologue: DOFs of the first tile, then two tiles of gathers in flight
     GathT<NP> ga, gb;
-    if (ls < nb) load_dofs(ls, lt);
+    if (lc.k < nb) load_dofs();
     refill(ga);
     refill(gb);
 
@@ -228,12 +254,12 @@ __global__ void __launch_bounds__(fea_t5_threads(P), 1) k_tensor5(const __grid_c
                 if (s + PF < nb) prefetch_blk(s + PF);
             }
             double* sV = sV0 + b * vbuf;
-            while (cs == s) {
-                const int le = ct * 32 + lane;
-                if (le < blk_of(s).nE) compute(ga, sV, le);
+            while (cc.k == s) {
+                const int le = cc.t * 32 + lane;
+                if (le < cc.nE) compute(ga, sV, le);
                 ga = gb;
                 refill(gb);
-                advance(cs, ct);
+                advance(cc);
             }
             __syncwarp();
             if (lane == 0) mbar_arrive(&full[b]);
