@@ -367,7 +367,7 @@ __device__ __forceinline__ double dkeval(const FeaCoef& c, double u) {
 static __device__ __noinline__ double dk_exp(double c0, double c1, double u) { return c0 * c1 * exp(c1 * u); }
 static __device__ __noinline__ double dk_pwl(const FeaCoef& c, double u) { return dkeval(c, u); }
 // k'(u_q) for all N quadrature points at once (the same per-point arithmetic as dkeval: Horner on
-// i par_i from the top, the N points as independent FMA chains; exp / PWL out of line)
+// i par_i from the top, the N points as independent FMA chains; PWL, and exp for N > 4, out of line)
 template <int N>
 __device__ __forceinline__ void dkeval_all(const FeaCoef& c, const double (&u)[N], double (&k)[N]) {
     if (c.kind == 0) {
@@ -388,7 +388,7 @@ __device__ __forceinline__ void dkeval_all(const FeaCoef& c, const double (&u)[N
         }
     } else if (c.kind == 1) {
 #pragma unroll
-        for (int q = 0; q < N; ++q) k[q] = dk_exp(c.par[0], c.par[1], u[q]);
+        for (int q = 0; q < N; ++q) k[q] = N <= 4 ? c.par[0] * c.par[1] * exp(c.par[1] * u[q]) : dk_exp(c.par[0], c.par[1], u[q]);
     } else {
 #pragma unroll
         for (int q = 0; q < N; ++q) k[q] = dk_pwl(c, u[q]);

@@ -319,17 +319,29 @@ __global__ void __launch_bounds__(fea_t4_threads(P, DO_M, DO_C), 1) k_tensor4(co
             const int q = mt * 8 + g, le0 = et * 8 + 2 * cq;
             if (q < NQP) {
                 double lm[2] = {0.0, 0.0}, p0[2] = {0.0, 0.0}, p1[2] = {0.0, 0.0};
+                // k'(u_q) of both accumulator columns at once (values of columns past nE are unused)
+                const double uqs[2] = {u0, u1};
+                double dms[2], dcs[2];
+                if (DO_M) dkeval_all<2>(prm.coef_m, uqs, dms);
+                if (DO_C) {
+                    if (DO_M && prm.same_coef) {
+                        dcs[0] = dms[0];
+                        dcs[1] = dms[1];
+                    } else {
+                        dkeval_all<2>(prm.coef_c, uqs, dcs);
+                    }
+                }
 #pragma unroll
                 for (int h = 0; h < 2; ++h) {
                     const int le = le0 + h;
                     if (le < nE && q < nq) {
                         double absdet, A00, A11, A01;
                         geometry(gX, e_max, le, absdet, A00, A11, A01);
-                        const double uq = h ? u1 : u0, wb = W[q] * absdet;
-                        const double dm = DO_M ? dkeval(prm.coef_m, uq) : 0.0;
+                        const double wb = W[q] * absdet;
+                        const double dm = DO_M ? dms[h] : 0.0;
                         if (DO_M) lm[h] = wb * dm * (h ? v1 : v0);
                         if (DO_C) {
-                            const double dc = DO_M && prm.same_coef ? dm : dkeval(prm.coef_c, uq);
+                            const double dc = dcs[h];
                             const double lc = wb * dc, gx = h ? x1 : x0, gy = h ? y1 : y0;
                             p0[h] = lc * fma(A00, gx, A01 * gy);
                             p1[h] = lc * fma(A01, gx, A11 * gy);
