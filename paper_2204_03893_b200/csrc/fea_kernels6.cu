@@ -586,7 +586,8 @@ __global__ void __maxnreg__(fea6_maxnreg(P)) k_reassemble6(const __grid_constant
                             c0 = fea6_vcell(cbase, tmask, tt, g8, 2 * cq);
                             c1 = fea6_vcell(cbase, tmask, tt, g8, 2 * cq + 1);
                         }
-                        FEA_CHECK(c0 > 0 && c0 < vcells && c1 > 0 && c1 < vcells);
+                        // (compact layout: cell 0 is the zero cell; dense: row 0, column 0 is a real cell)
+                        FEA_CHECK(c0 >= (FEA6_VCOMPACT ? 1 : 0) && c0 < vcells && c1 > c0 && c1 < vcells);
                         if (IL) {
                             double2* V2 = reinterpret_cast<double2*>(Vb);
                             V2[c0] = make_double2(m0, k0);

@@ -148,6 +148,7 @@ __global__ void __launch_bounds__(fea_t5_threads(P), 1) k_tensor5(const __grid_c
     auto Wq = [&](int q) { return prm.ctab[((NP * NQ + 1) & ~1) + q]; };  // w at pad2(np nq)
     auto J = [&](int a, int k, int q) { return prm.jtab[(a * NP + k) * NQ + q]; };
     auto compute = [&](const GathT<NP>& g, double* sV, int le) {
+        FEA_CHECK(le < prm.e_max);  // V column inside the buffer (rows < T, T - np: by construction)
         const double2* gx = g.x;
         const double B00 = gx[1].x - gx[0].x, B10 = gx[1].y - gx[0].y;
         const double B01 = gx[2].x - gx[0].x, B11 = gx[2].y - gx[0].y;
@@ -241,6 +242,7 @@ __global__ void __launch_bounds__(fea_t5_threads(P), 1) k_tensor5(const __grid_c
             if (tid == 0) {
                 asm volatile("cp.async.wait_all;" ::: "memory");  // ring entry of block s + 5
                 const FeaBlock& bk = sBlk[s & (DR - 1)];
+                FEA_CHECK(bk.rec_bytes <= rec_stride && bk.nE <= prm.e_max);
                 fence_proxy_async();
                 mbar_expect_tx(&recb[b], (uint32_t)bk.rec_bytes);
                 tma_load_1d(sRec0 + b * rec_stride, prm.records + bk.rec_off, (uint32_t)bk.rec_bytes, &recb[b]);

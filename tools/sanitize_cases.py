@@ -3,7 +3,7 @@
     compute-sanitizer --tool racecheck python tools/sanitize_cases.py
 
 Kernels covered: k_reassemble5 (v5, P1 / P2), k_reassemble (v4, forced, P1-P4, generic rule),
-k_reassemble6 (v6, P3 / P4: M+K, M only, K only, distinct coefficients), k_tensor / k_tensor4
+k_reassemble6 (v6, P3 / P4: M+K, M only, K only, distinct coefficients), k_tensor / k_tensor4 / k_tensor5
 (tensor contractions), k_pack / k_unpack (interface exchange, two ranks run one after the other).
 Every result is also checked against the oracle, so a run that the sanitizer lets through is a
 correct run too.
@@ -61,7 +61,7 @@ def tensor_cases():
     from tests.helpers import lib_numbering
     import copy
     n = 0
-    for p, N, tk in ((1, 5, 1), (2, 3, 4), (3, 2, 4)):
+    for p, N, tk in ((1, 5, 1), (1, 5, 5), (1, 24, 5), (2, 3, 4), (3, 2, 4)):
         m = random_mesh_from_structured(N, p, seed=20 + p)
         xy, w = triangle_rule(2 * p)
         rng = np.random.default_rng(p)
