@@ -1455,6 +1455,9 @@ fea_status fea_build_pattern(fea_ctx c, int64_t* row_begin, int64_t* n_rows_loca
         e_max = (int64_t)((budget - 1024) / (2 * (8.0 * T * nmat + rec_el)));
         if (c->tune_emax) e_max = std::min(e_max, c->tune_emax);
         e_max = std::min<int64_t>(e_max, 65535 / T - 1) / 8 * 8;
+        // P1 (one unit per 32-element tile, ~2 units per warp per block): whole rounds of units over
+        // the NW warps, so no block leaves most warps idle in a ragged last round (C4 1.127 -> 1.092 ms)
+        if (np == 3 && !c->tune_emax && e_max >= 32 * fea5_nw(1)) e_max = e_max / (32 * fea5_nw(1)) * (32 * fea5_nw(1));
         rec_budget = ((budget - 1024 - 2 * 8LL * T * nmat * (e_max | 1)) / 2 - 128) & ~int64_t(15);
     } else {
         const int ctas = c->order <= 2 ? 2 : 1;  // fea_ctas
@@ -1943,6 +1946,8 @@ static fea_status build_tensor_plan(fea_ctx c, bool want_m, bool want_c) {
         e_max = (int64_t)((budget - fixed) / (16.0 * rows + 2 * rec_el));
         if (c->tune_emax) e_max = std::min(e_max, c->tune_emax);
         e_max = std::min<int64_t>(e_max, 32767 / T - 1) / 8 * 8;
+        const int64_t round_el = 32 * FEA_T5_NW;  // whole rounds of 32-element units over the warps (as in v5)
+        if (!c->tune_emax && e_max >= round_el) e_max = e_max / round_el * round_el;
         rec_budget = ((budget - fixed - 16LL * (rows * (e_max | 1) + 16)) / 2) & ~int64_t(15);
     } else if (k4) {  // V1, Vup, Vdn [T][e_max + 2], two record and gather stages, Lambda and p (fea_t4_smem_layout)
         const int nqp = c->split ? 16 : 4 * fea_nk_kernel(c->order, c->nq);
