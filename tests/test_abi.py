@@ -85,6 +85,23 @@ def test_small_budgets_give_finer_tilings():
     assert np.array_equal(a.get_pattern()[1], b.get_pattern()[1])
 
 
+def test_p1_blocks_in_whole_unit_rounds():
+    """P1 (kernel v5): e_max is a multiple of 32 * 20 warps, so a block's 32-element units fill whole
+    rounds over the warps (DESIGN 7.2); an explicit FEA_TUNE_EMAX is taken as given."""
+    m = random_mesh_from_structured(40, 1, seed=11)
+    a = _plan(m, 1)
+    assert a.stat(7) >= 640 and a.stat(7) % 640 == 0
+    ctx = fea.Context(device=-1)
+    xy, w = triangle_rule(2)
+    ctx.set_element(1, xy, w)
+    ctx.mesh_upload(m.vert_xy, m.elem_vert, m.n_dof, m.elem_dof, reorder=True)
+    ctx.set_tuning(3, 700)
+    ctx.build_pattern()
+    assert ctx.stat(7) == 696  # 700 rounded down to a multiple of 8 only
+    assert ctx.stat(1) <= a.stat(1)
+    assert np.array_equal(a.get_pattern()[1], ctx.get_pattern()[1])
+
+
 def test_planning_errors():
     ctx = fea.Context(device=-1)
     xy, w = triangle_rule(2)
