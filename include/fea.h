@@ -68,7 +68,9 @@ enum {
     FEA_TUNE_KERNEL = 2,        /* kernel generation: 0 = automatic (v5 for p <= 2 with the native
                                    3/6-point rules, v4 otherwise), 4 = force v4                      */
     FEA_TUNE_EMAX = 3,          /* cap on elements per row block (all kernels; 0 = from the
-                                   shared-memory budget)                                             */
+                                   shared-memory budget; the P1 kernels then round it down to whole
+                                   rounds of 32-element units over their warps, an explicit cap is
+                                   taken as given)                                                   */
     FEA_TUNE_EXCHANGE = 5,      /* world > 1: 0 = interface-only exchange of u (default), 1 = full-
                                    vector allgather                                                 */
     FEA_TUNE_OVERLAP = 7,       /* world > 1: 1 = the interior blocks (reading only owned u) assemble
