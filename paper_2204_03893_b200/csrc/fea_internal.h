@@ -378,7 +378,10 @@ int fea_kernel_occupancy5(int order, int do_m, int do_c, int smem_bytes, int* ct
 #ifndef FEA6_NB
 #define FEA6_NB 7
 #endif
-__host__ __device__ constexpr int fea6_nb(int p) { return p == 4 && FEA6_P4_MERGED ? 0 : FEA6_NB; }
+#ifndef FEA6_NB3
+#define FEA6_NB3 FEA6_NB  // P3 phase-B warps (measured: an eighth, 16 warps, C3 1.463 ms vs 1.417 with 7)
+#endif
+__host__ __device__ constexpr int fea6_nb(int p) { return p == 4 ? (FEA6_P4_MERGED ? 0 : FEA6_NB) : FEA6_NB3; }
 __host__ __device__ constexpr bool fea6_supported(int p, int nq) { return p >= 3 && nq == fea_nq_native(p); }
 // P4 A warps: 8 with two row tiles each (default), or (FEA6_P4_NA15) 15 with one row tile each
 // -- four A warps per SM sub-partition keep the FP64 pipe fed while some of them run their
